@@ -1,0 +1,474 @@
+"""Benchmark of the rollout -> advantage -> loss hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--dtype f32|bf16]
+    python bench.py --impl reference ...        # the reference's CPU path on host cores
+
+One step = one pass of the hot path over one batch: the SoA rollout buffer in HBM ->
+assemble_ppo_batch (segmented GAE + counted masks + stats) -> fused PPO loss with all
+coefficients (GRPO configs: group assembly -> fused GRPO loss). Default workload is the
+north star's 256-env OpenVLA-OFT chunk-level PPO config (cfg3). Multi-GPU is weak
+scaling: every rank owns its own 256 envs; ranks exchange only the 64-byte stats record
+and the loss scalars over NCCL.
+
+Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on the
+launching stream, max over ranks. Inputs rotate over R replicas whose total size exceeds
+the 126 MB L2, so every step streams its logits from HBM.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/s through rollout→advantage→PPO/GRPO loss; % HBM roofline; 1/2/4/8 GPU"
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def loss_kernel_bytes(cfg, dtype_bytes, spec, algo):
+    """Algorithmic DRAM bytes of one fused-loss launch: per token the logits
+    row (V * s), token id, old log-prob, and the two written coefficients; per slot the
+    counted mask (PPO) or weight + membership (GRPO); per advantage/value unit the
+    advantage, return, new value and value coefficient."""
+    E, Tc, C, M, V = cfg.num_envs, cfg.num_chunks, cfg.chunk_len, cfg.tokens_per_action, cfg.vocab
+    tokens = E * Tc * C * M
+    slots = E * Tc * C
+    tok_bytes = 1 if V <= 256 else 4
+    b = tokens * (V * dtype_bytes + tok_bytes + 4 + 4 + 4)
+    if algo == "ppo":
+        units = E * Tc if spec[0] == 0 else slots
+        b += slots * 1 + units * (4 + 4 + 4 + 4)
+    else:
+        b += slots * (4 + 1) + E * (4 + 8 + 4)
+    return b
+
+
+def env_steps(cfg):
+    return cfg.num_envs * cfg.num_chunks * cfg.chunk_len
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified chunkrl sources),
+    env-sharded over every host core, on the same config."""
+    if rank != 0:
+        return
+    from paper_2510_06710_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    spec = synth.SPECS[args.config]
+    res = cpu_reference_timing(cfg, spec, args.config, os.cpu_count() or 1,
+                               warmup=args.warmup, steps=args.steps, budget_s=None)
+    line = {"metric": METRIC, "impl": "reference", "value": res["value"], "unit": "env-steps/s",
+            "n_gpus": world, "steps": res["steps"], "warmup": res["warmup"],
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload(args, cfg, world),
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_reference_timing(cfg, spec, name, threads, warmup=1, steps=None, budget_s=10.0):
+    """Times the reference (kind 'reference') or, if it was not built, the oracle port."""
+    from oracle import bindings
+    E, Tc, C = cfg.num_envs, cfg.num_chunks, cfg.chunk_len
+    if bindings.ref_available():
+        # Reference rollout of the same shape (ToyReach env, V-bin x M-token policy with a
+        # minimal trunk: hidden=1, no trunk layers, so the CPU does the logits->loss work).
+        kw = dict(num_envs=E, num_chunks=Tc, chunk_length=C, vocab=cfg.vocab,
+                  tokens_per_action=cfg.tokens_per_action, hidden=1, trunk_layers=0,
+                  value_hidden=4, max_episode_steps=cfg.max_episode_steps, env_seed=4)
+        if cfg.algo == "grpo":
+            kw.update(use_fixed_reset_state_ids=1, group_size=cfg.group_size, auto_reset=0,
+                      deferred_reset=1, ignore_terminations=int(cfg.mode == "fixed"),
+                      num_reset_states=max(64, E // cfg.group_size))
+        sc = bindings.RefScenario(**kw)
+        kind = "reference"
+        if cfg.algo == "ppo":
+            fn = lambda: sc.bench_ppo(spec, threads, 1)[0]  # noqa: E731
+        else:
+            fn = lambda: sc.bench_grpo(spec, threads, 1, cfg.group_size)[0]  # noqa: E731
+        sample = (f"full {name} workload ({E} envs x {Tc * C} steps, V={cfg.vocab}, "
+                  f"M={cfg.tokens_per_action}) through the reference's assemble+loss forward, "
+                  f"env-sharded over {threads} threads, minimal trunk")
+    else:
+        kind = "port"
+        threads = 1
+        orc = bindings.Oracle()
+        from paper_2510_06710_b200 import synth
+        d = synth.episodes_numpy(cfg)
+        rng = __import__("numpy").random.default_rng(0)
+        d["tokens"] = rng.integers(0, cfg.vocab, (E, Tc, C, cfg.tokens_per_action)).astype("int32")
+        d["old_logprob"] = -5.5 + 0.1 * rng.standard_normal(d["tokens"].shape)
+        d["logits"] = 2.0 * rng.standard_normal((*d["tokens"].shape, cfg.vocab))
+        d["V"] = cfg.vocab
+
+        def fn():
+            t0 = time.perf_counter()
+            if cfg.algo == "ppo":
+                st, c, a, r = orc.assemble_ppo(d, spec, 0.99, 0.95)
+                a = orc.normalize_advantages(c, a, spec[0])
+                nv = d["new_value_scalar"] if spec[2] == 0 else d["new_value_vector"]
+                orc.ppo_loss(d, spec, c, a, r, d["logits"], nv, 0.2, 0.5, 0.01)
+            else:
+                st, asm = orc.assemble_grpo(d, spec)
+                orc.grpo_loss(d, spec[1], asm, d["logits"], 0.2)
+            return time.perf_counter() - t0
+        sample = f"full {name} workload through the oracle port (single thread)"
+    for _ in range(max(0, warmup)):
+        fn()
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        s = fn()
+        if s < 0:
+            raise RuntimeError("reference benchmark failed")
+        times.append(s)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and time.perf_counter() - t_start >= budget_s:
+            break
+    per = sum(times) / len(times)
+    return {"value": env_steps(cfg) / per, "unit": "env-steps/s", "cores": threads, "kind": kind,
+            "sample": sample + f"; {len(times)} timed iterations", "steps": len(times),
+            "warmup": warmup, "ms_per_step": per * 1e3}
+
+
+def workload(args, cfg, world):
+    from paper_2510_06710_b200 import synth
+    a, l, v = synth.SPECS[args.config]
+    lv = ["chunk", "action", "token"]
+    names = {"cfg1": "PPO+GAE 64 envs x 80 steps, token-level logprob (CPU oracle config)",
+             "cfg2": "GRPO 256 envs, group 8, success-rate filter, action-level logprob",
+             "cfg3": "OpenVLA-OFT chunk-level PPO, 256 envs x 80 steps, chunk 8, partial reset",
+             "cfg4": "LIBERO-scale GRPO 512 envs x 512 steps, fixed length, valid-action masks"}
+    return {"workload": f"{args.config}: {names[args.config]}", "envs_per_gpu": cfg.num_envs,
+            "steps_per_env": cfg.num_chunks * cfg.chunk_len, "chunk": cfg.chunk_len,
+            "action_dim": cfg.tokens_per_action, "bins": cfg.vocab,
+            "granularity": {"advantage": lv[a], "logprob": lv[l], "value": lv[v]},
+            "global_envs": cfg.num_envs * world, "parallelism": f"env-sharded x{world}",
+            "logits_dtype": args.dtype}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2510_06710_b200 as ck
+    from paper_2510_06710_b200 import _lib, optim, synth
+    from paper_2510_06710_b200.core import (EpisodeTable, GaeParams, GranularitySpec,
+                                            GrpoAssemblyOptions, GrpoParams, Level,
+                                            PolicyOutputs, PpoParams, RolloutBuffer)
+    ck.lib()
+
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2510_06710_b200 import dist as ckdist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = ckdist.Comm.from_torch()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+
+    cfg = synth.CONFIGS[args.config]
+    a, l, v = synth.SPECS[args.config]
+    spec = GranularitySpec(Level(a), Level(l), Level(v))
+    ldtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    dbytes = 2 if args.dtype == "bf16" else 4
+
+    # --- inputs: R replicas (rank-distinct envs) so the working set exceeds L2
+    per_rep = env_steps(cfg) * cfg.tokens_per_action * cfg.vocab * dbytes
+    R = 1 if args.profile else max(2, math.ceil(3 * L2_BYTES / per_rep))
+    reps = []
+    for r in range(R):
+        c = synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + 101 * r})
+        d = synth.episodes_numpy(c, env_offset=rank * cfg.num_envs)
+        logits, tokens, old = synth.token_tensors(c, dev, ldtype, env_offset=rank * cfg.num_envs)
+        d["tokens"], d["old_logprob"] = tokens, old
+        boot = d["boot_scalar"] if a == 0 else d["boot_vector0"]
+        ro = RolloutBuffer.from_arrays(d, boot, cfg.vocab, dev)
+        nv = d["new_value_scalar"] if v == 0 else d["new_value_vector"]
+        pol = PolicyOutputs(logits, torch.tensor(nv, dtype=torch.float32, device=dev))
+        ept = EpisodeTable.from_arrays(d, dev) if cfg.algo == "grpo" else None
+        reps.append((ro, pol, ept, d))
+    if cfg.algo == "ppo":
+        step = optim.PpoStep(reps[0][0], GaeParams(0.99, 0.95), spec,
+                             PpoParams(0.2, 0.5, 0.01, True), comm=comm)
+        run = lambda i: step(reps[i % R][0], reps[i % R][1])  # noqa: E731
+        launches_per_step = 2
+    else:
+        opts = GrpoAssemblyOptions(spec)
+        step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
+        run = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
+        launches_per_step = 3
+    if world > 1:
+        launches_per_step += 1  # finalize after the loss-scalar all-reduce
+
+    stream = torch.cuda.current_stream()
+    for i in range(max(3, args.warmup)):
+        run(i)
+    torch.cuda.synchronize()
+    diag0 = step.diagnostics()
+
+    # --- optional CUDA graph of one step per replica (removes host launch overhead)
+    graph = None
+    if not args.no_graph and world == 1 and not args.profile:
+        try:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                run(0)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g):
+                for i in range(R):
+                    run(i)
+            graph = g
+        except Exception as e:  # eager launches are the fallback, still the CUDA path
+            print(f"# graph capture failed ({e}); timing eager launches", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+
+    K = args.steps
+    if graph is not None:
+        K = max(R, (K // R) * R)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        if graph is not None:
+            for _ in range(K // R):
+                graph.replay()
+        else:
+            for i in range(K):
+                run(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1) / K
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * env_steps(cfg) / (ms * 1e-3)
+    diag = step.diagnostics()
+
+    # --- dominant kernel (fused loss) timed alone with events on its stream
+    ws = step.ws
+    kms = []
+    for i in range(min(K, 50)):
+        ro, pol, ept, _ = reps[i % R]
+        if cfg.algo == "ppo":
+            from paper_2510_06710_b200 import advantage
+            from paper_2510_06710_b200.core import PpoAssemblyOptions
+            advantage.assemble_ppo_batch(ro, PpoAssemblyOptions(GaeParams(0.99, 0.95), spec),
+                                         out=step.batch)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            optim.ppo_loss(ro, pol, step.batch, PpoParams(0.2, 0.5, 0.01, True), step.outputs,
+                           diag=step.diag)
+            e1.record(stream)
+        else:
+            from paper_2510_06710_b200 import advantage
+            advantage.assemble_grpo_batch(ro, ept, GrpoAssemblyOptions(spec), out=step.batch)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            optim.grpo_loss(ro, pol, step.batch, GrpoParams(0.2), step.outputs, diag=step.diag)
+            e1.record(stream)
+        kms.append((e0, e1))
+    torch.cuda.synchronize()
+    kernel_ms = sum(e0.elapsed_time(e1) for e0, e1 in kms) / len(kms)
+    kbytes = loss_kernel_bytes(cfg, dbytes, (a, l, v), cfg.algo)
+    peak, peak_kind = peaks()
+    achieved = kbytes / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{args.config}_{args.dtype}")
+
+    # --- e2e through the public API with host (pinned) buffers
+    e2e = None
+    if not args.profile:
+        e2e = e2e_timing(args, cfg, reps[0], step, run, R, dev, world)
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and not args.profile:
+        try:
+            cpu = cpu_reference_timing(cfg, (a, l, v), args.config, os.cpu_count() or 1,
+                                       warmup=1, budget_s=args.cpu_seconds)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # report, never hide
+            cpu = {"value": None, "unit": "env-steps/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {**workload(args, cfg, world),
+                   "l2": f"inputs rotate over {R} replicas ({R * per_rep / 2**20:.0f} MiB of logits > 126 MB L2)",
+                   "cuda_graph": graph is not None},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "tile_kernel (fused token + loss)", "kernel_ms": kernel_ms,
+                     "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
+                     "step_frac": (kbytes / (ms * 1e-3) / 1e9) / peak},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": K * launches_per_step,
+        "clocks": clk.summary(),
+        "diagnostics": {k: diag[k] for k in ("loss", "surrogate", "value_loss", "entropy",
+                                              "clip_frac", "approx_kl", "units")},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def e2e_timing(args, cfg, rep, step, run, R, dev, world):
+    """Same metric through the public API with host buffers: every step copies that step's
+    inputs host->device from pinned memory, runs the step and reads the loss back."""
+    import torch
+    ro, pol, ept, d = rep
+    names = ["tokens", "old_logprob", "reward", "flags", "episode_id", "value_scalar",
+             "value_vector", "bootstrap"]
+    dev_t = [getattr(ro, n) for n in names] + [pol.logits, pol.values]
+    if ept is not None:
+        dev_t += [getattr(ept, n) for n in ("env_id", "episode_id", "start_step", "length",
+                                            "total_reward", "first_success", "complete",
+                                            "task_id", "reset_state_id")]
+    host_t = [t.detach().cpu().pin_memory() for t in dev_t]
+    h2d = sum(t.numel() * t.element_size() for t in host_t)
+    out = torch.empty(8, dtype=torch.float64).pin_memory()
+    d2h = out.numel() * out.element_size()
+    stream = torch.cuda.current_stream()
+    n = max(5, min(args.steps, 30))
+
+    def one():
+        for hd, dd in zip(host_t, dev_t):
+            dd.copy_(hd, non_blocking=True)
+        run(0)
+        out.copy_(step.diag, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": world * env_steps(cfg) / (ms * 1e-3), "unit": "env-steps/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,283 @@
+/*
+ * ckrl.h — C ABI of the B200-native rollout -> advantage -> loss hot path.
+ *
+ * Drop-in boundary for the chunkrl reference (/root/reference/proj/src/chunkrl).
+ * The reference exposes plain C++20 free functions over an AoS TrajectorySlab;
+ * this ABI exposes the same operators over a caller-owned structure-of-arrays
+ * slab in device memory (HBM), with explicit cudaStream_t, caller-provided
+ * workspace (no allocation on the hot call) and status codes 1:1 with the
+ * reference's exception types. Each entry point cites the reference interface
+ * it replaces. There is no CPU fallback: every compute entry point launches
+ * sm_100a kernels and fails with CKRL_ERR_CUDA when no device is usable.
+ *
+ * SoA slab layout (row-major, innermost last):
+ *   record r = e*Tc + t      slot s = r*C + j      token k = s*M + m
+ *   tokens       [E][Tc][C][M]      u8 (V <= 256) or i32
+ *   old_logprob  [E][Tc][C][M]      f32   (TokenLogprobs, core/types.hpp:29-38)
+ *   reward       [E][Tc][C]         f32
+ *   flags        [E][Tc][C]         u8    bit0 terminated, bit1 truncated, bit2 valid
+ *   episode_id   [E][Tc][C]         i32   uid & 0xffffffff (envsim/vec_env.cpp:14-16), -1 frozen
+ *   value_scalar [E][Tc]            f32   StepRecord::value_scalar
+ *   value_vector [E][Tc][C]         f32   StepRecord::value_vector
+ *   bootstrap    [E][Tc][C]         f32   V_snapshot(post_obs[slot]) of the advantage-level
+ *                                         head (scalar at chunk level, vector[0] at action
+ *                                         level; assembler.cpp:114-118, 148-152)
+ *   logits       [E][Tc][C][M][V]   f32 or bf16, current policy (forward_logits)
+ *   new values   [E][Tc] (chunk value level) or [E][Tc][C] (action value level), f32
+ */
+#ifndef CKRL_H
+#define CKRL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct CUstream_st* ckrl_stream_t; /* == cudaStream_t */
+
+/* Status codes, 1:1 with chunkrl/core/errors.hpp:9-48 (+ CUDA / argument errors). */
+typedef enum {
+  CKRL_OK = 0,
+  CKRL_ERR_UNSUPPORTED_COMBINATION = 1,  /* UnsupportedCombination */
+  CKRL_ERR_GRANULARITY_ORDER = 2,        /* GranularityOrderViolation */
+  CKRL_ERR_LENGTH_MISMATCH = 3,          /* LengthMismatch */
+  CKRL_ERR_BAD_RESET_ID = 4,             /* BadResetId */
+  CKRL_ERR_HEAD_MISMATCH = 5,            /* HeadMismatch */
+  CKRL_ERR_NON_FINITE = 6,               /* NonFinite */
+  CKRL_ERR_DEGENERATE_GROUP = 7,         /* DegenerateGroup */
+  CKRL_ERR_SKIP_UPDATE = 8,              /* SkipUpdate */
+  CKRL_ERR_INVALID_PLAN = 9,             /* InvalidPlan */
+  CKRL_ERR_MEMORY_OVERFLOW = 10,         /* MemoryOverflow */
+  CKRL_ERR_EMPTY_TRACE = 11,             /* EmptyTrace */
+  CKRL_ERR_CONFIG = 12,                  /* ConfigError */
+  CKRL_ERR_GENERIC = 13,                 /* chunkrl::Error */
+  CKRL_ERR_CUDA = 14,                    /* device / launch failure */
+  CKRL_ERR_INVALID_ARGUMENT = 15,        /* null pointer, bad dims, workspace too small */
+  CKRL_ERR_NCCL = 16
+} ckrl_status;
+
+/* core/granularity.hpp:8 enum class Level { Chunk, Action, Token } */
+enum { CKRL_LEVEL_CHUNK = 0, CKRL_LEVEL_ACTION = 1, CKRL_LEVEL_TOKEN = 2 };
+enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3 };
+enum { CKRL_FLAG_TERMINATED = 1, CKRL_FLAG_TRUNCATED = 2, CKRL_FLAG_VALID = 4 };
+
+/* Diagnostics slots written to device memory (optim/losses.hpp:31-39 LossDiagnostics). */
+enum {
+  CKRL_DIAG_LOSS = 0, CKRL_DIAG_SURROGATE, CKRL_DIAG_VALUE_LOSS, CKRL_DIAG_ENTROPY,
+  CKRL_DIAG_CLIP_FRAC, CKRL_DIAG_APPROX_KL, CKRL_DIAG_UNITS, CKRL_DIAG_STATUS,
+  CKRL_DIAG_COUNT = 8
+};
+
+typedef struct {
+  int32_t advantage_level, logprob_level, value_level;
+} ckrl_granularity; /* GranularitySpec, core/granularity.hpp:21-27 */
+
+typedef struct {
+  double gamma, lambda;
+} ckrl_gae_params; /* advantage/gae.hpp:8-13 */
+
+typedef struct {
+  double clip_eps, value_loss_coef, entropy_coef;
+  int32_t advantage_normalization; /* applied once before the loss (optim/update.cpp:66-67) */
+} ckrl_ppo_params; /* optim/losses.hpp:12-21 (optimizer fields are out of scope) */
+
+typedef struct {
+  double clip_eps;
+} ckrl_grpo_params; /* optim/losses.hpp:23-29 */
+
+typedef struct {
+  double eps_std;
+  int32_t apply_filter;
+  double filter_lower, filter_upper;
+  int32_t length_normalized;
+  int32_t min_group_size;
+} ckrl_grpo_options; /* advantage/assembler.hpp:76-83 */
+
+/* The SoA rollout buffer (replaces TrajectorySlab, core/types.hpp:89-104). Device pointers. */
+typedef struct {
+  int32_t num_envs, num_chunks, chunk_len, tokens_per_action, vocab;
+  int32_t token_dtype; /* CKRL_DTYPE_U8 | CKRL_DTYPE_I32 */
+  const void* tokens;
+  const float* old_logprob;
+  const float* reward;
+  const uint8_t* flags;
+  const int32_t* episode_id;
+  const float* value_scalar;
+  const float* value_vector;
+  const float* bootstrap;
+} ckrl_rollout;
+
+/* Current-policy outputs consumed by the loss (what ppo_loss recomputes through
+ * PolicyNet::evaluate_chunk / value, losses.cpp:115, 196). Device pointers. */
+typedef struct {
+  int32_t logits_dtype; /* CKRL_DTYPE_F32 | CKRL_DTYPE_BF16 */
+  const void* logits;
+  const float* values;  /* new values at the value level; may be NULL if value_loss_coef == 0 */
+} ckrl_policy_outputs;
+
+/* Episode table (EpisodeInfo, core/types.hpp:72-85) as SoA, device pointers. */
+typedef struct {
+  int32_t count;
+  const int32_t* env_id;
+  const int32_t* episode_id;
+  const int32_t* start_step;
+  const int32_t* length;
+  const double* total_reward;
+  const int32_t* first_success;
+  const uint8_t* complete;
+  const int32_t* task_id;
+  const int32_t* reset_state_id;
+} ckrl_episodes;
+
+/* PpoBatch (advantage/assembler.hpp:16-37) as SoA, device pointers (outputs of assembly). */
+typedef struct {
+  uint8_t* counted;   /* [E][Tc][C] */
+  float* advantages;  /* [E][Tc] (chunk) or [E][Tc][C] (action); raw GAE */
+  float* returns;     /* same shape */
+} ckrl_ppo_batch;
+
+/* GrpoBatch (advantage/assembler.hpp:40-62) as SoA: each env owns at most one retained
+ * trajectory (only complete episodes starting at step 0 are grouped). Device pointers. */
+typedef struct {
+  int32_t* env_group;       /* [E] retained-group ordinal in GroupKey order, -1 none */
+  int32_t* env_member;      /* [E] member index inside its group */
+  int32_t* env_episode;     /* [E] episode_id of the trajectory */
+  double* env_advantage;    /* [E] group-relative advantage */
+  int32_t* env_group_size;  /* [E] trajectories in the group */
+  float* slot_weight;       /* [E][Tc][C] per-step weight (0 outside the trajectory / masked) */
+  uint8_t* slot_member;     /* [E][Tc][C] slot belongs to the trajectory */
+  int32_t* group_counts;    /* [2] groups_total, groups_retained (device) */
+} ckrl_grpo_batch;
+
+/* Optional per-token / per-unit outputs of the loss (device, may be NULL each). */
+typedef struct {
+  float* coeff_logprob;  /* [E][Tc][C][M]  dLoss/dlogprob per position (accumulate_chunk_gradient) */
+  float* coeff_entropy;  /* [E][Tc][C][M]  dLoss/dentropy per position */
+  float* coeff_value;    /* value level shape, dLoss/dV */
+  float* token_logprob;  /* [E][Tc][C][M]  new log-probs (evaluate_chunk) */
+  float* token_entropy;  /* [E][Tc][C][M]  new entropies */
+} ckrl_loss_outputs;
+
+/* ---- host-only helpers (no device work) ---------------------------------------------- */
+const char* ckrl_version(void);
+const char* ckrl_status_string(int32_t status);
+const char* ckrl_last_error(void); /* thread-local message of the last failing call */
+
+/* validate_granularity (core/granularity.cpp:47-60). */
+int32_t ckrl_validate_granularity(const ckrl_granularity* spec);
+
+/* Workspace bytes for a slab of this shape (whole step incl. cross-rank stats for
+ * `world` ranks). Caller allocates device memory of at least this size once. */
+size_t ckrl_workspace_bytes(int32_t num_envs, int32_t num_chunks, int32_t chunk_len,
+                            int32_t tokens_per_action, int32_t world);
+
+/* Zero the workspace once after allocating it (its last-CTA counters self-reset). */
+int32_t ckrl_workspace_init(void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
+
+/* Merge `world` per-rank whitening/normaliser stats records (host memory, the layout
+ * ckrl_stats_record_bytes() describes) in rank order. Exposed for the multi-rank
+ * host tests; the device path merges the same records inside the loss kernel. */
+size_t ckrl_stats_record_bytes(void);
+int32_t ckrl_merge_stats_host(const void* records, int32_t world, double* out_mean,
+                              double* out_denom, int64_t* out_counts /* n_adv,n_val,n_pos */);
+
+/* ---- (c) advantage -------------------------------------------------------------------- */
+
+/* compute_gae (advantage/gae.cpp:7-37) over `num_seqs` independent flat unit sequences
+ * packed back to back; seq_offsets[num_seqs+1] (device) delimits them. flags use the
+ * CKRL_FLAG_* bits (valid ignored). Outputs in fp64 (the reference's precision). */
+int32_t ckrl_compute_gae(int32_t num_seqs, const int32_t* seq_offsets, const double* rewards,
+                         const double* values, const double* bootstrap, const uint8_t* flags,
+                         const ckrl_gae_params* params, double* advantages, double* returns,
+                         ckrl_stream_t stream);
+
+/* assemble_ppo_batch (advantage/assembler.cpp:78-195): segmentation, chunk/action units,
+ * counted masks, bootstraps, GAE (warp-segmented reverse scan), plus the rank-local
+ * normaliser / whitening stats record left in `workspace`. */
+int32_t ckrl_assemble_ppo_batch(const ckrl_rollout* rollout, const ckrl_gae_params* gae,
+                                const ckrl_granularity* spec, ckrl_ppo_batch* batch,
+                                void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
+
+/* normalize_advantages (optim/update.cpp:14-45), materialised in place over the counted
+ * units, using the stats left in `workspace` by ckrl_assemble_ppo_batch. */
+int32_t ckrl_normalize_advantages(const ckrl_rollout* rollout, const ckrl_granularity* spec,
+                                  ckrl_ppo_batch* batch, void* workspace,
+                                  size_t workspace_bytes, ckrl_stream_t stream);
+
+/* assemble_grpo_batch (advantage/assembler.cpp:197-267): eligibility, GroupKey-ordered
+ * grouping (std::map order), min size, strict success-rate filter, group-relative
+ * advantages, valid-action masks and length-normalised per-step weights. */
+int32_t ckrl_assemble_grpo_batch(const ckrl_rollout* rollout, const ckrl_episodes* episodes,
+                                 const ckrl_granularity* spec, const ckrl_grpo_options* options,
+                                 ckrl_grpo_batch* batch, void* workspace, size_t workspace_bytes,
+                                 ckrl_stream_t stream);
+
+/* ---- (b) fused action-token kernel ---------------------------------------------------- */
+
+/* PolicyNet::evaluate_chunk (policy/policy_net.cpp:333-357) + aggregate_logprob
+ * (core/granularity.cpp:83-113): per-token log-prob and entropy from logits rows, and the
+ * action / chunk aggregates in canonical order. Any output may be NULL. */
+int32_t ckrl_token_stats(int64_t num_chunks, int32_t chunk_len, int32_t tokens_per_action,
+                         int32_t vocab, int32_t logits_dtype, const void* logits,
+                         int32_t token_dtype, const void* tokens, float* token_logprob,
+                         float* token_entropy, double* action_logprob, double* chunk_logprob,
+                         ckrl_stream_t stream);
+
+/* ---- (d) losses ----------------------------------------------------------------------- */
+
+/* ppo_loss (optim/losses.cpp:62-232) over every record (full batch), fused with the token
+ * kernel: one pass over the logits computes log-softmax, gather, entropy, the clipped
+ * surrogate at logprob granularity, value and entropy terms and all coefficients.
+ * Diagnostics go to `diag_device` (double[CKRL_DIAG_COUNT], device) without host sync.
+ * Requires the stats record produced by ckrl_assemble_ppo_batch in `workspace`
+ * (whitening applied on the fly when params->advantage_normalization). */
+int32_t ckrl_ppo_loss(const ckrl_rollout* rollout, const ckrl_ppo_batch* batch,
+                      const ckrl_policy_outputs* policy, const ckrl_granularity* spec,
+                      const ckrl_ppo_params* params, ckrl_loss_outputs* outputs,
+                      double* diag_device, void* workspace, size_t workspace_bytes,
+                      ckrl_stream_t stream);
+
+/* grpo_loss (optim/losses.cpp:234-331) over every retained group. */
+int32_t ckrl_grpo_loss(const ckrl_rollout* rollout, const ckrl_grpo_batch* batch,
+                       const ckrl_policy_outputs* policy, const ckrl_granularity* spec,
+                       const ckrl_grpo_params* params, ckrl_loss_outputs* outputs,
+                       double* diag_device, void* workspace, size_t workspace_bytes,
+                       ckrl_stream_t stream);
+
+/* Whole step (the measured hot path): assemble -> [stats allgather over `comm`] -> fused
+ * loss. comm may be NULL (single rank). */
+typedef struct ckrl_comm ckrl_comm;
+int32_t ckrl_ppo_step(const ckrl_rollout* rollout, const ckrl_policy_outputs* policy,
+                      const ckrl_gae_params* gae, const ckrl_granularity* spec,
+                      const ckrl_ppo_params* params, ckrl_ppo_batch* batch,
+                      ckrl_loss_outputs* outputs, double* diag_device, void* workspace,
+                      size_t workspace_bytes, ckrl_comm* comm, ckrl_stream_t stream);
+int32_t ckrl_grpo_step(const ckrl_rollout* rollout, const ckrl_episodes* episodes,
+                       const ckrl_policy_outputs* policy, const ckrl_granularity* spec,
+                       const ckrl_grpo_options* options, const ckrl_grpo_params* params,
+                       ckrl_grpo_batch* batch, ckrl_loss_outputs* outputs, double* diag_device,
+                       void* workspace, size_t workspace_bytes, ckrl_comm* comm,
+                       ckrl_stream_t stream);
+
+/* Copy the device diagnostics to the host (synchronises `stream`) and map the device
+ * status word to the reference's exceptions: SkipUpdate (no retained groups),
+ * DegenerateGroup, NonFinite (losses.cpp:229-230, 326-327). */
+int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream);
+
+/* ---- multi-GPU (NCCL over NVLink): stats + loss scalars only -------------------------- */
+int32_t ckrl_comm_unique_id(void* out_id /* 128 bytes */);
+int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out);
+int32_t ckrl_comm_destroy(ckrl_comm* comm);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKRL_H */

@@ -1,0 +1,144 @@
+"""ctypes binding of include/ckrl.h (the C ABI of libckrl.so).
+
+The structures below mirror ckrl.h field for field. Loading fails loudly when the
+library is missing: there is no Python / CPU fallback for the hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libckrl.so")
+
+LEVEL_CHUNK, LEVEL_ACTION, LEVEL_TOKEN = 0, 1, 2
+DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32 = 0, 1, 2, 3
+FLAG_TERMINATED, FLAG_TRUNCATED, FLAG_VALID = 1, 2, 4
+DIAG_COUNT = 8
+DIAG_NAMES = ("loss", "surrogate", "value_loss", "entropy", "clip_frac", "approx_kl", "units",
+              "status")
+
+vp = C.c_void_p
+
+
+class Granularity(C.Structure):
+    _fields_ = [("advantage_level", C.c_int32), ("logprob_level", C.c_int32),
+                ("value_level", C.c_int32)]
+
+
+class GaeParams(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("lambda_", C.c_double)]
+
+
+class PpoParams(C.Structure):
+    _fields_ = [("clip_eps", C.c_double), ("value_loss_coef", C.c_double),
+                ("entropy_coef", C.c_double), ("advantage_normalization", C.c_int32)]
+
+
+class GrpoParams(C.Structure):
+    _fields_ = [("clip_eps", C.c_double)]
+
+
+class GrpoOptions(C.Structure):
+    _fields_ = [("eps_std", C.c_double), ("apply_filter", C.c_int32),
+                ("filter_lower", C.c_double), ("filter_upper", C.c_double),
+                ("length_normalized", C.c_int32), ("min_group_size", C.c_int32)]
+
+
+class Rollout(C.Structure):
+    _fields_ = [("num_envs", C.c_int32), ("num_chunks", C.c_int32), ("chunk_len", C.c_int32),
+                ("tokens_per_action", C.c_int32), ("vocab", C.c_int32),
+                ("token_dtype", C.c_int32), ("tokens", vp), ("old_logprob", vp),
+                ("reward", vp), ("flags", vp), ("episode_id", vp), ("value_scalar", vp),
+                ("value_vector", vp), ("bootstrap", vp)]
+
+
+class PolicyOutputs(C.Structure):
+    _fields_ = [("logits_dtype", C.c_int32), ("logits", vp), ("values", vp)]
+
+
+class Episodes(C.Structure):
+    _fields_ = [("count", C.c_int32), ("env_id", vp), ("episode_id", vp), ("start_step", vp),
+                ("length", vp), ("total_reward", vp), ("first_success", vp), ("complete", vp),
+                ("task_id", vp), ("reset_state_id", vp)]
+
+
+class PpoBatchC(C.Structure):
+    _fields_ = [("counted", vp), ("advantages", vp), ("returns", vp)]
+
+
+class GrpoBatchC(C.Structure):
+    _fields_ = [("env_group", vp), ("env_member", vp), ("env_episode", vp),
+                ("env_advantage", vp), ("env_group_size", vp), ("slot_weight", vp),
+                ("slot_member", vp), ("group_counts", vp)]
+
+
+class LossOutputs(C.Structure):
+    _fields_ = [("coeff_logprob", vp), ("coeff_entropy", vp), ("coeff_value", vp),
+                ("token_logprob", vp), ("token_entropy", vp)]
+
+
+# (name, restype, argtypes) for every exported symbol of ckrl.h
+P = C.POINTER
+SIGNATURES = {
+    "ckrl_version": (C.c_char_p, []),
+    "ckrl_status_string": (C.c_char_p, [C.c_int32]),
+    "ckrl_last_error": (C.c_char_p, []),
+    "ckrl_validate_granularity": (C.c_int32, [P(Granularity)]),
+    "ckrl_workspace_bytes": (C.c_size_t, [C.c_int32] * 5),
+    "ckrl_workspace_init": (C.c_int32, [vp, C.c_size_t, vp]),
+    "ckrl_stats_record_bytes": (C.c_size_t, []),
+    "ckrl_merge_stats_host": (C.c_int32, [vp, C.c_int32, P(C.c_double), P(C.c_double),
+                                          P(C.c_int64)]),
+    "ckrl_compute_gae": (C.c_int32, [C.c_int32, vp, vp, vp, vp, vp, P(GaeParams), vp, vp, vp]),
+    "ckrl_assemble_ppo_batch": (C.c_int32, [P(Rollout), P(GaeParams), P(Granularity),
+                                            P(PpoBatchC), vp, C.c_size_t, vp]),
+    "ckrl_normalize_advantages": (C.c_int32, [P(Rollout), P(Granularity), P(PpoBatchC), vp,
+                                              C.c_size_t, vp]),
+    "ckrl_assemble_grpo_batch": (C.c_int32, [P(Rollout), P(Episodes), P(Granularity),
+                                             P(GrpoOptions), P(GrpoBatchC), vp, C.c_size_t, vp]),
+    "ckrl_token_stats": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
+                                     C.c_int32, vp, vp, vp, vp, vp, vp]),
+    "ckrl_ppo_loss": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
+                                  P(PpoParams), P(LossOutputs), vp, vp, C.c_size_t, vp]),
+    "ckrl_grpo_loss": (C.c_int32, [P(Rollout), P(GrpoBatchC), P(PolicyOutputs), P(Granularity),
+                                   P(GrpoParams), P(LossOutputs), vp, vp, C.c_size_t, vp]),
+    "ckrl_ppo_step": (C.c_int32, [P(Rollout), P(PolicyOutputs), P(GaeParams), P(Granularity),
+                                  P(PpoParams), P(PpoBatchC), P(LossOutputs), vp, vp,
+                                  C.c_size_t, vp, vp]),
+    "ckrl_grpo_step": (C.c_int32, [P(Rollout), P(Episodes), P(PolicyOutputs), P(Granularity),
+                                   P(GrpoOptions), P(GrpoParams), P(GrpoBatchC),
+                                   P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
+    "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
+    "ckrl_comm_unique_id": (C.c_int32, [vp]),
+    "ckrl_comm_create": (C.c_int32, [C.c_int32, C.c_int32, vp, P(vp)]),
+    "ckrl_comm_destroy": (C.c_int32, [vp]),
+}
+
+_LIB = None
+
+
+def lib():
+    """Load libckrl.so (once). Raises if the CUDA extension was not built."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+        h = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = h
+    return _LIB
+
+
+def check(status: int):
+    """Map a ckrl status code to the reference's exception types (core/errors.hpp)."""
+    if status != 0:
+        msg = lib().ckrl_last_error().decode(errors="replace")
+        raise errors.from_status(status, msg)

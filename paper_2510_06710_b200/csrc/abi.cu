@@ -1,0 +1,577 @@
+// C-ABI layer (include/ckrl.h): argument validation with the reference's error
+// taxonomy, workspace carve-up, kernel dispatch and the NCCL stats exchange.
+// No entry point allocates device memory or synchronises the stream, except
+// ckrl_read_diagnostics (which returns host scalars) and the communicator setup.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace ckrl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int32_t fail(int32_t code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CKRL_CUDA(x)                                                                      \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) return fail(CKRL_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKRL_REQUIRE(cond, code, msg) \
+  do {                                \
+    if (!(cond)) return fail((code), (msg)); \
+  } while (0)
+
+int32_t check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(CKRL_ERR_CUDA, "no CUDA device: the ckrl hot path has no CPU fallback");
+  return CKRL_OK;
+}
+
+int32_t check_rollout(const ckrl_rollout* ro, bool need_values) {
+  CKRL_REQUIRE(ro != nullptr, CKRL_ERR_INVALID_ARGUMENT, "rollout is null");
+  CKRL_REQUIRE(ro->num_envs >= 0 && ro->num_chunks >= 0 && ro->chunk_len >= 1 &&
+                   ro->tokens_per_action >= 1 && ro->vocab >= 1,
+               CKRL_ERR_LENGTH_MISMATCH, "rollout dimensions must be positive");
+  CKRL_REQUIRE(ro->token_dtype == CKRL_DTYPE_U8 || ro->token_dtype == CKRL_DTYPE_I32,
+               CKRL_ERR_INVALID_ARGUMENT, "token dtype must be u8 or i32");
+  CKRL_REQUIRE(ro->token_dtype == CKRL_DTYPE_I32 || ro->vocab <= 256, CKRL_ERR_INVALID_ARGUMENT,
+               "u8 tokens require vocab <= 256");
+  CKRL_REQUIRE((int64_t)ro->chunk_len * ro->tokens_per_action <= 8192, CKRL_ERR_INVALID_ARGUMENT,
+               "C*M must be <= 8192");
+  const int64_t n = (int64_t)ro->num_envs * ro->num_chunks;
+  if (n > 0) {
+    CKRL_REQUIRE(ro->flags && ro->episode_id && ro->reward, CKRL_ERR_INVALID_ARGUMENT,
+                 "rollout flags / episode_id / reward are required");
+    if (need_values)
+      CKRL_REQUIRE(ro->value_scalar && ro->value_vector && ro->bootstrap,
+                   CKRL_ERR_INVALID_ARGUMENT, "rollout values / bootstrap are required");
+  }
+  return CKRL_OK;
+}
+
+int32_t check_ws(void* ws, size_t bytes, int E, int world) {
+  CKRL_REQUIRE(ws != nullptr, CKRL_ERR_INVALID_ARGUMENT, "workspace is null");
+  size_t need = ws_layout(E, world).total;
+  if (bytes < need)
+    return fail(CKRL_ERR_INVALID_ARGUMENT, "workspace too small: need " + std::to_string(need) +
+                                               " bytes, got " + std::to_string(bytes));
+  return CKRL_OK;
+}
+
+int32_t validate(const ckrl_granularity* g) {
+  CKRL_REQUIRE(g != nullptr, CKRL_ERR_INVALID_ARGUMENT, "granularity is null");
+  auto ok = [](int l) { return l >= CKRL_LEVEL_CHUNK && l <= CKRL_LEVEL_TOKEN; };
+  CKRL_REQUIRE(ok(g->advantage_level) && ok(g->logprob_level) && ok(g->value_level),
+               CKRL_ERR_CONFIG, "unknown granularity level");
+  // core/granularity.cpp:47-60
+  if (g->advantage_level == CKRL_LEVEL_TOKEN)
+    return fail(CKRL_ERR_UNSUPPORTED_COMBINATION, "advantage level must be chunk_level or action_level");
+  if (g->value_level == CKRL_LEVEL_TOKEN)
+    return fail(CKRL_ERR_UNSUPPORTED_COMBINATION, "value level must be chunk_level or action_level");
+  if (g->logprob_level < g->advantage_level)
+    return fail(CKRL_ERR_UNSUPPORTED_COMBINATION,
+                "unsupported combination: logprob level coarser than advantage level");
+  return CKRL_OK;
+}
+
+LossArgs base_args(const ckrl_rollout* ro, const ckrl_policy_outputs* po, char* ws, int world) {
+  LossArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.E = ro->num_envs;
+  a.Tc = ro->num_chunks;
+  a.C = ro->chunk_len;
+  a.M = ro->tokens_per_action;
+  a.V = ro->vocab;
+  a.n_rec = (int64_t)ro->num_envs * ro->num_chunks;
+  a.logits_bf16 = po->logits_dtype == CKRL_DTYPE_BF16;
+  a.tok_i32 = ro->token_dtype == CKRL_DTYPE_I32;
+  a.logits = po->logits;
+  a.tokens = ro->tokens;
+  a.old_lp = ro->old_logprob;
+  a.ws = ws;
+  a.L = ws_layout(ro->num_envs, world);
+  a.world = world;
+  return a;
+}
+
+void set_outputs(LossArgs& a, const ckrl_loss_outputs* o) {
+  if (!o) return;
+  a.coeff_lp = o->coeff_logprob;
+  a.coeff_ent = o->coeff_entropy;
+  a.coeff_val = o->coeff_value;
+  a.tok_lp = o->token_logprob;
+  a.tok_ent = o->token_entropy;
+  a.all_rows = (o->token_logprob || o->token_entropy) ? 1 : 0;
+}
+
+int32_t check_policy(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
+  CKRL_REQUIRE(po != nullptr, CKRL_ERR_INVALID_ARGUMENT, "policy outputs are null");
+  CKRL_REQUIRE(po->logits_dtype == CKRL_DTYPE_F32 || po->logits_dtype == CKRL_DTYPE_BF16,
+               CKRL_ERR_INVALID_ARGUMENT, "logits dtype must be f32 or bf16");
+  if ((int64_t)ro->num_envs * ro->num_chunks > 0)
+    CKRL_REQUIRE(po->logits && ro->tokens && ro->old_logprob, CKRL_ERR_INVALID_ARGUMENT,
+                 "logits, tokens and old_logprob are required");
+  if (ro->vocab == 256) {
+    uintptr_t p = reinterpret_cast<uintptr_t>(po->logits);
+    CKRL_REQUIRE((p & 15) == 0, CKRL_ERR_INVALID_ARGUMENT, "logits must be 16-byte aligned");
+  }
+  return CKRL_OK;
+}
+
+// ---- NCCL, resolved at communicator creation (no link-time dependency) -------------
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    // Reuse the NCCL already in the process (torch's), else load the system one.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce &&
+               api.CommDestroy && api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+}  // namespace
+
+struct ckrl_comm {
+  ncclComm_t nc;
+  int world, rank;
+};
+
+#define CKRL_NCCL(x)                                                                    \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess) return fail(CKRL_ERR_NCCL, std::string(#x ": ") + nccl().GetErrorString(r_)); \
+  } while (0)
+
+extern "C" {
+
+const char* ckrl_version(void) { return "ckrl 0.1.0 (sm_100a)"; }
+
+const char* ckrl_status_string(int32_t s) {
+  switch (s) {
+    case CKRL_OK: return "ok";
+    case CKRL_ERR_UNSUPPORTED_COMBINATION: return "UnsupportedCombination";
+    case CKRL_ERR_GRANULARITY_ORDER: return "GranularityOrderViolation";
+    case CKRL_ERR_LENGTH_MISMATCH: return "LengthMismatch";
+    case CKRL_ERR_BAD_RESET_ID: return "BadResetId";
+    case CKRL_ERR_HEAD_MISMATCH: return "HeadMismatch";
+    case CKRL_ERR_NON_FINITE: return "NonFinite";
+    case CKRL_ERR_DEGENERATE_GROUP: return "DegenerateGroup";
+    case CKRL_ERR_SKIP_UPDATE: return "SkipUpdate";
+    case CKRL_ERR_INVALID_PLAN: return "InvalidPlan";
+    case CKRL_ERR_MEMORY_OVERFLOW: return "MemoryOverflow";
+    case CKRL_ERR_EMPTY_TRACE: return "EmptyTrace";
+    case CKRL_ERR_CONFIG: return "ConfigError";
+    case CKRL_ERR_GENERIC: return "Error";
+    case CKRL_ERR_CUDA: return "CudaError";
+    case CKRL_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case CKRL_ERR_NCCL: return "NcclError";
+    default: return "unknown";
+  }
+}
+
+const char* ckrl_last_error(void) { return g_last_error.c_str(); }
+
+int32_t ckrl_validate_granularity(const ckrl_granularity* spec) { return validate(spec); }
+
+size_t ckrl_workspace_bytes(int32_t num_envs, int32_t num_chunks, int32_t chunk_len,
+                            int32_t tokens_per_action, int32_t world) {
+  (void)num_chunks;
+  (void)chunk_len;
+  (void)tokens_per_action;
+  return ws_layout(num_envs, world).total;
+}
+
+int32_t ckrl_workspace_init(void* ws, size_t bytes, ckrl_stream_t stream) {
+  CKRL_REQUIRE(ws != nullptr, CKRL_ERR_INVALID_ARGUMENT, "workspace is null");
+  CKRL_CUDA(cudaMemsetAsync(ws, 0, bytes, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+size_t ckrl_stats_record_bytes(void) { return sizeof(StatsRecord); }
+
+int32_t ckrl_merge_stats_host(const void* records, int32_t world, double* out_mean,
+                              double* out_denom, int64_t* out_counts) {
+  CKRL_REQUIRE(records && world >= 1, CKRL_ERR_INVALID_ARGUMENT, "bad stats records");
+  const StatsRecord* r = static_cast<const StatsRecord*>(records);
+  Moments m{0.0, 0.0, 0.0};
+  int64_t c[4] = {0, 0, 0, 0};
+  for (int i = 0; i < world; ++i) {
+    m = merge_moments(m, Moments{(double)r[i].n_units, r[i].mean, r[i].m2});
+    c[0] += r[i].n_adv;
+    c[1] += r[i].n_val;
+    c[2] += r[i].n_pos;
+    c[3] += r[i].groups_retained;
+  }
+  if (out_mean) *out_mean = m.mean;
+  if (out_denom) *out_denom = m.n > 0 ? sqrt(m.m2 / m.n) + 1e-8 : 1.0;
+  if (out_counts) std::memcpy(out_counts, c, sizeof(c));
+  return CKRL_OK;
+}
+
+int32_t ckrl_compute_gae(int32_t num_seqs, const int32_t* seq_offsets, const double* rewards,
+                         const double* values, const double* bootstrap, const uint8_t* flags,
+                         const ckrl_gae_params* params, double* advantages, double* returns,
+                         ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(params && num_seqs >= 0, CKRL_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (num_seqs == 0) return CKRL_OK;
+  CKRL_REQUIRE(seq_offsets && rewards && values && bootstrap && flags && advantages && returns,
+               CKRL_ERR_LENGTH_MISMATCH, "compute_gae: null input");
+  CKRL_CUDA(launch_flat_gae(num_seqs, seq_offsets, rewards, values, bootstrap, flags, params->gamma,
+                            params->lambda, advantages, returns, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_assemble_ppo_batch(const ckrl_rollout* ro, const ckrl_gae_params* gae,
+                                const ckrl_granularity* spec, ckrl_ppo_batch* batch,
+                                void* workspace, size_t ws_bytes, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  // assembler.cpp:82-83
+  if (spec->value_level != spec->advantage_level)
+    return fail(CKRL_ERR_CONFIG, "value_type must match reward_type for GAE assembly");
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, true))) return st;
+  if ((st = check_ws(workspace, ws_bytes, ro->num_envs, 1))) return st;
+  CKRL_REQUIRE(gae && batch && batch->counted && batch->advantages && batch->returns,
+               CKRL_ERR_INVALID_ARGUMENT, "batch outputs are required");
+  WsLayout L = ws_layout(ro->num_envs, 1);
+  CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
+                                gae->lambda, *batch, (char*)workspace, L, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_normalize_advantages(const ckrl_rollout* ro, const ckrl_granularity* spec,
+                                  ckrl_ppo_batch* batch, void* workspace, size_t ws_bytes,
+                                  ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_ws(workspace, ws_bytes, ro->num_envs, 1))) return st;
+  WsLayout L = ws_layout(ro->num_envs, 1);
+  CKRL_CUDA(launch_normalize(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, batch->counted,
+                             batch->advantages,
+                             reinterpret_cast<const StatsRecord*>((char*)workspace + L.stats_local), 1,
+                             (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_assemble_grpo_batch(const ckrl_rollout* ro, const ckrl_episodes* ep,
+                                 const ckrl_granularity* spec, const ckrl_grpo_options* opt,
+                                 ckrl_grpo_batch* gb, void* workspace, size_t ws_bytes,
+                                 ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_ws(workspace, ws_bytes, ro->num_envs, 1))) return st;
+  CKRL_REQUIRE(ep && opt && gb, CKRL_ERR_INVALID_ARGUMENT, "episodes / options / batch required");
+  CKRL_REQUIRE(gb->env_group && gb->env_member && gb->env_episode && gb->env_advantage &&
+                   gb->env_group_size && gb->slot_weight && gb->slot_member && gb->group_counts,
+               CKRL_ERR_INVALID_ARGUMENT, "grpo batch outputs are required");
+  CKRL_REQUIRE(ep->count >= 0, CKRL_ERR_LENGTH_MISMATCH, "negative episode count");
+  WsLayout L = ws_layout(ro->num_envs, 1);
+  CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, (char*)workspace, L, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, int32_t logits_dtype,
+                         const void* logits, int32_t token_dtype, const void* tokens,
+                         float* token_logprob, float* token_entropy, double* action_logprob,
+                         double* chunk_logprob, ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(num_chunks >= 0 && C >= 1 && M >= 1 && V >= 1 && (int64_t)C * M <= 8192,
+               CKRL_ERR_LENGTH_MISMATCH, "bad token_stats dimensions");
+  if (num_chunks == 0) return CKRL_OK;
+  CKRL_REQUIRE(logits && tokens, CKRL_ERR_INVALID_ARGUMENT, "logits / tokens required");
+  LossArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.mode = MODE_STATS;
+  a.C = C;
+  a.M = M;
+  a.V = V;
+  a.E = 1;
+  a.Tc = (int)num_chunks;
+  a.n_rec = num_chunks;
+  a.logits_bf16 = logits_dtype == CKRL_DTYPE_BF16;
+  a.tok_i32 = token_dtype == CKRL_DTYPE_I32;
+  a.logits = logits;
+  a.tokens = tokens;
+  a.tok_lp = token_logprob;
+  a.tok_ent = token_entropy;
+  a.action_lp = action_logprob;
+  a.chunk_lp = chunk_logprob;
+  a.all_rows = 1;
+  a.world = 0;
+  CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));
+  return CKRL_OK;
+}
+
+static int32_t ppo_loss_impl(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
+                             const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                             const ckrl_ppo_params* p, ckrl_loss_outputs* out, double* diag,
+                             void* ws, int world, const StatsRecord* recs, int finalize,
+                             cudaStream_t s) {
+  LossArgs a = base_args(ro, po, (char*)ws, world);
+  a.mode = MODE_PPO;
+  a.counted = b->counted;
+  a.adv = b->advantages;
+  a.ret = b->returns;
+  a.new_values = po->values;
+  a.adv_level = spec->advantage_level;
+  a.lp_level = spec->logprob_level;
+  a.val_level = spec->value_level;
+  a.clip = p->clip_eps;
+  a.vcoef = p->value_loss_coef;
+  a.ecoef = p->entropy_coef;
+  a.normalize = p->advantage_normalization;
+  a.recs = recs;
+  a.diag = diag;
+  a.finalize = finalize;
+  set_outputs(a, out);
+  CKRL_CUDA(launch_tile(a, s, nullptr));
+  return CKRL_OK;
+}
+
+int32_t ckrl_ppo_loss(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
+                      const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                      const ckrl_ppo_params* p, ckrl_loss_outputs* out, double* diag,
+                      void* ws, size_t ws_bytes, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, 1))) return st;
+  CKRL_REQUIRE(b && p && diag && b->counted && b->advantages && b->returns,
+               CKRL_ERR_INVALID_ARGUMENT, "batch / params / diag required");
+  CKRL_REQUIRE(p->value_loss_coef == 0.0 || po->values, CKRL_ERR_INVALID_ARGUMENT,
+               "new values required when value_loss_coef != 0");
+  WsLayout L = ws_layout(ro->num_envs, 1);
+  return ppo_loss_impl(ro, b, po, spec, p, out, diag, ws, 1,
+                       reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
+                       (cudaStream_t)stream);
+}
+
+static int32_t grpo_loss_impl(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
+                              const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                              const ckrl_grpo_params* p, ckrl_loss_outputs* out, double* diag,
+                              void* ws, int world, const StatsRecord* recs, int finalize,
+                              cudaStream_t s) {
+  LossArgs a = base_args(ro, po, (char*)ws, world);
+  a.mode = MODE_GRPO;
+  a.adv_level = spec->advantage_level;
+  a.lp_level = spec->logprob_level;
+  a.val_level = spec->value_level;
+  a.clip = p->clip_eps;
+  a.env_group = gb->env_group;
+  a.env_adv = gb->env_advantage;
+  a.env_group_size = gb->env_group_size;
+  a.slot_weight = gb->slot_weight;
+  a.slot_member = gb->slot_member;
+  a.recs = recs;
+  a.diag = diag;
+  a.finalize = finalize;
+  set_outputs(a, out);
+  a.coeff_ent = nullptr;
+  a.coeff_val = nullptr;
+  CKRL_CUDA(launch_tile(a, s, nullptr));
+  if (out && out->coeff_entropy)
+    CKRL_CUDA(cudaMemsetAsync(out->coeff_entropy, 0,
+                              sizeof(float) * (size_t)a.n_rec * a.C * a.M, s));
+  return CKRL_OK;
+}
+
+int32_t ckrl_grpo_loss(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
+                       const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                       const ckrl_grpo_params* p, ckrl_loss_outputs* out, double* diag,
+                       void* ws, size_t ws_bytes, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, 1))) return st;
+  CKRL_REQUIRE(gb && p && diag, CKRL_ERR_INVALID_ARGUMENT, "batch / params / diag required");
+  WsLayout L = ws_layout(ro->num_envs, 1);
+  return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
+                        reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
+                        (cudaStream_t)stream);
+}
+
+// Exchange the rank-local stats record (before the loss) over NCCL.
+static int32_t gather_stats(ckrl_comm* comm, char* ws, const WsLayout& L, cudaStream_t s) {
+  CKRL_NCCL(nccl().AllGather(ws + L.stats_local, ws + L.stats_all, sizeof(StatsRecord), ncclUint8,
+                             comm->nc, s));
+  return CKRL_OK;
+}
+
+int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
+                      const ckrl_gae_params* gae, const ckrl_granularity* spec,
+                      const ckrl_ppo_params* p, ckrl_ppo_batch* b, ckrl_loss_outputs* out,
+                      double* diag, void* ws, size_t ws_bytes, ckrl_comm* comm,
+                      ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if (spec->value_level != spec->advantage_level)
+    return fail(CKRL_ERR_CONFIG, "value_type must match reward_type for GAE assembly");
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, true))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(gae && p && b && diag && b->counted && b->advantages && b->returns,
+               CKRL_ERR_INVALID_ARGUMENT, "gae / params / batch / diag required");
+  CKRL_REQUIRE(p->value_loss_coef == 0.0 || po->values, CKRL_ERR_INVALID_ARGUMENT,
+               "new values required when value_loss_coef != 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  WsLayout L = ws_layout(ro->num_envs, world);
+  char* w = (char*)ws;
+  CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
+                                gae->lambda, *b, w, L, s));
+  if (world == 1)
+    return ppo_loss_impl(ro, b, po, spec, p, out, diag, ws, 1,
+                         reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s);
+  if ((st = gather_stats(comm, w, L, s))) return st;
+  if ((st = ppo_loss_impl(ro, b, po, spec, p, out, diag, ws, world,
+                          reinterpret_cast<const StatsRecord*>(w + L.stats_all), 0, s)))
+    return st;
+  CKRL_NCCL(nccl().AllReduce(w + L.loss_raw, w + L.loss_raw, RAW_COUNT, ncclFloat64, ncclSum,
+                             comm->nc, s));
+  LossArgs a = base_args(ro, po, w, world);
+  a.mode = MODE_PPO;
+  a.vcoef = p->value_loss_coef;
+  a.ecoef = p->entropy_coef;
+  a.normalize = p->advantage_normalization;
+  a.recs = reinterpret_cast<const StatsRecord*>(w + L.stats_all);
+  a.diag = diag;
+  CKRL_CUDA(launch_finalize(a, s));
+  return CKRL_OK;
+}
+
+int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
+                       const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                       const ckrl_grpo_options* opt, const ckrl_grpo_params* p,
+                       ckrl_grpo_batch* gb, ckrl_loss_outputs* out, double* diag, void* ws,
+                       size_t ws_bytes, ckrl_comm* comm, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(ep && opt && p && gb && diag, CKRL_ERR_INVALID_ARGUMENT,
+               "episodes / options / params / batch / diag required");
+  cudaStream_t s = (cudaStream_t)stream;
+  WsLayout L = ws_layout(ro->num_envs, world);
+  char* w = (char*)ws;
+  CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, w, L, s));
+  if (world == 1)
+    return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
+                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s);
+  if ((st = gather_stats(comm, w, L, s))) return st;
+  if ((st = grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, world,
+                           reinterpret_cast<const StatsRecord*>(w + L.stats_all), 0, s)))
+    return st;
+  CKRL_NCCL(nccl().AllReduce(w + L.loss_raw, w + L.loss_raw, RAW_COUNT, ncclFloat64, ncclSum,
+                             comm->nc, s));
+  LossArgs a = base_args(ro, po, w, world);
+  a.mode = MODE_GRPO;
+  a.recs = reinterpret_cast<const StatsRecord*>(w + L.stats_all);
+  a.diag = diag;
+  CKRL_CUDA(launch_finalize(a, s));
+  return CKRL_OK;
+}
+
+int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream) {
+  CKRL_REQUIRE(diag_device && diag_host, CKRL_ERR_INVALID_ARGUMENT, "null diagnostics");
+  CKRL_CUDA(cudaMemcpyAsync(diag_host, diag_device, sizeof(double) * CKRL_DIAG_COUNT,
+                            cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CKRL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int status = (int)diag_host[CKRL_DIAG_STATUS];
+  if (status == CKRL_ERR_SKIP_UPDATE) return fail(status, "no GRPO groups retained");
+  if (status == CKRL_ERR_DEGENERATE_GROUP)
+    return fail(status, "all trajectories in the group have equal return");
+  if (status == CKRL_ERR_NON_FINITE) return fail(status, "loss is not finite");
+  if (status) return fail(status, "device-side error");
+  return CKRL_OK;
+}
+
+int32_t ckrl_comm_unique_id(void* out_id) {
+  CKRL_REQUIRE(out_id, CKRL_ERR_INVALID_ARGUMENT, "null id buffer");
+  if (!nccl().ok) return fail(CKRL_ERR_NCCL, "NCCL library not found");
+  ncclUniqueId id;
+  CKRL_NCCL(nccl().GetUniqueId(&id));
+  std::memcpy(out_id, &id, sizeof(id));
+  return CKRL_OK;
+}
+
+int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out) {
+  CKRL_REQUIRE(out && unique_id && world >= 1 && world <= kMaxRanks && rank >= 0 && rank < world,
+               CKRL_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+  if (!nccl().ok) return fail(CKRL_ERR_NCCL, "NCCL library not found");
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ckrl_comm* c = new ckrl_comm;
+  c->world = world;
+  c->rank = rank;
+  ncclResult_t r = nccl().CommInitRank(&c->nc, world, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(CKRL_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+  }
+  *out = c;
+  return CKRL_OK;
+}
+
+int32_t ckrl_comm_destroy(ckrl_comm* comm) {
+  if (!comm) return CKRL_OK;
+  if (nccl().ok) nccl().CommDestroy(comm->nc);
+  delete comm;
+  return CKRL_OK;
+}
+
+}  // extern "C"

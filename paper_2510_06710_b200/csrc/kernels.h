@@ -1,0 +1,66 @@
+// Launchers shared between the kernel translation units and the C-ABI layer.
+#pragma once
+
+#include "common.cuh"
+
+namespace ckrl {
+
+enum LossMode { MODE_STATS = 0, MODE_PPO = 1, MODE_GRPO = 2 };
+
+struct LossArgs {
+  int mode;
+  int E, Tc, C, M, V;
+  int64_t n_rec;        // records (E*Tc), or chunks for MODE_STATS
+  int rec_per_tile;
+  int64_t n_tiles;
+  int logits_bf16, tok_i32;
+  const void* logits;
+  const void* tokens;
+  const float* old_lp;
+  // PPO
+  const uint8_t* counted;
+  const float* adv;
+  const float* ret;
+  const float* new_values;
+  int adv_level, lp_level, val_level;
+  double clip, vcoef, ecoef;
+  int normalize;
+  // GRPO
+  const int32_t* env_group;
+  const double* env_adv;
+  const int32_t* env_group_size;
+  const float* slot_weight;
+  const uint8_t* slot_member;
+  // outputs (nullable)
+  float* coeff_lp;
+  float* coeff_ent;
+  float* coeff_val;
+  float* tok_lp;
+  float* tok_ent;
+  double* action_lp;
+  double* chunk_lp;
+  int all_rows;  // evaluate every row (token outputs requested / MODE_STATS)
+  // cross-rank stats
+  const StatsRecord* recs;
+  int world;
+  char* ws;
+  WsLayout L;
+  double* diag;      // finalised diagnostics (world == 1); raw sums go to ws.loss_raw
+  int finalize;      // 1: last CTA finalises into diag; 0: leave raw sums for an allreduce
+};
+
+cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
+                                double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
+                                cudaStream_t s);
+cudaError_t launch_flat_gae(int num_seqs, const int32_t* offs, const double* r, const double* v,
+                            const double* b, const uint8_t* f, double gamma, double lambda,
+                            double* adv, double* ret, cudaStream_t s);
+cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uint8_t* counted,
+                             float* adv, const StatsRecord* recs, int world, cudaStream_t s);
+cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep,
+                                 const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
+                                 const WsLayout& L, cudaStream_t s);
+cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
+
+}  // namespace ckrl

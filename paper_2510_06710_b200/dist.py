@@ -1,0 +1,122 @@
+"""Multi-GPU plumbing: env / group sharding and the NCCL communicator used by the step.
+
+The path shards by environment (GAE segments never cross envs, assembler.cpp:108-193)
+and, for GRPO, by whole groups (GroupKey, assembler.cpp:207-226). The only exchanges are
+the 64-byte per-rank stats record before the loss (whitening moments + normalisers or the
+retained-group count) and the loss scalars after it — both inside ckrl_*_step on the
+caller's stream. torch.distributed only bootstraps the NCCL unique id.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError
+
+
+def env_shard(num_envs: int, world: int, rank: int, group_size: int = 1) -> range:
+    """Contiguous env range of `rank`; GRPO groups (group_size consecutive envs sharing a
+    reset id, train.cpp:92-101) are never split across ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError("bad world/rank")
+    if num_envs % group_size:
+        raise ConfigError("num_envs must be a multiple of group_size")
+    groups = num_envs // group_size
+    base, extra = divmod(groups, world)
+    g0 = rank * base + min(rank, extra)
+    g1 = g0 + base + (1 if rank < extra else 0)
+    return range(g0 * group_size, g1 * group_size)
+
+
+def check_group_sharding(env_of_episode, key_of_episode, world: int, shard_of_env) -> None:
+    """Raises ConfigError if any GroupKey (task, reset id) has members on two ranks: the
+    rank-local grouping would then differ from the reference's global std::map grouping."""
+    owner = {}
+    for e, k in zip(np.asarray(env_of_episode).tolist(), [tuple(x) for x in np.asarray(key_of_episode).tolist()]):
+        r = shard_of_env(e)
+        if owner.setdefault(k, r) != r:
+            raise ConfigError(f"group key {k} spans ranks {owner[k]} and {r}")
+
+
+@dataclass
+class StatsRecord:
+    """Host view of the 64-byte record ranks all-gather (csrc/common.cuh StatsRecord)."""
+    mean: float = 0.0
+    m2: float = 0.0
+    n_units: int = 0
+    n_adv: int = 0
+    n_val: int = 0
+    n_pos: int = 0
+    groups_retained: int = 0
+    status: int = 0
+
+    DTYPE = np.dtype([("mean", "<f8"), ("m2", "<f8"), ("n_units", "<i8"), ("n_adv", "<i8"),
+                      ("n_val", "<i8"), ("n_pos", "<i8"), ("groups_retained", "<i8"),
+                      ("status", "<i8")])
+
+    def to_bytes(self) -> bytes:
+        a = np.zeros(1, self.DTYPE)
+        for k in self.DTYPE.names:
+            a[k] = getattr(self, k)
+        return a.tobytes()
+
+    @classmethod
+    def from_units(cls, adv_units, n_val, n_pos, groups=0):
+        a = np.asarray(adv_units, dtype=np.float64)
+        n = a.size
+        mean = float(a.mean()) if n else 0.0
+        m2 = float(((a - mean) ** 2).sum()) if n else 0.0
+        return cls(mean, m2, n, n, int(n_val), int(n_pos), int(groups), 0)
+
+
+def merge_stats(records) -> dict:
+    """Merges per-rank records in rank order with the same code the device uses
+    (ckrl_merge_stats_host -> merge_moments)."""
+    raw = b"".join(r.to_bytes() if isinstance(r, StatsRecord) else bytes(r) for r in records)
+    assert _lib.lib().ckrl_stats_record_bytes() == StatsRecord.DTYPE.itemsize
+    buf = C.create_string_buffer(raw, len(raw))
+    mean, denom = C.c_double(), C.c_double()
+    counts = (C.c_int64 * 4)()
+    _lib.check(_lib.lib().ckrl_merge_stats_host(buf, len(records), C.byref(mean), C.byref(denom),
+                                                counts))
+    return {"mean": mean.value, "denom": denom.value, "n_adv": counts[0], "n_val": counts[1],
+            "n_pos": counts[2], "groups_retained": counts[3]}
+
+
+class Comm:
+    """Owns a ckrl_comm (an NCCL communicator over NVLink) for one rank."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes):
+        self.world, self.rank = world, rank
+        h = C.c_void_p()
+        _lib.check(_lib.lib().ckrl_comm_create(world, rank, C.create_string_buffer(unique_id, 128),
+                                               C.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _lib.check(_lib.lib().ckrl_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(world, rank, obj[0])
+
+    def close(self):
+        if self.handle:
+            _lib.lib().ckrl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

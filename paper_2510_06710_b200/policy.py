@@ -1,0 +1,33 @@
+"""The fused action-token kernel as a standalone operator: PolicyNet::evaluate_chunk
+(policy/policy_net.cpp:333-357) + aggregate_logprob (core/granularity.cpp:83-113) over
+current-policy logits rows."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .core import _ptr, stream_ptr
+
+
+def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, stream=None):
+    """logits [..., C, M, V] (f32/bf16), tokens [..., C, M] -> dict of token log-probs and
+    entropies [..., C, M] (f32), action log-probs [..., C] and chunk log-probs [...] (f64,
+    canonical summation order)."""
+    *lead, Cn, M, V = logits.shape
+    n = 1
+    for d in lead:
+        n *= d
+    dev = logits.device
+    lp = torch.empty((*lead, Cn, M), dtype=torch.float32, device=dev)
+    ent = torch.empty_like(lp)
+    act = torch.empty((*lead, Cn), dtype=torch.float64, device=dev)
+    chk = torch.empty(tuple(lead), dtype=torch.float64, device=dev)
+    ld = _lib.DTYPE_BF16 if logits.dtype == torch.bfloat16 else _lib.DTYPE_F32
+    td = _lib.DTYPE_U8 if tokens.dtype == torch.uint8 else _lib.DTYPE_I32
+    tokens = tokens.contiguous() if tokens.dtype in (torch.uint8, torch.int32) else tokens.to(torch.int32).contiguous()
+    _lib.check(_lib.lib().ckrl_token_stats(n, Cn, M, V, ld, _ptr(logits.contiguous()), td,
+                                           _ptr(tokens), _ptr(lp), _ptr(ent), _ptr(act), _ptr(chk),
+                                           stream_ptr(stream)))
+    return {"token_logprob": lp, "token_entropy": ent, "action_logprob": act, "chunk_logprob": chk}
