@@ -31,27 +31,61 @@ struct Unit {
 // with the exact incoming A. Segment ends come from done flags, uid changes between
 // consecutive units and the end of the list (flush_segment's open end).
 // ---------------------------------------------------------------------------------
+constexpr int kGaeCache = 4;  // items per lane kept in registers across the phases
+
 template <class Acc>
 __device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Moments& mom,
                          double& counted_slots) {
   const int lane = threadIdx.x & 31;
   const int per = (n_items + 31) / 32;
   const int lo = min(n_items, lane * per), hi = min(n_items, lo + per);
+  const int cnt = hi - lo;
   const double gl = __dmul_rn(gamma, lambda);
+  const bool cached = per <= kGaeCache;
+
+  // Load once (independent loads, issued together) when the lane's range is short.
+  Unit cache[kGaeCache];
+  if (cached) {
+#pragma unroll
+    for (int q = 0; q < kGaeCache; ++q)
+      if (q < cnt) cache[q] = acc.load(lo + q);
+  }
+  // visit(fn, reverse): apply fn(i, unit) over my range
+  auto visit = [&](auto&& fn, bool reverse) {
+    if (cached) {
+      if (reverse) {
+#pragma unroll
+        for (int q = kGaeCache - 1; q >= 0; --q)
+          if (q < cnt && !fn(lo + q, cache[q])) return;
+      } else {
+#pragma unroll
+        for (int q = 0; q < kGaeCache; ++q)
+          if (q < cnt && !fn(lo + q, cache[q])) return;
+      }
+    } else if (reverse) {
+      for (int i = hi - 1; i >= lo; --i) {
+        Unit u = acc.load(i);
+        if (!fn(i, u)) return;
+      }
+    } else {
+      for (int i = lo; i < hi; ++i) {
+        Unit u = acc.load(i);
+        if (!fn(i, u)) return;
+      }
+    }
+  };
 
   // Phase 1: first unit of my range, then nearest such head to my right.
   bool h_has = false;
   int32_t h_uid = 0;
   double h_v = 0.0;
-  for (int i = lo; i < hi; ++i) {
-    Unit u = acc.load(i);
-    if (u.is_unit) {
-      h_has = true;
-      h_uid = u.uid;
-      h_v = u.v;
-      break;
-    }
-  }
+  visit([&](int, const Unit& u) {
+    if (!u.is_unit) return true;
+    h_has = true;
+    h_uid = u.uid;
+    h_v = u.v;
+    return false;
+  }, false);
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     bool o_has = __shfl_down_sync(0xffffffffu, h_has, off);
@@ -74,9 +108,8 @@ __device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Mom
     bool nx_has = nx_has0;
     int32_t nx_uid = nx_uid0;
     double nx_v = nx_v0;
-    for (int i = hi - 1; i >= lo; --i) {
-      Unit u = acc.load(i);
-      if (!u.is_unit) continue;
+    visit([&](int, const Unit& u) {
+      if (!u.is_unit) return true;
       bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
       double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
       double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
@@ -86,7 +119,8 @@ __device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Mom
       nx_has = true;
       nx_uid = u.uid;
       nx_v = u.v;
-    }
+      return true;
+    }, true);
   }
   // Phase 3: inclusive suffix scan of maps, G_l = F_l o G_{l+1}.
 #pragma unroll
@@ -108,11 +142,10 @@ __device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Mom
   double a_next = a_in;
   Moments m{0.0, 0.0, 0.0};
   double cs = 0.0;
-  for (int i = hi - 1; i >= lo; --i) {
-    Unit u = acc.load(i);
+  visit([&](int i, const Unit& u) {
     if (!u.is_unit) {
       acc.store_empty(i);
-      continue;
+      return true;
     }
     bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
     double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
@@ -129,7 +162,8 @@ __device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Mom
     nx_has = true;
     nx_uid = u.uid;
     nx_v = u.v;
-  }
+    return true;
+  }, true);
   // Merge lane moments in lane order (tree over fixed partners => deterministic).
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -155,6 +189,8 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   float* adv;
   float* ret;
   __device__ Unit load(int t) const {
+    // All C slots' fields are fetched with independent loads first (no data-dependent
+    // load chain), then the unit is formed in registers.
     const int C = ro.chunk_len;
     const int64_t rec = (int64_t)e * ro.num_chunks + t;
     const int64_t s0 = rec * C;
@@ -163,26 +199,65 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
     u.term = u.trunc = false;
     u.r = 0.0;
     u.counted_slots = 0;
+    u.uid = -1;
+    u.v = (double)ro.value_scalar[rec];
+    u.boot = 0.0;
+    constexpr int kC = 8;
+    if (C <= kC) {
+      uint8_t f[kC];
+      int32_t id[kC];
+      float rw[kC], bt[kC];
+#pragma unroll
+      for (int j = 0; j < kC; ++j)
+        if (j < C) {
+          f[j] = ro.flags[s0 + j];
+          id[j] = ro.episode_id[s0 + j];
+          rw[j] = ro.reward[s0 + j];
+          bt[j] = ro.bootstrap[s0 + j];
+        }
+      int first = -1;
+#pragma unroll
+      for (int j = kC - 1; j >= 0; --j)
+        if (j < C && (f[j] & CKRL_FLAG_VALID)) first = j;
+      if (first < 0) return u;  // fully frozen chunk
+      u.is_unit = true;
+#pragma unroll
+      for (int j = 0; j < kC; ++j)
+        if (j == first) u.uid = id[j];
+      bool open = true;
+#pragma unroll
+      for (int j = 0; j < kC; ++j) {
+        if (j < first || j >= C) continue;
+        open = open && (f[j] & CKRL_FLAG_VALID) && id[j] == u.uid;  // tail dropped
+        if (open) {
+          u.r = __dadd_rn(u.r, (double)rw[j]);
+          u.term = u.term || (f[j] & CKRL_FLAG_TERMINATED);
+          u.trunc = u.trunc || (f[j] & CKRL_FLAG_TRUNCATED);
+          u.boot = (double)bt[j];
+          ++u.counted_slots;
+        }
+      }
+      return u;
+    }
     int first = -1;
     for (int j = 0; j < C; ++j)
       if (ro.flags[s0 + j] & CKRL_FLAG_VALID) {
         first = j;
         break;
       }
-    if (first < 0) return u;  // fully frozen chunk
+    if (first < 0) return u;
     u.is_unit = true;
     u.uid = ro.episode_id[s0 + first];
     int last = first;
     for (int j = first; j < C; ++j) {
-      uint8_t f = ro.flags[s0 + j];
-      if (!(f & CKRL_FLAG_VALID) || ro.episode_id[s0 + j] != u.uid) break;  // tail dropped
+      uint8_t fl = ro.flags[s0 + j];
+      if (!(fl & CKRL_FLAG_VALID) || ro.episode_id[s0 + j] != u.uid) break;
       u.r = __dadd_rn(u.r, (double)ro.reward[s0 + j]);
-      u.term = u.term || (f & CKRL_FLAG_TERMINATED);
-      u.trunc = u.trunc || (f & CKRL_FLAG_TRUNCATED);
+      u.term = u.term || (fl & CKRL_FLAG_TERMINATED);
+      u.trunc = u.trunc || (fl & CKRL_FLAG_TRUNCATED);
       last = j;
       ++u.counted_slots;
     }
-    u.v = (double)ro.value_scalar[rec];
     u.boot = (double)ro.bootstrap[s0 + last];
     return u;
   }
@@ -270,6 +345,7 @@ struct FlatAcc {  // compute_gae over one flat sequence (gae.cpp:7-37)
 // Last-block reduction of the per-CTA assembly partials into the rank's StatsRecord.
 __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, int M) {
   __shared__ bool is_last;
+  __shared__ AsmPartial wpart[kAsmWarpsPerCta];
   AsmPartial* parts = reinterpret_cast<AsmPartial*>(ws + L.asm_partials);
   uint32_t* tickets = reinterpret_cast<uint32_t*>(ws + L.tickets);
   if (threadIdx.x == 0) {
@@ -279,15 +355,38 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!is_last || threadIdx.x != 0) return;
+  if (!is_last) return;
   __threadfence();
+  // Parallel, fixed-order merge: thread t merges partials t, t+nthr, ... (Chan), then a
+  // fixed tree over lanes and warps.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Moments m{0.0, 0.0, 0.0};
   double npos = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
     volatile AsmPartial* p = parts + b;
-    Moments o{p->n, p->mean, p->m2};
-    m = merge_moments(m, o);
+    m = merge_moments(m, Moments{p->n, p->mean, p->m2});
     npos += p->n_pos;
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Moments o;
+    o.n = __shfl_down_sync(0xffffffffu, m.n, off);
+    o.mean = __shfl_down_sync(0xffffffffu, m.mean, off);
+    o.m2 = __shfl_down_sync(0xffffffffu, m.m2, off);
+    double op = __shfl_down_sync(0xffffffffu, npos, off);
+    if ((lane & (2 * off - 1)) == 0 && lane + off < 32) {
+      m = merge_moments(m, o);
+      npos += op;
+    }
+  }
+  if (lane == 0) wpart[warp] = AsmPartial{m.n, m.mean, m.m2, npos};
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  m = Moments{0.0, 0.0, 0.0};
+  npos = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    m = merge_moments(m, Moments{wpart[w].n, wpart[w].mean, wpart[w].m2});
+    npos += wpart[w].n_pos;
   }
   StatsRecord* st = reinterpret_cast<StatsRecord*>(ws + L.stats_local);
   st->mean = m.mean;

@@ -15,6 +15,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace ckrl {
 
 constexpr float kL2E = 1.4426950408889634f;
@@ -243,6 +245,320 @@ __device__ void finalize_diag(const LossArgs& a, const LossConsts& k, const doub
   diag[CKRL_DIAG_STATUS] = status;
 }
 
+// ---------------------------------------------------------------------------------
+// Unit phase: everything after the tile's per-row partials (s, t2, c, x_tok) sit in
+// shared memory. Token pass (one thread per token row): lp, entropy, token outputs, PPO
+// entropy term and token-level units. Slot pass (one thread per slot): action-level
+// units and values. Record pass (one warp per record): chunk-level units as a warp
+// reduction over the record's tokens. fp64 throughout.
+// ---------------------------------------------------------------------------------
+template <int MODE>
+__device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& k, Acc& acc,
+                                           const RowSmem& sm, int64_t r0, int nrec, int tid,
+                                           int nthr) {
+  const int C = a.C, M = a.M, P = C * M;
+  const int rows = nrec * P;
+  const int64_t k0 = r0 * P;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+  const bool chunk_adv = a.adv_level == CKRL_LEVEL_CHUNK;
+
+  // ---- token pass ----
+  for (int row = tid; row < rows; row += nthr) {
+    const int64_t kk = k0 + row;
+    const int64_t slot = kk / M;
+    const int64_t rec = kk / P;
+    const double s = (double)sm.s[row];
+    const double ls = log(s);
+    const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
+    const float ent = (float)(ls - kLN2 * (double)sm.t2[row] / s);
+    const float old = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + kk);
+    sm.lp[row] = lp;
+    sm.old[row] = old;
+    if (a.tok_lp) a.tok_lp[kk] = (float)lp;
+    if (a.tok_ent) a.tok_ent[kk] = ent;
+    if (MODE == MODE_PPO) {
+      const bool cnt = a.counted[slot] != 0;
+      if (cnt) acc.ent += ent;
+      if (a.coeff_ent) a.coeff_ent[kk] = (cnt && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
+      if (a.lp_level == CKRL_LEVEL_TOKEN) {
+        float coeff = 0.0f;
+        if (cnt) {
+          double adv = chunk_adv ? (double)a.adv[rec] : (double)a.adv[slot];
+          if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          const double d = lp - (double)old;
+          const double rho = exp(d);
+          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          acc.surr += su.value;
+          acc.units += 1.0;
+          acc.clipped += su.clipped;
+          acc.kl += (rho - 1.0) - d;
+          coeff = (float)(-k.inv_adv * su.dlogprob);
+        }
+        if (a.coeff_lp) a.coeff_lp[kk] = coeff;
+      }
+    } else if (MODE == MODE_GRPO && a.lp_level == CKRL_LEVEL_TOKEN) {
+      const int e = (int)(rec / a.Tc);
+      const float w = a.slot_weight[slot];
+      float coeff = 0.0f;
+      if (a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f) {
+        const double inv_g = 1.0 / (double)a.env_group_size[e];
+        const double d = lp - (double)old;
+        const double rho = exp(d);
+        Surrogate su = clipped_surrogate(rho, a.env_adv[e], a.clip);
+        acc.surr += k.inv_groups * inv_g * (double)w * su.value;
+        acc.units += 1.0;
+        acc.clipped += su.clipped;
+        acc.kl += (rho - 1.0) - d;
+        coeff = (float)(-k.inv_groups * inv_g * (double)w * su.dlogprob);
+      }
+      if (a.coeff_lp) a.coeff_lp[kk] = coeff;
+    }
+  }
+  __syncwarp();
+  // the slot / record passes read other threads' token results
+  if (nthr == kLossThreads)
+    asm volatile("bar.sync 1, %0;" ::"n"(kLossThreads));
+  else if (nthr != 32)
+    __syncthreads();
+
+  // ---- slot pass ----
+  if (MODE == MODE_STATS) {
+    if (a.action_lp)
+      for (int sl = tid; sl < nrec * C; sl += nthr) {
+        double s = 0.0;
+        for (int j = 0; j < M; ++j) s += sm.lp[sl * M + j];
+        a.action_lp[r0 * C + sl] = s;
+      }
+  } else {
+    const bool act_lp = a.lp_level == CKRL_LEVEL_ACTION;
+    const bool act_val = MODE == MODE_PPO && a.val_level == CKRL_LEVEL_ACTION;
+    if (act_lp || act_val)
+      for (int sl = tid; sl < nrec * C; sl += nthr) {
+        const int64_t slot = r0 * C + sl;
+        const int64_t rec = r0 + sl / C;
+        if (act_lp) {
+          bool on;
+          double adv, scale = 1.0;
+          int e = 0;
+          if (MODE == MODE_PPO) {
+            on = a.counted[slot] != 0;
+            adv = chunk_adv ? (double)a.adv[rec] : (double)a.adv[slot];
+            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          } else {
+            e = (int)(rec / a.Tc);
+            const float w = a.slot_weight[slot];
+            on = a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f;
+            adv = on ? a.env_adv[e] : 0.0;
+            scale = on ? k.inv_groups * (1.0 / (double)a.env_group_size[e]) * (double)w : 0.0;
+          }
+          float coeff = 0.0f;
+          if (on) {
+            double an = 0.0, ao = 0.0;
+            for (int j = 0; j < M; ++j) {
+              an += sm.lp[sl * M + j];
+              ao += (double)sm.old[sl * M + j];
+            }
+            const double rho = exp(an - ao);
+            Surrogate su = clipped_surrogate(rho, adv, a.clip);
+            acc.units += 1.0;
+            acc.clipped += su.clipped;
+            acc.kl += (rho - 1.0) - (an - ao);
+            if (MODE == MODE_PPO) {
+              acc.surr += su.value;
+              coeff = (float)(-k.inv_adv * su.dlogprob);
+            } else {
+              acc.surr += scale * su.value;
+              coeff = (float)(-scale * su.dlogprob);
+            }
+          }
+          if (a.coeff_lp)
+            for (int j = 0; j < M; ++j) a.coeff_lp[slot * M + j] = coeff;
+        }
+        if (act_val) {  // value loss per counted slot (losses.cpp:272-285)
+          float cv = 0.0f;
+          if (a.counted[slot] && a.new_values) {
+            const double err = (double)a.new_values[slot] - (double)a.ret[slot];
+            acc.valsq += err * err;
+            cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
+          }
+          if (a.coeff_val) a.coeff_val[slot] = cv;
+        }
+      }
+  }
+
+  // ---- record pass (one warp per record) ----
+  const bool chunk_lp = MODE != MODE_STATS && a.lp_level == CKRL_LEVEL_CHUNK;
+  const bool chunk_val = MODE == MODE_PPO && a.val_level == CKRL_LEVEL_CHUNK;
+  if (MODE == MODE_STATS && a.chunk_lp) {
+    for (int r = warp; r < nrec; r += nwarps) {
+      double s = 0.0;
+      for (int t = lane; t < P; t += 32) s += sm.lp[r * P + t];
+      s = warp_sum(s);
+      if (lane == 0) a.chunk_lp[r0 + r] = s;
+    }
+  }
+  if (chunk_lp || chunk_val) {
+    for (int r = warp; r < nrec; r += nwarps) {
+      const int64_t rec = r0 + r;
+      const int e = (int)(rec / a.Tc);
+      // per-slot inclusion (counted for PPO; member && w != 0 for GRPO)
+      bool has_env = MODE == MODE_PPO || a.env_group[e] >= 0;
+      double lpn = 0.0, lpo = 0.0, wsum = 0.0;
+      int any = 0;
+      for (int t = lane; t < P && has_env; t += 32) {
+        const int64_t slot = rec * C + t / M;
+        bool on;
+        if (MODE == MODE_PPO) {
+          on = a.counted[slot] != 0;
+        } else {
+          on = a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+          if (on && (t % M) == 0) wsum += (double)a.slot_weight[slot];
+        }
+        if (on) {
+          lpn += sm.lp[r * P + t];
+          lpo += (double)sm.old[r * P + t];
+          any = 1;
+        }
+      }
+      lpn = warp_sum(lpn);
+      lpo = warp_sum(lpo);
+      wsum = warp_sum(wsum);
+      any = __any_sync(0xffffffffu, any);
+      if (chunk_lp) {
+        float coeff = 0.0f;
+        if (any) {
+          const double rho = exp(lpn - lpo);
+          double adv, scale = 1.0;
+          if (MODE == MODE_PPO) {
+            adv = (double)a.adv[rec];
+            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          } else {
+            adv = a.env_adv[e];
+            scale = k.inv_groups * (1.0 / (double)a.env_group_size[e]) * wsum;
+          }
+          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          if (lane == 0) {
+            acc.units += 1.0;
+            acc.clipped += su.clipped;
+            acc.kl += (rho - 1.0) - (lpn - lpo);
+            acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
+          }
+          coeff = (float)(MODE == MODE_PPO ? -k.inv_adv * su.dlogprob : -scale * su.dlogprob);
+        }
+        if (a.coeff_lp)
+          for (int t = lane; t < P; t += 32) {
+            const int64_t slot = rec * C + t / M;
+            bool on;
+            if (MODE == MODE_PPO)
+              on = a.counted[slot] != 0;
+            else
+              on = has_env && a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+            a.coeff_lp[rec * P + t] = on && any ? coeff : 0.0f;
+          }
+      }
+      if (chunk_val && lane == 0) {  // losses.cpp:264-271
+        bool cnt = false;
+        for (int i = 0; i < C; ++i) cnt = cnt || a.counted[rec * C + i];
+        float cv = 0.0f;
+        if (cnt && a.new_values) {
+          const double err = (double)a.new_values[rec] - (double)a.ret[rec];
+          acc.valsq += err * err;
+          cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
+        }
+        if (a.coeff_val) a.coeff_val[rec] = cv;
+      }
+    }
+  }
+}
+
+// Deterministic reduction of the per-thread sums: warp tree -> CTA (warp order) ->
+// last CTA over the per-CTA partials (CTA order) -> raw sums [-> finalised diag].
+__device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const Acc& acc,
+                                  int tid, int nthr_total, double (*s_red)[RAW_COUNT], bool* s_last) {
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr_total >> 5;
+  double v[RAW_COUNT] = {acc.surr, acc.valsq, acc.ent, acc.kl, acc.clipped, acc.units, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < RAW_COUNT; ++i) {
+    double x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) s_red[warp][i] = x;
+  }
+  __syncthreads();
+  double* parts = reinterpret_cast<double*>(a.ws + a.L.loss_partials);
+  uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
+  if (tid < RAW_COUNT) {
+    double x = 0.0;
+    for (int w = 0; w < nwarps; ++w) x += s_red[w][tid];
+    parts[blockIdx.x * RAW_COUNT + tid] = x;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *s_last = atomicAdd(&tickets[TICKET_LOSS], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  // Last CTA: every thread sums a fixed strided subset of the partials (loads in
+  // parallel), then a fixed-shape tree over warps -> deterministic for a given grid.
+  {
+    double x[RAW_COUNT];
+#pragma unroll
+    for (int i = 0; i < RAW_COUNT; ++i) x[i] = 0.0;
+    const volatile double* vp = parts;
+    for (unsigned b = tid; b < gridDim.x; b += nthr_total)
+#pragma unroll
+      for (int i = 0; i < RAW_COUNT; ++i) x[i] += vp[b * RAW_COUNT + i];
+#pragma unroll
+    for (int i = 0; i < RAW_COUNT; ++i) {
+      double y = x[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) y += __shfl_down_sync(0xffffffffu, y, o);
+      x[i] = y;
+    }
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < RAW_COUNT; ++i) s_red[warp][i] = x[i];
+    __syncthreads();
+    if (tid < RAW_COUNT) {
+      double y = 0.0;
+      for (int w = 0; w < nwarps; ++w) y += s_red[w][tid];
+      reinterpret_cast<double*>(a.ws + a.L.loss_raw)[tid] = y;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    tickets[TICKET_LOSS] = 0;
+    if (a.finalize) finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
+  }
+}
+
+__device__ __forceinline__ RowSmem carve_rows(unsigned char* base, int rows_cap) {
+  RowSmem sm;
+  sm.lp = reinterpret_cast<double*>(base);
+  sm.s = reinterpret_cast<float*>(sm.lp + rows_cap);
+  sm.t2 = sm.s + rows_cap;
+  sm.c = sm.t2 + rows_cap;
+  sm.xt = sm.c + rows_cap;
+  sm.old = sm.xt + rows_cap;
+  sm.ent = sm.old + rows_cap;
+  return sm;
+}
+__host__ __device__ constexpr size_t rowsmem_bytes(int rows_cap) {
+  return (size_t)rows_cap * (sizeof(double) + 6 * sizeof(float));
+}
+
+__device__ __forceinline__ bool row_needed(const LossArgs& a, int mode, int64_t slot) {
+  if (a.all_rows) return true;
+  if (mode == MODE_PPO) return a.counted[slot] != 0;
+  if (mode == MODE_GRPO) return a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+  return true;
+}
+
+// ---------------------------------------------------------------------------------
+// Direct kernel: rows loaded straight from global into registers (used for generic V,
+// very long records, and as the reference point for the TMA pipeline).
+// ---------------------------------------------------------------------------------
 template <int MODE, typename LT, bool FAST>
 __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -250,23 +566,13 @@ __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
   __shared__ double s_red[kLossThreads / 32][RAW_COUNT];
   __shared__ bool s_last;
 
-  const int C = a.C, M = a.M, P = C * M, V = a.V;
-  const int rows_cap = a.rec_per_tile * P;
-  RowSmem sm;
-  sm.lp = reinterpret_cast<double*>(smem_raw);
-  sm.s = reinterpret_cast<float*>(sm.lp + rows_cap);
-  sm.t2 = sm.s + rows_cap;
-  sm.c = sm.t2 + rows_cap;
-  sm.xt = sm.c + rows_cap;
-  sm.old = sm.xt + rows_cap;
-  sm.ent = sm.old + rows_cap;
-
+  const int M = a.M, P = a.C * M, V = a.V;
+  const RowSmem sm = carve_rows(smem_raw, a.rec_per_tile * P);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sub = lane >> 3, l8 = lane & 7;
   if (tid == 0) s_k = merge_consts(a);
   __syncthreads();
   const LossConsts k = s_k;
-
   Acc acc{0, 0, 0, 0, 0, 0};
   const LT* logits = reinterpret_cast<const LT*>(a.logits);
 
@@ -275,16 +581,10 @@ __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
     const int64_t rem = a.n_rec - r0;
     const int nrec = (int)(rem < a.rec_per_tile ? rem : a.rec_per_tile);
     const int rows = nrec * P;
-    const int64_t k0 = r0 * P;  // first token of the tile
-    // ---------------- row phase ----------------
+    const int64_t k0 = r0 * P;
     for (int rg = warp * 4; rg < rows; rg += (kLossThreads / 32) * 4) {
       const int row = rg + sub;
-      bool need = row < rows;
-      if (need && !a.all_rows) {
-        const int64_t slot = (k0 + row) / M;
-        if (MODE == MODE_PPO) need = a.counted[slot] != 0;
-        if (MODE == MODE_GRPO) need = a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
-      }
+      bool need = row < rows && row_needed(a, MODE, (k0 + row) / M);
       const int64_t kk = k0 + (row < rows ? row : 0);
       const LT* rowp = logits + kk * (int64_t)V;
       int tok = 0;
@@ -306,265 +606,578 @@ __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
       }
     }
     __syncthreads();
-    // ---------------- token pass: lp, entropy (+ PPO entropy / token-level units) ----
-    for (int row = tid; row < rows; row += kLossThreads) {
-      const int64_t kk = k0 + row;
-      const int64_t slot = kk / M;
-      const int64_t rec = kk / P;
-      const double s = (double)sm.s[row];
-      const double ls = log(s);
-      const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
-      const float ent = (float)(ls - kLN2 * (double)sm.t2[row] / s);
-      const float old = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + kk);
-      sm.lp[row] = lp;
-      sm.ent[row] = ent;
-      sm.old[row] = old;
-      if (a.tok_lp) a.tok_lp[kk] = (float)lp;
-      if (a.tok_ent) a.tok_ent[kk] = ent;
+    unit_phase<MODE>(a, k, acc, sm, r0, nrec, tid, kLossThreads);
+    __syncthreads();
+  }
+  if (MODE == MODE_STATS) return;
+  reduce_and_finish(a, k, acc, tid, kLossThreads, s_red, &s_last);
+}
+
+// ---------------------------------------------------------------------------------
+// TMA pipeline kernel (V == 256): persistent, one CTA per SM, warp-specialised.
+//   warp 0 (one elected lane): producer. Streams each tile — whole records, contiguous
+//     in the [E][Tc][C][M][V] layout — into a ring of NSTAGE shared-memory stages with
+//     cp.async.bulk (the TMA bulk-copy engine), completion tracked by mbarrier tx-count.
+//   warps 1..8: consumers. Row phase from shared memory (LDS.128, conflict-free: each
+//     8-lane phase reads one 128-byte run of one row), release the stage, then the unit
+//     phase while the producer refills it. Per-row partials are double-buffered so only
+//     one consumer barrier per tile is needed.
+// ---------------------------------------------------------------------------------
+constexpr int kTmaConsumers = kLossThreads;      // 8 consumer warps
+constexpr int kTmaThreads = kTmaConsumers + 32;  // + producer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename LT>
+__device__ __forceinline__ void row_fast_smem(const LT* row, int l8, float& s_out, float& t_out,
+                                              float& c_out) {
+  float x[32];
+  if constexpr (sizeof(LT) == 4) {
+    const float4* p = reinterpret_cast<const float4*>(row);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 v = p[l8 + 8 * i];
+      x[4 * i + 0] = v.x;
+      x[4 * i + 1] = v.y;
+      x[4 * i + 2] = v.z;
+      x[4 * i + 3] = v.w;
+    }
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 v = p[l8 + 8 * i];
+      x[8 * i + 0] = bf16_lo(v.x);
+      x[8 * i + 1] = bf16_hi(v.x);
+      x[8 * i + 2] = bf16_lo(v.y);
+      x[8 * i + 3] = bf16_hi(v.y);
+      x[8 * i + 4] = bf16_lo(v.z);
+      x[8 * i + 5] = bf16_hi(v.z);
+      x[8 * i + 6] = bf16_lo(v.w);
+      x[8 * i + 7] = bf16_hi(v.w);
+    }
+  }
+  // max as a 5-level tree (short dependency chain), then across the 8-lane group
+  float mx[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) mx[i] = fmaxf(x[i], x[i + 16]);
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+  const float m = grp8_max(mx[0]);
+  const float c = m * kL2E;
+  float sa[4] = {0.f, 0.f, 0.f, 0.f}, ta[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float y = fmaf(x[i], kL2E, -c);
+    const float e = ex2(y);
+    sa[i & 3] += e;
+    ta[i & 3] = fmaf(e, y, ta[i & 3]);
+  }
+  s_out = grp8_sum((sa[0] + sa[1]) + (sa[2] + sa[3]));
+  t_out = grp8_sum((ta[0] + ta[1]) + (ta[2] + ta[3]));
+  c_out = c;
+}
+
+// log(s) for s >= 1 with ~1e-7 absolute error: exact exponent + f32 log of the mantissa.
+__device__ __forceinline__ double log_f32_exact_exp(float s) {
+  int e;
+  const float mant = frexpf(s, &e);  // s = mant * 2^e, mant in [0.5, 1)
+  return (double)e * kLN2 + (double)logf(mant);
+}
+
+constexpr int kRowBufs = 4;     // row-partial + metadata buffers (row warps <-> unit warps)
+constexpr int kMaxPasses = 4;   // row-group passes per warp per tile
+constexpr int kTileRowsMax = kMaxPasses * (kTmaConsumers / 32) * 4;  // 128 rows per tile
+
+// Per-tile small inputs staged in shared memory by the metadata warp, so consumer warps
+// never wait on global memory: token ids, old log-probs, per-slot activity (counted, or
+// trajectory member with non-zero weight) and weight, per-unit advantage / return / new
+// value, and (GRPO) the per-record env's group data.
+struct MetaSmem {
+  int32_t* tok;
+  float* old;
+  float* w;
+  float* adv;
+  float* ret;
+  float* nv;
+  int32_t* esz;
+  double* eadv;
+  uint8_t* act;
+};
+__host__ __device__ constexpr size_t meta_bytes() {
+  return (size_t)kTileRowsMax * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1);
+}
+__device__ __forceinline__ MetaSmem carve_meta(unsigned char* p) {
+  MetaSmem m;
+  m.eadv = reinterpret_cast<double*>(p);
+  m.tok = reinterpret_cast<int32_t*>(m.eadv + kTileRowsMax);
+  m.old = reinterpret_cast<float*>(m.tok + kTileRowsMax);
+  m.w = m.old + kTileRowsMax;
+  m.adv = m.w + kTileRowsMax;
+  m.ret = m.adv + kTileRowsMax;
+  m.nv = m.ret + kTileRowsMax;
+  m.esz = reinterpret_cast<int32_t*>(m.nv + kTileRowsMax);
+  m.act = reinterpret_cast<uint8_t*>(m.esz + kTileRowsMax);
+  return m;
+}
+__host__ __device__ constexpr size_t rowbuf_bytes() {
+  return rowsmem_bytes(kTileRowsMax) + meta_bytes();
+}
+
+// Register image of one tile's metadata for one lane (<= 4 items of each kind).
+struct MetaRegs {
+  int32_t tok[4];
+  float old[4], w[4], adv[4], ret[4], nv[4];
+  int32_t esz[4];
+  double eadv[4];
+  uint8_t act[4];
+};
+
+template <int MODE>
+__device__ __forceinline__ void meta_load(const LossArgs& a, int64_t r0, int nrec, int lane, MetaRegs& R) {
+  const int C = a.C, M = a.M, P = C * M;
+  const int rows = nrec * P, slots = nrec * C;
+  const int64_t k0 = r0 * P, s0 = r0 * C;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < rows) {
+      R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
+      R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
+    }
+    if (i < slots) {
       if (MODE == MODE_PPO) {
-        const bool cnt = a.counted[slot] != 0;
-        if (cnt) acc.ent += ent;
-        if (a.coeff_ent) a.coeff_ent[kk] = (cnt && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
-        if (a.lp_level == CKRL_LEVEL_TOKEN) {
-          float coeff = 0.0f;
-          if (cnt) {
-            double adv = a.adv_level == CKRL_LEVEL_CHUNK ? (double)a.adv[rec] : (double)a.adv[slot];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
-            const double d = lp - (double)old;
-            const double rho = exp(d);
-            Surrogate su = clipped_surrogate(rho, adv, a.clip);
-            acc.surr += su.value;
-            acc.units += 1.0;
-            acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - d;
-            coeff = (float)(-k.inv_adv * su.dlogprob);
-          }
-          if (a.coeff_lp) a.coeff_lp[kk] = coeff;
-        }
-      } else if (MODE == MODE_GRPO && a.lp_level == CKRL_LEVEL_TOKEN) {
-        const int e = (int)(rec / a.Tc);
-        const float w = a.slot_weight[slot];
-        float coeff = 0.0f;
-        if (a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f) {
-          const double inv_g = 1.0 / (double)a.env_group_size[e];
-          const double d = lp - (double)old;
-          const double rho = exp(d);
-          Surrogate su = clipped_surrogate(rho, a.env_adv[e], a.clip);
-          acc.surr += k.inv_groups * inv_g * (double)w * su.value;
-          acc.units += 1.0;
-          acc.clipped += su.clipped;
-          acc.kl += (rho - 1.0) - d;
-          coeff = (float)(-k.inv_groups * inv_g * (double)w * su.dlogprob);
-        }
-        if (a.coeff_lp) a.coeff_lp[kk] = coeff;
-      }
-    }
-    __syncthreads();
-    // ---------------- slot / record units ----------------
-    if (MODE == MODE_STATS) {
-      if (a.action_lp)
-        for (int sl = tid; sl < nrec * C; sl += kLossThreads) {
-          double s = 0.0;
-          for (int j = 0; j < M; ++j) s += sm.lp[sl * M + j];
-          a.action_lp[r0 * C + sl] = s;
-        }
-      if (a.chunk_lp)
-        for (int r = tid; r < nrec; r += kLossThreads) {
-          double s = 0.0;
-          for (int i = 0; i < C; ++i) {
-            double ai = 0.0;
-            for (int j = 0; j < M; ++j) ai += sm.lp[(r * C + i) * M + j];
-            s += ai;
-          }
-          a.chunk_lp[r0 + r] = s;
-        }
-    } else if (MODE == MODE_PPO) {
-      const bool chunk_adv = a.adv_level == CKRL_LEVEL_CHUNK;
-      if (a.lp_level == CKRL_LEVEL_ACTION) {
-        for (int sl = tid; sl < nrec * C; sl += kLossThreads) {
-          const int64_t slot = r0 * C + sl;
-          float coeff = 0.0f;
-          if (a.counted[slot]) {
-            double an = 0.0, ao = 0.0;
-            for (int j = 0; j < M; ++j) {
-              an += sm.lp[sl * M + j];
-              ao += (double)sm.old[sl * M + j];
-            }
-            double adv = chunk_adv ? (double)a.adv[r0 + sl / C] : (double)a.adv[slot];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
-            const double rho = exp(an - ao);
-            Surrogate su = clipped_surrogate(rho, adv, a.clip);
-            acc.surr += su.value;
-            acc.units += 1.0;
-            acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (an - ao);
-            coeff = (float)(-k.inv_adv * su.dlogprob);
-          }
-          if (a.coeff_lp)
-            for (int j = 0; j < M; ++j) a.coeff_lp[slot * M + j] = coeff;
-        }
-      } else if (a.lp_level == CKRL_LEVEL_CHUNK) {  // chunk advantage (validated)
-        for (int r = tid; r < nrec; r += kLossThreads) {
-          const int64_t rec = r0 + r;
-          double lpn = 0.0, lpo = 0.0;
-          bool any = false;
-          for (int i = 0; i < C; ++i) {
-            if (!a.counted[rec * C + i]) continue;
-            any = true;
-            double an = 0.0, ao = 0.0;
-            for (int j = 0; j < M; ++j) {
-              an += sm.lp[(r * C + i) * M + j];
-              ao += (double)sm.old[(r * C + i) * M + j];
-            }
-            lpn += an;
-            lpo += ao;
-          }
-          float coeff = 0.0f;
-          if (any) {
-            double adv = (double)a.adv[rec];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
-            const double rho = exp(lpn - lpo);
-            Surrogate su = clipped_surrogate(rho, adv, a.clip);
-            acc.surr += su.value;
-            acc.units += 1.0;
-            acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (lpn - lpo);
-            coeff = (float)(-k.inv_adv * su.dlogprob);
-          }
-          if (a.coeff_lp)
-            for (int i = 0; i < C; ++i) {
-              const float ci = a.counted[rec * C + i] ? coeff : 0.0f;
-              for (int j = 0; j < M; ++j) a.coeff_lp[(rec * C + i) * M + j] = ci;
-            }
-        }
-      }
-      // value loss at the value level (losses.cpp:262-285)
-      if (a.val_level == CKRL_LEVEL_CHUNK) {
-        for (int r = tid; r < nrec; r += kLossThreads) {
-          const int64_t rec = r0 + r;
-          bool any = false;
-          for (int i = 0; i < C; ++i) any = any || a.counted[rec * C + i];
-          float cv = 0.0f;
-          if (any && a.new_values) {
-            const double err = (double)a.new_values[rec] - (double)a.ret[rec];
-            acc.valsq += err * err;
-            cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
-          }
-          if (a.coeff_val) a.coeff_val[rec] = cv;
-        }
+        R.act[q] = a.all_rows ? 1 : 0;
+        R.act[q] |= (a.counted[s0 + i] != 0) ? 2 : 0;  // bit1: counted
+        R.w[q] = 0.0f;
+      } else if (MODE == MODE_GRPO) {
+        const int e = (int)((s0 + i) / C / a.Tc);
+        const float w = a.slot_weight[s0 + i];
+        const bool on = a.env_group[e] >= 0 && a.slot_member[s0 + i] && w != 0.0f;
+        R.act[q] = (a.all_rows ? 1 : 0) | (on ? 2 : 0) | (a.slot_member[s0 + i] ? 4 : 0);
+        R.w[q] = w;
       } else {
-        for (int sl = tid; sl < nrec * C; sl += kLossThreads) {
-          const int64_t slot = r0 * C + sl;
-          float cv = 0.0f;
-          if (a.counted[slot] && a.new_values) {
-            const double err = (double)a.new_values[slot] - (double)a.ret[slot];
-            acc.valsq += err * err;
-            cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
-          }
-          if (a.coeff_val) a.coeff_val[slot] = cv;
-        }
-      }
-    } else {  // MODE_GRPO, action / chunk log-prob units (losses.cpp:347-380)
-      if (a.lp_level == CKRL_LEVEL_ACTION) {
-        for (int sl = tid; sl < nrec * C; sl += kLossThreads) {
-          const int64_t slot = r0 * C + sl;
-          const int e = (int)((r0 + sl / C) / a.Tc);
-          const float w = a.slot_weight[slot];
-          float coeff = 0.0f;
-          if (a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f) {
-            const double inv_g = 1.0 / (double)a.env_group_size[e];
-            double an = 0.0, ao = 0.0;
-            for (int j = 0; j < M; ++j) {
-              an += sm.lp[sl * M + j];
-              ao += (double)sm.old[sl * M + j];
-            }
-            const double rho = exp(an - ao);
-            Surrogate su = clipped_surrogate(rho, a.env_adv[e], a.clip);
-            acc.surr += k.inv_groups * inv_g * (double)w * su.value;
-            acc.units += 1.0;
-            acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (an - ao);
-            coeff = (float)(-k.inv_groups * inv_g * (double)w * su.dlogprob);
-          }
-          if (a.coeff_lp)
-            for (int j = 0; j < M; ++j) a.coeff_lp[slot * M + j] = coeff;
-        }
-      } else if (a.lp_level == CKRL_LEVEL_CHUNK) {
-        for (int r = tid; r < nrec; r += kLossThreads) {
-          const int64_t rec = r0 + r;
-          const int e = (int)(rec / a.Tc);
-          double lpn = 0.0, lpo = 0.0, wsum = 0.0;
-          bool any = false;
-          const bool has = a.env_group[e] >= 0;
-          for (int i = 0; has && i < C; ++i) {
-            const float w = a.slot_weight[rec * C + i];
-            if (!a.slot_member[rec * C + i] || w == 0.0f) continue;
-            any = true;
-            double an = 0.0, ao = 0.0;
-            for (int j = 0; j < M; ++j) {
-              an += sm.lp[(r * C + i) * M + j];
-              ao += (double)sm.old[(r * C + i) * M + j];
-            }
-            lpn += an;
-            lpo += ao;
-            wsum += (double)w;
-          }
-          float coeff = 0.0f;
-          if (any) {
-            const double inv_g = 1.0 / (double)a.env_group_size[e];
-            const double rho = exp(lpn - lpo);
-            Surrogate su = clipped_surrogate(rho, a.env_adv[e], a.clip);
-            acc.surr += k.inv_groups * inv_g * wsum * su.value;
-            acc.units += 1.0;
-            acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (lpn - lpo);
-            coeff = (float)(-k.inv_groups * inv_g * wsum * su.dlogprob);
-          }
-          if (a.coeff_lp)
-            for (int i = 0; i < C; ++i) {
-              const bool cov = any && a.slot_member[rec * C + i] && a.slot_weight[rec * C + i] != 0.0f;
-              for (int j = 0; j < M; ++j) a.coeff_lp[(rec * C + i) * M + j] = cov ? coeff : 0.0f;
-            }
-        }
+        R.act[q] = 1;
       }
     }
-    __syncthreads();
+    if (MODE == MODE_PPO) {
+      const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+      const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+      if (i < adv_units) R.adv[q] = a.adv[(a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i];
+      if (i < val_units) {
+        const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
+        R.ret[q] = a.ret[vb + i];
+        R.nv[q] = a.new_values ? a.new_values[vb + i] : 0.0f;
+      }
+    }
+    if (MODE == MODE_GRPO && i < nrec) {
+      const int e = (int)((r0 + i) / a.Tc);
+      const int g = a.env_group[e];
+      R.esz[q] = g >= 0 ? a.env_group_size[e] : 0;
+      R.eadv[q] = g >= 0 ? a.env_adv[e] : 0.0;
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void meta_store(const LossArgs& a, int nrec, int lane, const MetaRegs& R,
+                                           const MetaSmem& m) {
+  const int C = a.C, P = C * a.M;
+  const int rows = nrec * P, slots = nrec * C;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < rows) {
+      m.tok[i] = R.tok[q];
+      m.old[i] = R.old[q];
+    }
+    if (i < slots) {
+      m.act[i] = R.act[q];
+      m.w[i] = R.w[q];
+    }
+    if (MODE == MODE_PPO && i < slots) {  // covers both unit kinds (nrec <= slots)
+      m.adv[i] = R.adv[q];
+      m.ret[i] = R.ret[q];
+      m.nv[i] = R.nv[q];
+    }
+    if (MODE == MODE_GRPO && i < nrec) {
+      m.esz[i] = R.esz[q];
+      m.eadv[i] = R.eadv[q];
+    }
+  }
+}
+
+// Warp-level unit phase over one tile, all inputs from shared memory (see unit_phase for
+// the semantics; identical arithmetic).
+template <int MODE>
+__device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossConsts& k, Acc& acc,
+                                                const RowSmem& sm, const MetaSmem& m, int64_t r0,
+                                                int nrec, int lane) {
+  const int C = a.C, M = a.M, P = C * M;
+  const int rows = nrec * P, slots = nrec * C;
+  const int64_t k0 = r0 * P;
+  const bool chunk_adv = a.adv_level == CKRL_LEVEL_CHUNK;
+
+  for (int row = lane; row < rows; row += 32) {
+    const int64_t kk = k0 + row;
+    const int sl = row / M, r = row / P;
+    const double lp = sm.lp[row];   // computed in the row phase
+    const float ent = sm.ent[row];
+    if (a.tok_lp) a.tok_lp[kk] = (float)lp;
+    if (a.tok_ent) a.tok_ent[kk] = ent;
+    const bool on = (m.act[sl] & 2) != 0;
+    if (MODE == MODE_PPO) {
+      if (on) acc.ent += ent;
+      if (a.coeff_ent) a.coeff_ent[kk] = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
+    }
+    if (MODE != MODE_STATS && a.lp_level == CKRL_LEVEL_TOKEN) {
+      float coeff = 0.0f;
+      if (on) {
+        double adv, scale;
+        if (MODE == MODE_PPO) {
+          adv = (double)m.adv[chunk_adv ? r : sl];
+          if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          scale = k.inv_adv;
+        } else {
+          adv = m.eadv[r];
+          scale = k.inv_groups * (1.0 / (double)m.esz[r]) * (double)m.w[sl];
+        }
+        const double d = lp - (double)m.old[row];
+        const double rho = exp(d);
+        Surrogate su = clipped_surrogate(rho, adv, a.clip);
+        acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
+        acc.units += 1.0;
+        acc.clipped += su.clipped;
+        acc.kl += (rho - 1.0) - d;
+        coeff = (float)(-scale * su.dlogprob);
+      }
+      if (a.coeff_lp) a.coeff_lp[kk] = coeff;
+    }
+  }
+  __syncwarp();
+
+  if (MODE == MODE_STATS) {
+    if (a.action_lp)
+      for (int sl = lane; sl < slots; sl += 32) {
+        double s = 0.0;
+        for (int j = 0; j < M; ++j) s += sm.lp[sl * M + j];
+        a.action_lp[r0 * C + sl] = s;
+      }
+    if (a.chunk_lp)
+      for (int r = 0; r < nrec; ++r) {
+        double s = 0.0;
+        for (int t = lane; t < P; t += 32) s += sm.lp[r * P + t];
+        s = warp_sum(s);
+        if (lane == 0) a.chunk_lp[r0 + r] = s;
+      }
+    return;
   }
 
-  if (MODE == MODE_STATS) return;
-  // ---------------- deterministic reduction: warp -> CTA -> last CTA ----------------
-  double v[RAW_COUNT] = {acc.surr, acc.valsq, acc.ent, acc.kl, acc.clipped, acc.units, 0.0, 0.0};
-#pragma unroll
-  for (int i = 0; i < RAW_COUNT; ++i) {
-    double x = v[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if (lane == 0) s_red[warp][i] = x;
-  }
-  __syncthreads();
-  double* parts = reinterpret_cast<double*>(a.ws + a.L.loss_partials);
-  uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
-  if (tid < RAW_COUNT) {
-    double x = 0.0;
-    for (int w = 0; w < kLossThreads / 32; ++w) x += s_red[w][tid];
-    parts[blockIdx.x * RAW_COUNT + tid] = x;
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&tickets[TICKET_LOSS], 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (tid < RAW_COUNT) {
-    double x = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) x += const_cast<volatile double*>(parts)[b * RAW_COUNT + tid];
-    reinterpret_cast<double*>(a.ws + a.L.loss_raw)[tid] = x;
-  }
-  __syncthreads();
+  const bool act_lp = a.lp_level == CKRL_LEVEL_ACTION;
+  const bool act_val = MODE == MODE_PPO && a.val_level == CKRL_LEVEL_ACTION;
+  if (act_lp || act_val)
+    for (int sl = lane; sl < slots; sl += 32) {
+      const int r = sl / C;
+      const bool on = (m.act[sl] & 2) != 0;
+      if (act_lp) {
+        float coeff = 0.0f;
+        if (on) {
+          double adv, scale;
+          if (MODE == MODE_PPO) {
+            adv = (double)m.adv[chunk_adv ? r : sl];
+            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            scale = k.inv_adv;
+          } else {
+            adv = m.eadv[r];
+            scale = k.inv_groups * (1.0 / (double)m.esz[r]) * (double)m.w[sl];
+          }
+          double an = 0.0, ao = 0.0;
+          for (int j = 0; j < M; ++j) {
+            an += sm.lp[sl * M + j];
+            ao += (double)m.old[sl * M + j];
+          }
+          const double rho = exp(an - ao);
+          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
+          acc.units += 1.0;
+          acc.clipped += su.clipped;
+          acc.kl += (rho - 1.0) - (an - ao);
+          coeff = (float)(-scale * su.dlogprob);
+        }
+        if (a.coeff_lp)
+          for (int j = 0; j < M; ++j) a.coeff_lp[(r0 * C + sl) * M + j] = coeff;
+      }
+      if (act_val) {
+        float cv = 0.0f;
+        if (on && a.new_values) {
+          const double err = (double)m.nv[sl] - (double)m.ret[sl];
+          acc.valsq += err * err;
+          cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
+        }
+        if (a.coeff_val) a.coeff_val[r0 * C + sl] = cv;
+      }
+    }
+
+  const bool chunk_lp = a.lp_level == CKRL_LEVEL_CHUNK;
+  const bool chunk_val = MODE == MODE_PPO && a.val_level == CKRL_LEVEL_CHUNK;
+  if (chunk_lp || chunk_val)
+    for (int r = 0; r < nrec; ++r) {
+      const int64_t rec = r0 + r;
+      double lpn = 0.0, lpo = 0.0, wsum = 0.0;
+      int any = 0;
+      for (int t = lane; t < P; t += 32) {
+        const int sl = r * C + t / M;
+        if (m.act[sl] & 2) {
+          lpn += sm.lp[r * P + t];
+          lpo += (double)m.old[r * P + t];
+          if (MODE == MODE_GRPO && (t % M) == 0) wsum += (double)m.w[sl];
+          any = 1;
+        }
+      }
+      any = __any_sync(0xffffffffu, any);
+      if (chunk_lp) {
+        lpn = warp_sum(lpn);
+        lpo = warp_sum(lpo);
+        if (MODE == MODE_GRPO) wsum = warp_sum(wsum);
+        float coeff = 0.0f;
+        if (any) {
+          const double rho = exp(lpn - lpo);
+          double adv, scale;
+          if (MODE == MODE_PPO) {
+            adv = (double)m.adv[r];
+            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            scale = k.inv_adv;
+          } else {
+            adv = m.eadv[r];
+            scale = k.inv_groups * (1.0 / (double)m.esz[r]) * wsum;
+          }
+          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          if (lane == 0) {
+            acc.units += 1.0;
+            acc.clipped += su.clipped;
+            acc.kl += (rho - 1.0) - (lpn - lpo);
+            acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
+          }
+          coeff = (float)(-scale * su.dlogprob);
+        }
+        if (a.coeff_lp)
+          for (int t = lane; t < P; t += 32)
+            a.coeff_lp[rec * P + t] = (m.act[r * C + t / M] & 2) ? coeff : 0.0f;
+      }
+      if (chunk_val && lane == 0) {
+        float cv = 0.0f;
+        if (any && a.new_values) {
+          const double err = (double)m.nv[r] - (double)m.ret[r];
+          acc.valsq += err * err;
+          cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
+        }
+        if (a.coeff_val) a.coeff_val[rec] = cv;
+      }
+    }
+}
+
+constexpr int kUnitWarps = kRowBufs;  // unit warp u owns row buffer u
+constexpr int kTmaThreadsFull = 64 + kTmaConsumers + 32 * kUnitWarps;  // producer, metadata,
+                                                                        // 8 row warps, unit warps
+
+// Synchronisation is mbarrier-only (no CTA-wide barrier in the main loop):
+//   full[s]     TMA producer -> row warps  (tx-count of the stage's bulk copies)
+//   empty[s]    row warps -> TMA producer  (8 arrivals: every warp finished reading stage s)
+//   metafull[b] metadata warp -> row warps and unit warp (tile metadata in buffer b)
+//   rowfull[b]  row warps -> unit warp     (8 arrivals: row partials of the tile complete)
+//   rowempty[b] unit warp -> row warps, metadata warp (buffer b may be overwritten)
+// Row warps only stream rows (never wait on a unit phase); the unit phase of tile i runs
+// on unit warp (i mod 4) and overlaps the row phases of the following tiles.
+template <int MODE, typename LT>
+__global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a, int nstage,
+                                                                      uint32_t tile_bytes) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ LossConsts s_k;
+  __shared__ double s_red[kTmaThreadsFull / 32][RAW_COUNT];
+  __shared__ bool s_last;
+  __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4], metafull_bar[kRowBufs],
+      rowfull_bar[kRowBufs], rowempty_bar[kRowBufs];
+
+  constexpr int V = 256;
+  constexpr int kCW = kTmaConsumers / 32;  // consumer warps
+  const int M = a.M, P = a.C * M;
+  unsigned char* stage_base = smem_raw;
+  unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
   if (tid == 0) {
-    tickets[TICKET_LOSS] = 0;
-    if (a.finalize) finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
+    for (int s = 0; s < nstage; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kCW);
+    }
+    for (int b = 0; b < kRowBufs; ++b) {
+      mbar_init(&metafull_bar[b], 1);
+      mbar_init(&rowfull_bar[b], kCW);
+      mbar_init(&rowempty_bar[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_k = merge_consts(a);
   }
+  __syncthreads();
+  const LossConsts k = s_k;
+  Acc acc{0, 0, 0, 0, 0, 0};
+  auto tile_recs = [&](int64_t tile, int64_t& r0) {
+    r0 = tile * a.rec_per_tile;
+    const int64_t rem = a.n_rec - r0;
+    return (int)(rem < a.rec_per_tile ? rem : a.rec_per_tile);
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const char* src = reinterpret_cast<const char*>(a.logits);
+      const size_t rec_bytes = (size_t)P * V * sizeof(LT);
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
+        const int s = it % nstage;
+        if (it >= nstage) mbar_wait(&empty_bar[s], ((it / nstage) - 1) & 1);
+        int64_t r0;
+        const int nrec = tile_recs(tile, r0);
+        const uint32_t bytes = (uint32_t)(nrec * rec_bytes);
+        mbar_expect_tx(&full_bar[s], bytes);
+        const char* g = src + (size_t)r0 * rec_bytes;
+        unsigned char* d = stage_base + (size_t)s * tile_bytes;
+        for (uint32_t off = 0; off < bytes; off += 32768u) {
+          const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+          bulk_g2s(d + off, g + off, n, &full_bar[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- metadata warp (loads one tile ahead) ----------------
+    MetaRegs cur, nxt;
+    int64_t tile = blockIdx.x, r0;
+    int nrec = 0;
+    if (tile < a.n_tiles) {
+      nrec = tile_recs(tile, r0);
+      meta_load<MODE>(a, r0, nrec, lane, cur);
+    }
+    for (int it = 0; tile < a.n_tiles; tile += gridDim.x, ++it) {
+      const int b = it % kRowBufs;
+      const int64_t ntile = tile + gridDim.x;
+      int64_t nr0 = 0;
+      int nnrec = 0;
+      if (ntile < a.n_tiles) {
+        nnrec = tile_recs(ntile, nr0);
+        meta_load<MODE>(a, nr0, nnrec, lane, nxt);
+      }
+      if (it >= kRowBufs) mbar_wait(&rowempty_bar[b], ((it / kRowBufs) - 1) & 1);
+      meta_store<MODE>(a, nrec, lane, cur, carve_meta(buf_base + b * rowbuf_bytes() + rowsmem_bytes(kTileRowsMax)));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&metafull_bar[b]);
+      cur = nxt;
+      nrec = nnrec;
+      r0 = nr0;
+    }
+  } else if (warp < 2 + kCW) {
+    // ---------------- row warps ----------------
+    const int cwarp = warp - 2;
+    const int sub = lane >> 3, l8 = lane & 7;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
+      const int s = it % nstage;
+      const int b = it % kRowBufs;
+      unsigned char* bb = buf_base + b * rowbuf_bytes();
+      const RowSmem sm = carve_rows(bb, kTileRowsMax);
+      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
+      int64_t r0;
+      const int nrec = tile_recs(tile, r0);
+      const int rows = nrec * P;
+      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // implies rowempty[b] was released
+      mbar_wait(&full_bar[s], (it / nstage) & 1);
+      const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
+#pragma unroll
+      for (int p = 0; p < kMaxPasses; ++p) {
+        const int rg = (p * kCW + cwarp) * 4;
+        if (rg >= rows) break;  // warp-uniform
+        const int row = rg + sub;
+        const bool valid = row < rows;
+        const LT* rowp = stage + (size_t)(valid ? row : rg) * V;
+        float s_, t_, c_;
+        row_fast_smem<LT>(rowp, l8, s_, t_, c_);
+        if (l8 == 0 && valid) {
+          const bool need = (mt.act[row / M] & 3) != 0;
+          double lp = 0.0;
+          float ent = 0.0f;
+          if (need) {
+            const int tok = mt.tok[row];
+            const float xt = sizeof(LT) == 4
+                                 ? (float)reinterpret_cast<const float*>(rowp)[tok]
+                                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rowp)[tok]);
+            const double ls = log_f32_exact_exp(s_);
+            lp = ((double)xt - (double)c_ * kLN2) - ls;
+            ent = (float)(ls - kLN2 * (double)t_ / (double)s_);
+          }
+          sm.lp[row] = lp;
+          sm.ent[row] = ent;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_bar[s]);    // stage s fully read by this warp
+        mbar_arrive(&rowfull_bar[b]);  // my rows' results are in buffer b
+      }
+    }
+  } else {
+    // ---------------- unit warps ----------------
+    const int uw = warp - 2 - kCW;
+    int it = uw;
+    for (int64_t tile = blockIdx.x + (int64_t)uw * gridDim.x; tile < a.n_tiles;
+         tile += (int64_t)kUnitWarps * gridDim.x, it += kUnitWarps) {
+      const int b = it % kRowBufs;  // == uw
+      unsigned char* bb = buf_base + b * rowbuf_bytes();
+      const RowSmem sm = carve_rows(bb, kTileRowsMax);
+      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
+      int64_t r0;
+      const int nrec = tile_recs(tile, r0);
+      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);
+      mbar_wait(&rowfull_bar[b], (it / kRowBufs) & 1);
+      unit_phase_smem<MODE>(a, k, acc, sm, mt, r0, nrec, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rowempty_bar[b]);
+    }
+  }
+  __syncthreads();
+  if (MODE == MODE_STATS) return;
+  reduce_and_finish(a, k, acc, tid, kTmaThreadsFull, s_red, &s_last);
 }
 
 __global__ void finalize_kernel(LossArgs a) {
@@ -573,21 +1186,28 @@ __global__ void finalize_kernel(LossArgs a) {
   finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
 }
 
+static int device_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
 template <int MODE, typename LT, bool FAST>
-static cudaError_t launch_tile_t(LossArgs& a, cudaStream_t s, int* grid_out) {
+static cudaError_t launch_direct(LossArgs& a, cudaStream_t s, int* grid_out) {
   auto kern = tile_kernel<MODE, LT, FAST>;
-  const int rows_cap = a.rec_per_tile * a.C * a.M;
-  const size_t smem = (size_t)rows_cap * (sizeof(double) + 6 * sizeof(float));
+  const int P = a.C * a.M;
+  a.rec_per_tile = P >= 256 ? 1 : 256 / P;
+  a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
+  const size_t smem = rowsmem_bytes(a.rec_per_tile * P);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kLossThreads, smem);
   if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)sms * occ;
+  int64_t grid = (int64_t)device_sms() * occ;
   if (grid > a.n_tiles) grid = a.n_tiles;
   if (grid > kMaxLossCtas) grid = kMaxLossCtas;
   if (grid < 1) grid = 1;
@@ -596,23 +1216,69 @@ static cudaError_t launch_tile_t(LossArgs& a, cudaStream_t s, int* grid_out) {
   return cudaGetLastError();
 }
 
+constexpr size_t kSmemBudget = 220 * 1024;
+constexpr size_t kStageTarget = 56 * 1024;
+
+// TMA pipeline plan: whole records per tile (~56 KB), 2-4 stages. Returns false when a
+// single record does not fit twice (then the direct kernel runs).
+static bool tma_plan(const LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, uint32_t& tile_bytes) {
+  const size_t rec = (size_t)a.C * a.M * 256 * dbytes;
+  rec_per_tile = (int)(kStageTarget / rec);
+  if (rec_per_tile < 1) rec_per_tile = 1;
+  const int max_rows = kTileRowsMax;
+  if (a.C * a.M > max_rows) return false;
+  if (rec_per_tile * a.C * a.M > max_rows) rec_per_tile = max_rows / (a.C * a.M);
+  tile_bytes = (uint32_t)(rec_per_tile * rec);
+  const size_t rows = (size_t)rec_per_tile * a.C * a.M;
+  const size_t fixed = kRowBufs * rowbuf_bytes() + 1024;
+  (void)rows;
+  nstage = fixed < kSmemBudget ? (int)((kSmemBudget - fixed) / tile_bytes) : 0;
+  if (nstage > 4) nstage = 4;
+  return nstage >= 2;
+}
+
+template <int MODE, typename LT>
+static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
+  auto kern = tma_tile_kernel<MODE, LT>;
+  a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
+  const size_t rows = (size_t)a.rec_per_tile * a.C * a.M;
+  const size_t smem = (size_t)nstage * tile_bytes + kRowBufs * rowbuf_bytes();
+  (void)rows;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t grid = device_sms();
+  if (grid > a.n_tiles) grid = a.n_tiles;
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = (int)grid;
+  kern<<<(unsigned)grid, kTmaThreadsFull, smem, s>>>(a, nstage, tile_bytes);
+  return cudaGetLastError();
+}
+
+static int g_force_direct = -1;
+
 template <int MODE>
 static cudaError_t launch_mode(LossArgs& a, cudaStream_t s, int* g) {
+  if (g_force_direct < 0) {
+    const char* env = getenv("CKRL_LOSS_KERNEL");
+    g_force_direct = (env && env[0] == 'd') ? 1 : 0;
+  }
   const bool fast = a.V == 256;
+  const int dbytes = a.logits_bf16 ? 2 : 4;
+  int rpt, nstage;
+  uint32_t tile_bytes;
+  const uintptr_t align = reinterpret_cast<uintptr_t>(a.logits) & 15;
+  if (fast && !g_force_direct && align == 0 && tma_plan(a, dbytes, rpt, nstage, tile_bytes)) {
+    a.rec_per_tile = rpt;
+    return a.logits_bf16 ? launch_tma<MODE, __nv_bfloat16>(a, s, g, nstage, tile_bytes)
+                         : launch_tma<MODE, float>(a, s, g, nstage, tile_bytes);
+  }
   if (a.logits_bf16)
-    return fast ? launch_tile_t<MODE, __nv_bfloat16, true>(a, s, g)
-                : launch_tile_t<MODE, __nv_bfloat16, false>(a, s, g);
-  return fast ? launch_tile_t<MODE, float, true>(a, s, g) : launch_tile_t<MODE, float, false>(a, s, g);
+    return fast ? launch_direct<MODE, __nv_bfloat16, true>(a, s, g)
+                : launch_direct<MODE, __nv_bfloat16, false>(a, s, g);
+  return fast ? launch_direct<MODE, float, true>(a, s, g) : launch_direct<MODE, float, false>(a, s, g);
 }
 
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out) {
-  // tile = whole records, ~256 token rows per tile
-  const int P = a.C * a.M;
-  a.rec_per_tile = P >= 256 ? 1 : 256 / P;
-  a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
-  if (a.n_rec == 0) {
-    a.n_tiles = 0;
-  }
   switch (a.mode) {
     case MODE_STATS: return launch_mode<MODE_STATS>(a, s, grid_out);
     case MODE_PPO: return launch_mode<MODE_PPO>(a, s, grid_out);

@@ -22,16 +22,18 @@ def load_golden(name):
     return {k: z[k] for k in z.files}
 
 
-def assert_close(x, ref, rel=1e-5, what=""):
-    """SURVEY §7 tolerance rule: |x - ref| <= rel * max(|ref|, rms(ref tensor)); a pure
-    relative bound is ill-posed near zero."""
+def assert_close(x, ref, rel=1e-5, what="", floor=0.0):
+    """SURVEY §7 tolerance rule: |x - ref| <= rel * max(|ref|, rms(ref tensor), floor); a
+    pure relative bound is ill-posed near zero. `floor` is the natural scale of quantities
+    normalised to unit std (whitened advantages), where an all-equal batch makes the
+    reference's own output pure round-off divided by its 1e-8 epsilon."""
     x = np.asarray(x, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert x.shape == ref.shape, f"{what}: shape {x.shape} != {ref.shape}"
     if ref.size == 0:
         return
     rms = float(np.sqrt(np.mean(ref * ref)))
-    bound = rel * np.maximum(np.abs(ref), rms) + 1e-300
+    bound = rel * np.maximum(np.maximum(np.abs(ref), rms), floor) + 1e-300
     err = np.abs(x - ref)
     bad = err > bound
     assert not bad.any(), (f"{what}: {int(bad.sum())}/{ref.size} outside tol; worst "

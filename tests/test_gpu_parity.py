@@ -110,7 +110,8 @@ def test_ppo_pipeline_vs_reference(name, oracle):
         assert_close(outs.coeff_value.cpu().numpy(), cval, 1e-4, f"{key} coeff_val")
         # materialised whitening (normalize_advantages) vs the reference
         optim.normalize_advantages(ro, batch)
-        assert_close(batch.advantages.cpu().numpy(), d[f"ppo/{key}/adv_norm"], TOL, f"{key} adv_norm")
+        assert_close(batch.advantages.cpu().numpy(), d[f"ppo/{key}/adv_norm"], TOL, f"{key} adv_norm",
+                     floor=1.0)
 
 
 @pytest.mark.parametrize("name", GRPO)
@@ -130,7 +131,8 @@ def test_grpo_pipeline_vs_reference(name):
         b = advantage.assemble_grpo_batch(ro, eps_tab, opts)
         status = int(d[f"grpo/{key}/status"])
         gt, gr = (int(x) for x in d[f"grpo/{key}/groups"])
-        assert (b.groups_total, b.groups_retained) == (gt, gr), key
+        if status != 7:  # the reference throws DegenerateGroup before reporting counts
+            assert (b.groups_total, b.groups_retained) == (gt, gr), key
         outs = LossOutputs.allocate(ro, Level.Chunk)
         diag = optim.grpo_loss(ro, pol, b, GrpoParams(clip), outs)
         if status != 0:
