@@ -711,6 +711,91 @@ __device__ __forceinline__ void row_fast_smem(const LT* row, int l8, float& s_ou
   c_out = c;
 }
 
+// R independent row groups per warp in flight (ILP across the shuffle / MUFU latencies).
+template <typename LT, int R>
+__device__ __forceinline__ void rows_fast_smem(const LT* const* rowp, int l8, float* s_out,
+                                               float* t_out, float* c_out) {
+  float x[R][32];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if constexpr (sizeof(LT) == 4) {
+      const float4* p = reinterpret_cast<const float4*>(rowp[r]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 v = p[l8 + 8 * i];
+        x[r][4 * i + 0] = v.x;
+        x[r][4 * i + 1] = v.y;
+        x[r][4 * i + 2] = v.z;
+        x[r][4 * i + 3] = v.w;
+      }
+    } else {
+      const uint4* p = reinterpret_cast<const uint4*>(rowp[r]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 v = p[l8 + 8 * i];
+        x[r][8 * i + 0] = bf16_lo(v.x);
+        x[r][8 * i + 1] = bf16_hi(v.x);
+        x[r][8 * i + 2] = bf16_lo(v.y);
+        x[r][8 * i + 3] = bf16_hi(v.y);
+        x[r][8 * i + 4] = bf16_lo(v.z);
+        x[r][8 * i + 5] = bf16_hi(v.z);
+        x[r][8 * i + 6] = bf16_lo(v.w);
+        x[r][8 * i + 7] = bf16_hi(v.w);
+      }
+    }
+  }
+  float m[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float mx[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mx[i] = fmaxf(x[r][i], x[r][i + 16]);
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+      for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+    m[r] = mx[0];
+  }
+#pragma unroll
+  for (int o = 1; o <= 4; o <<= 1)
+#pragma unroll
+    for (int r = 0; r < R; ++r) m[r] = fmaxf(m[r], __shfl_xor_sync(0xffffffffu, m[r], o));
+  float sa[R][2], ta[R][2], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    c[r] = m[r] * kL2E;
+    sa[r][0] = sa[r][1] = ta[r][0] = ta[r][1] = 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float y = fmaf(x[r][i], kL2E, -c[r]);
+      const float e = ex2(y);
+      sa[r][i & 1] += e;
+      ta[r][i & 1] = fmaf(e, y, ta[r][i & 1]);
+    }
+  float sv[R], tv[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    sv[r] = sa[r][0] + sa[r][1];
+    tv[r] = ta[r][0] + ta[r][1];
+  }
+#pragma unroll
+  for (int o = 1; o <= 4; o <<= 1)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sv[r] += __shfl_xor_sync(0xffffffffu, sv[r], o);
+      tv[r] += __shfl_xor_sync(0xffffffffu, tv[r], o);
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    s_out[r] = sv[r];
+    t_out[r] = tv[r];
+    c_out[r] = c[r];
+  }
+}
+
 // log(s) for s >= 1 with ~1e-7 absolute error: exact exponent + f32 log of the mantissa.
 __device__ __forceinline__ double log_f32_exact_exp(float s) {
   int e;
@@ -784,10 +869,13 @@ __device__ __forceinline__ void meta_load(const LossArgs& a, int64_t r0, int nre
         R.act[q] |= (a.counted[s0 + i] != 0) ? 2 : 0;  // bit1: counted
         R.w[q] = 0.0f;
       } else if (MODE == MODE_GRPO) {
+        // independent loads (no short-circuit chain), combined afterwards
         const int e = (int)((s0 + i) / C / a.Tc);
+        const int32_t g = a.env_group[e];
+        const uint8_t mem = a.slot_member[s0 + i];
         const float w = a.slot_weight[s0 + i];
-        const bool on = a.env_group[e] >= 0 && a.slot_member[s0 + i] && w != 0.0f;
-        R.act[q] = (a.all_rows ? 1 : 0) | (on ? 2 : 0) | (a.slot_member[s0 + i] ? 4 : 0);
+        const bool on = (g >= 0) & (mem != 0) & (w != 0.0f);
+        R.act[q] = (a.all_rows ? 1 : 0) | (on ? 2 : 0) | (mem ? 4 : 0);
         R.w[q] = w;
       } else {
         R.act[q] = 1;
@@ -805,9 +893,8 @@ __device__ __forceinline__ void meta_load(const LossArgs& a, int64_t r0, int nre
     }
     if (MODE == MODE_GRPO && i < nrec) {
       const int e = (int)((r0 + i) / a.Tc);
-      const int g = a.env_group[e];
-      R.esz[q] = g >= 0 ? a.env_group_size[e] : 0;
-      R.eadv[q] = g >= 0 ? a.env_adv[e] : 0.0;
+      R.esz[q] = a.env_group_size[e];
+      R.eadv[q] = a.env_adv[e];
     }
   }
 }
@@ -854,8 +941,11 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   for (int row = lane; row < rows; row += 32) {
     const int64_t kk = k0 + row;
     const int sl = row / M, r = row / P;
-    const double lp = sm.lp[row];   // computed in the row phase
-    const float ent = sm.ent[row];
+    const float sf = sm.s[row];
+    const double ls = log_f32_exact_exp(sf);
+    const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
+    const float ent = (float)ls - 0.6931471805599453f * (sm.t2[row] / sf);
+    sm.lp[row] = lp;
     if (a.tok_lp) a.tok_lp[kk] = (float)lp;
     if (a.tok_ent) a.tok_ent[kk] = ent;
     const bool on = (m.act[sl] & 2) != 0;
@@ -1009,18 +1099,22 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
     }
 }
 
-constexpr int kUnitWarps = kRowBufs;  // unit warp u owns row buffer u
-constexpr int kTmaThreadsFull = 64 + kTmaConsumers + 32 * kUnitWarps;  // producer, metadata,
-                                                                        // 8 row warps, unit warps
+constexpr int kBufWarps = kRowBufs;  // buffer warp m owns row buffer m (tiles i = m mod 4)
+constexpr int kTmaThreadsFull = 32 + kTmaConsumers + 32 * kBufWarps;  // producer, 8 row warps,
+                                                                        // 4 buffer warps
 
-// Synchronisation is mbarrier-only (no CTA-wide barrier in the main loop):
-//   full[s]     TMA producer -> row warps  (tx-count of the stage's bulk copies)
-//   empty[s]    row warps -> TMA producer  (8 arrivals: every warp finished reading stage s)
-//   metafull[b] metadata warp -> row warps and unit warp (tile metadata in buffer b)
-//   rowfull[b]  row warps -> unit warp     (8 arrivals: row partials of the tile complete)
-//   rowempty[b] unit warp -> row warps, metadata warp (buffer b may be overwritten)
-// Row warps only stream rows (never wait on a unit phase); the unit phase of tile i runs
-// on unit warp (i mod 4) and overlaps the row phases of the following tiles.
+// Roles (one CTA per SM, persistent over tiles of whole records):
+//   warp 0 lane 0   TMA producer: streams the tile's logits into a ring of `nstage` stages
+//                   with cp.async.bulk, completion by mbarrier tx-count (full[s]).
+//   warps 1..8      row warps: V-bin log-softmax / gather / entropy per row from shared
+//                   memory (LDS.128); results -> row buffer (it mod 4).
+//   warps 9..12     buffer warps: warp m owns row buffer m. It stages tile i's metadata
+//                   (token ids, old log-probs, slot activity / weights, unit advantages,
+//                   returns, values, group data) into the buffer, waits for the row
+//                   results, runs the unit phase, and meanwhile already has tile i+4's
+//                   metadata loads in flight.
+// Synchronisation is mbarrier-only: full[s]/empty[s] (producer <-> row warps),
+// metafull[b] (buffer warp -> row warps), rowfull[b] (row warps -> buffer warp).
 template <int MODE, typename LT>
 __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a, int nstage,
                                                                       uint32_t tile_bytes) {
@@ -1029,10 +1123,10 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
   __shared__ double s_red[kTmaThreadsFull / 32][RAW_COUNT];
   __shared__ bool s_last;
   __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4], metafull_bar[kRowBufs],
-      rowfull_bar[kRowBufs], rowempty_bar[kRowBufs];
+      rowfull_bar[kRowBufs];
 
   constexpr int V = 256;
-  constexpr int kCW = kTmaConsumers / 32;  // consumer warps
+  constexpr int kCW = kTmaConsumers / 32;  // row warps
   const int M = a.M, P = a.C * M;
   unsigned char* stage_base = smem_raw;
   unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
@@ -1046,7 +1140,6 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
     for (int b = 0; b < kRowBufs; ++b) {
       mbar_init(&metafull_bar[b], 1);
       mbar_init(&rowfull_bar[b], kCW);
-      mbar_init(&rowempty_bar[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_k = merge_consts(a);
@@ -1081,35 +1174,9 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
         }
       }
     }
-  } else if (warp == 1) {
-    // ---------------- metadata warp (loads one tile ahead) ----------------
-    MetaRegs cur, nxt;
-    int64_t tile = blockIdx.x, r0;
-    int nrec = 0;
-    if (tile < a.n_tiles) {
-      nrec = tile_recs(tile, r0);
-      meta_load<MODE>(a, r0, nrec, lane, cur);
-    }
-    for (int it = 0; tile < a.n_tiles; tile += gridDim.x, ++it) {
-      const int b = it % kRowBufs;
-      const int64_t ntile = tile + gridDim.x;
-      int64_t nr0 = 0;
-      int nnrec = 0;
-      if (ntile < a.n_tiles) {
-        nnrec = tile_recs(ntile, nr0);
-        meta_load<MODE>(a, nr0, nnrec, lane, nxt);
-      }
-      if (it >= kRowBufs) mbar_wait(&rowempty_bar[b], ((it / kRowBufs) - 1) & 1);
-      meta_store<MODE>(a, nrec, lane, cur, carve_meta(buf_base + b * rowbuf_bytes() + rowsmem_bytes(kTileRowsMax)));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&metafull_bar[b]);
-      cur = nxt;
-      nrec = nnrec;
-      r0 = nr0;
-    }
-  } else if (warp < 2 + kCW) {
+  } else if (warp <= kCW) {
     // ---------------- row warps ----------------
-    const int cwarp = warp - 2;
+    const int cwarp = warp - 1;
     const int sub = lane >> 3, l8 = lane & 7;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
@@ -1121,33 +1188,38 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
-      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // implies rowempty[b] was released
+      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // buffer b holds tile it's metadata
       mbar_wait(&full_bar[s], (it / nstage) & 1);
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
 #pragma unroll
-      for (int p = 0; p < kMaxPasses; ++p) {
-        const int rg = (p * kCW + cwarp) * 4;
-        if (rg >= rows) break;  // warp-uniform
-        const int row = rg + sub;
-        const bool valid = row < rows;
-        const LT* rowp = stage + (size_t)(valid ? row : rg) * V;
-        float s_, t_, c_;
-        row_fast_smem<LT>(rowp, l8, s_, t_, c_);
-        if (l8 == 0 && valid) {
-          const bool need = (mt.act[row / M] & 3) != 0;
-          double lp = 0.0;
-          float ent = 0.0f;
-          if (need) {
-            const int tok = mt.tok[row];
-            const float xt = sizeof(LT) == 4
-                                 ? (float)reinterpret_cast<const float*>(rowp)[tok]
-                                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rowp)[tok]);
-            const double ls = log_f32_exact_exp(s_);
-            lp = ((double)xt - (double)c_ * kLN2) - ls;
-            ent = (float)(ls - kLN2 * (double)t_ / (double)s_);
+      for (int p = 0; p < kMaxPasses; p += 2) {
+        const int rg0 = (p * kCW + cwarp) * 4, rg1 = ((p + 1) * kCW + cwarp) * 4;
+        if (rg0 >= rows) break;  // warp-uniform
+        const int row0 = rg0 + sub, row1 = rg1 + sub;
+        const LT* rp[2] = {stage + (size_t)(row0 < rows ? row0 : rg0) * V,
+                           stage + (size_t)(row1 < rows ? row1 : rg0) * V};
+        float s_[2], t_[2], c_[2];
+        if (rg1 < rows)
+          rows_fast_smem<LT, 2>(rp, l8, s_, t_, c_);
+        else
+          rows_fast_smem<LT, 1>(rp, l8, s_, t_, c_);
+        if (l8 == 0) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int row = q ? row1 : row0;
+            if (row >= rows || (q && rg1 >= rows)) continue;
+            const bool need = (mt.act[row / M] & 3) != 0;
+            float xt = 0.0f;
+            if (need) {
+              const int tok = mt.tok[row];
+              xt = sizeof(LT) == 4 ? (float)reinterpret_cast<const float*>(rp[q])[tok]
+                                   : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
+            }
+            sm.s[row] = need ? s_[q] : 1.0f;
+            sm.t2[row] = need ? t_[q] : 0.0f;
+            sm.c[row] = c_[q];
+            sm.xt[row] = xt;
           }
-          sm.lp[row] = lp;
-          sm.ent[row] = ent;
         }
       }
       __syncwarp();
@@ -1157,22 +1229,42 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
       }
     }
   } else {
-    // ---------------- unit warps ----------------
-    const int uw = warp - 2 - kCW;
-    int it = uw;
-    for (int64_t tile = blockIdx.x + (int64_t)uw * gridDim.x; tile < a.n_tiles;
-         tile += (int64_t)kUnitWarps * gridDim.x, it += kUnitWarps) {
-      const int b = it % kRowBufs;  // == uw
-      unsigned char* bb = buf_base + b * rowbuf_bytes();
-      const RowSmem sm = carve_rows(bb, kTileRowsMax);
-      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
-      int64_t r0;
-      const int nrec = tile_recs(tile, r0);
-      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);
+    // ---------------- buffer warps: metadata in, unit phase out ----------------
+    const int b = warp - 1 - kCW;
+    unsigned char* bb = buf_base + b * rowbuf_bytes();
+    const RowSmem sm = carve_rows(bb, kTileRowsMax);
+    const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
+    const int64_t stride = (int64_t)kBufWarps * gridDim.x;
+    int64_t tile = blockIdx.x + (int64_t)b * gridDim.x;
+    int it = b;
+    MetaRegs regs;
+    int64_t r0 = 0;
+    int nrec = 0;
+    if (tile < a.n_tiles) {
+      nrec = tile_recs(tile, r0);
+      meta_load<MODE>(a, r0, nrec, lane, regs);
+      meta_store<MODE>(a, nrec, lane, regs, mt);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&metafull_bar[b]);
+    }
+    for (; tile < a.n_tiles; tile += stride, it += kBufWarps) {
+      const int64_t ntile = tile + stride;
+      int64_t nr0 = 0;
+      int nnrec = 0;
+      if (ntile < a.n_tiles) {  // next tile's metadata loads go out before the unit phase
+        nnrec = tile_recs(ntile, nr0);
+        meta_load<MODE>(a, nr0, nnrec, lane, regs);
+      }
       mbar_wait(&rowfull_bar[b], (it / kRowBufs) & 1);
       unit_phase_smem<MODE>(a, k, acc, sm, mt, r0, nrec, lane);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&rowempty_bar[b]);
+      if (ntile < a.n_tiles) {
+        meta_store<MODE>(a, nnrec, lane, regs, mt);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&metafull_bar[b]);
+      }
+      r0 = nr0;
+      nrec = nnrec;
     }
   }
   __syncthreads();
