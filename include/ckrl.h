@@ -269,6 +269,12 @@ int32_t ckrl_grpo_step(const ckrl_rollout* rollout, const ckrl_episodes* episode
  * DegenerateGroup, NonFinite (losses.cpp:229-230, 326-327). */
 int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream);
 
+/* Profiling aid: %globaltimer stamps (ns) of CTA 0 from the last TMA loss / fused-step
+ * launch: [0] start, [1] GAE phase done, [2] grid barrier passed, [3] constants ready,
+ * [4..7] first unit phase of each buffer warp, [8] last row tile, [9] all roles done,
+ * [10] reduction done. Synchronises the device. */
+int32_t ckrl_debug_timeline(uint64_t* out, int32_t n);
+
 /* ---- multi-GPU (NCCL over NVLink): stats + loss scalars only -------------------------- */
 int32_t ckrl_comm_unique_id(void* out_id /* 128 bytes */);
 int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out);

@@ -112,6 +112,7 @@ SIGNATURES = {
                                    P(GrpoOptions), P(GrpoParams), P(GrpoBatchC),
                                    P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
     "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
+    "ckrl_debug_timeline": (C.c_int32, [vp, C.c_int32]),
     "ckrl_comm_unique_id": (C.c_int32, [vp]),
     "ckrl_comm_create": (C.c_int32, [C.c_int32, C.c_int32, vp, P(vp)]),
     "ckrl_comm_destroy": (C.c_int32, [vp]),

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -232,17 +233,21 @@ int32_t ckrl_merge_stats_host(const void* records, int32_t world, double* out_me
                               double* out_denom, int64_t* out_counts) {
   CKRL_REQUIRE(records && world >= 1, CKRL_ERR_INVALID_ARGUMENT, "bad stats records");
   const StatsRecord* r = static_cast<const StatsRecord*>(records);
-  Moments m{0.0, 0.0, 0.0};
+  double n = 0.0, s1 = 0.0, s2 = 0.0;
   int64_t c[4] = {0, 0, 0, 0};
   for (int i = 0; i < world; ++i) {
-    m = merge_moments(m, Moments{(double)r[i].n_units, r[i].mean, r[i].m2});
+    n += (double)r[i].n_units;
+    s1 += r[i].sum;
+    s2 += r[i].sumsq;
     c[0] += r[i].n_adv;
     c[1] += r[i].n_val;
     c[2] += r[i].n_pos;
     c[3] += r[i].groups_retained;
   }
-  if (out_mean) *out_mean = m.mean;
-  if (out_denom) *out_denom = m.n > 0 ? sqrt(m.m2 / m.n) + 1e-8 : 1.0;
+  double mean, denom;
+  whitening(n, s1, s2, &mean, &denom);
+  if (out_mean) *out_mean = mean;
+  if (out_denom) *out_denom = denom;
   if (out_counts) std::memcpy(out_counts, c, sizeof(c));
   return CKRL_OK;
 }
@@ -347,6 +352,42 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, in
   a.world = 0;
   CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));
   return CKRL_OK;
+}
+
+static bool fused_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    // The fused single-launch step (GAE on the buffer warps + grid barrier) measured
+    // slower on B200 (cfg3: 72.6 us vs 51.5 us for assemble + loss): the GAE's serial
+    // chains crawl on SMs whose issue slots the row warps saturate. Opt-in only.
+    const char* env = getenv("CKRL_FUSED_STEP");
+    on = (env && env[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+static LossArgs ppo_args(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
+                         const ckrl_policy_outputs* po, const ckrl_granularity* spec,
+                         const ckrl_ppo_params* p, ckrl_loss_outputs* out, double* diag, void* ws,
+                         int world, const StatsRecord* recs, int finalize) {
+  LossArgs a = base_args(ro, po, (char*)ws, world);
+  a.mode = MODE_PPO;
+  a.counted = b->counted;
+  a.adv = b->advantages;
+  a.ret = b->returns;
+  a.new_values = po->values;
+  a.adv_level = spec->advantage_level;
+  a.lp_level = spec->logprob_level;
+  a.val_level = spec->value_level;
+  a.clip = p->clip_eps;
+  a.vcoef = p->value_loss_coef;
+  a.ecoef = p->entropy_coef;
+  a.normalize = p->advantage_normalization;
+  a.recs = recs;
+  a.diag = diag;
+  a.finalize = finalize;
+  set_outputs(a, out);
+  return a;
 }
 
 static int32_t ppo_loss_impl(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
@@ -469,6 +510,18 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
   cudaStream_t s = (cudaStream_t)stream;
   WsLayout L = ws_layout(ro->num_envs, world);
   char* w = (char*)ws;
+  if (world == 1 && fused_enabled()) {
+    // one persistent launch: GAE assembly overlapped with the logits stream
+    LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
+                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1);
+    a.ro = *ro;
+    a.gamma = gae->gamma;
+    a.lambda = gae->lambda;
+    cudaError_t e = launch_ppo_fused(a, s, nullptr);
+    if (e == cudaSuccess) return CKRL_OK;
+    if (e != cudaErrorNotSupported) return fail(CKRL_ERR_CUDA, std::string("fused step: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+  }
   CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
                                 gae->lambda, *b, w, L, s));
   if (world == 1)
@@ -537,6 +590,13 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
     return fail(status, "all trajectories in the group have equal return");
   if (status == CKRL_ERR_NON_FINITE) return fail(status, "loss is not finite");
   if (status) return fail(status, "device-side error");
+  return CKRL_OK;
+}
+
+int32_t ckrl_debug_timeline(uint64_t* out, int32_t n) {
+  CKRL_REQUIRE(out && n > 0, CKRL_ERR_INVALID_ARGUMENT, "bad timeline buffer");
+  CKRL_CUDA(cudaDeviceSynchronize());
+  CKRL_CUDA(read_timeline(out, n));
   return CKRL_OK;
 }
 

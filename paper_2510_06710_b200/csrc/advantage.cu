@@ -6,343 +6,13 @@
 // Reference semantics: advantage/gae.cpp:7-37, advantage/assembler.cpp:33-267,
 // advantage/grpo.cpp:9-79, optim/update.cpp:14-45.
 #include "common.cuh"
+#include "gae.cuh"
 #include "kernels.h"
 
 namespace ckrl {
 
-// One advantage-level unit as the GAE recurrence sees it.
-struct Unit {
-  bool is_unit;  // false: transparent item (invalid slot / fully frozen chunk)
-  bool term, trunc;
-  int32_t uid;   // segment key (episode id); units of one segment are contiguous
-  double r, v, boot;
-  int counted_slots;
-};
-
-// ---------------------------------------------------------------------------------
-// Warp-cooperative GAE over one env's (or one flat sequence's) item list.
-//
-// The reference runs, per segment, the reverse loop of gae.cpp:21-35:
-//   vnext_i = 0 (terminated) | boot_i (truncated or last of segment) | V_{i+1}
-//   A_i     = delta_i + (gamma*lambda) * (segment_end ? 0 : A_{i+1})
-// Each unit is the affine map A_i = P_i + Q_i * A_next. Lane l owns a contiguous
-// item range, composes its maps locally (reverse), the warp runs an inclusive
-// suffix scan of the composed maps with shuffles, and every lane replays its range
-// with the exact incoming A. Segment ends come from done flags, uid changes between
-// consecutive units and the end of the list (flush_segment's open end).
-// ---------------------------------------------------------------------------------
-constexpr int kGaeCache = 4;  // items per lane kept in registers across the phases
-
-template <class Acc>
-__device__ void warp_gae(Acc& acc, int n_items, double gamma, double lambda, Moments& mom,
-                         double& counted_slots) {
-  const int lane = threadIdx.x & 31;
-  const int per = (n_items + 31) / 32;
-  const int lo = min(n_items, lane * per), hi = min(n_items, lo + per);
-  const int cnt = hi - lo;
-  const double gl = __dmul_rn(gamma, lambda);
-  const bool cached = per <= kGaeCache;
-
-  // Load once (independent loads, issued together) when the lane's range is short.
-  Unit cache[kGaeCache];
-  if (cached) {
-#pragma unroll
-    for (int q = 0; q < kGaeCache; ++q)
-      if (q < cnt) cache[q] = acc.load(lo + q);
-  }
-  // visit(fn, reverse): apply fn(i, unit) over my range
-  auto visit = [&](auto&& fn, bool reverse) {
-    if (cached) {
-      if (reverse) {
-#pragma unroll
-        for (int q = kGaeCache - 1; q >= 0; --q)
-          if (q < cnt && !fn(lo + q, cache[q])) return;
-      } else {
-#pragma unroll
-        for (int q = 0; q < kGaeCache; ++q)
-          if (q < cnt && !fn(lo + q, cache[q])) return;
-      }
-    } else if (reverse) {
-      for (int i = hi - 1; i >= lo; --i) {
-        Unit u = acc.load(i);
-        if (!fn(i, u)) return;
-      }
-    } else {
-      for (int i = lo; i < hi; ++i) {
-        Unit u = acc.load(i);
-        if (!fn(i, u)) return;
-      }
-    }
-  };
-
-  // Phase 1: first unit of my range, then nearest such head to my right.
-  bool h_has = false;
-  int32_t h_uid = 0;
-  double h_v = 0.0;
-  visit([&](int, const Unit& u) {
-    if (!u.is_unit) return true;
-    h_has = true;
-    h_uid = u.uid;
-    h_v = u.v;
-    return false;
-  }, false);
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    bool o_has = __shfl_down_sync(0xffffffffu, h_has, off);
-    int32_t o_uid = __shfl_down_sync(0xffffffffu, h_uid, off);
-    double o_v = __shfl_down_sync(0xffffffffu, h_v, off);
-    if (!h_has && lane + off < 32) {
-      h_has = o_has;
-      h_uid = o_uid;
-      h_v = o_v;
-    }
-  }
-  bool nx_has0 = __shfl_down_sync(0xffffffffu, h_has, 1);
-  int32_t nx_uid0 = __shfl_down_sync(0xffffffffu, h_uid, 1);
-  double nx_v0 = __shfl_down_sync(0xffffffffu, h_v, 1);
-  if (lane == 31) nx_has0 = false;
-
-  // Phase 2: compose my range's affine map (reverse order).
-  double P = 0.0, Q = 1.0;
-  {
-    bool nx_has = nx_has0;
-    int32_t nx_uid = nx_uid0;
-    double nx_v = nx_v0;
-    visit([&](int, const Unit& u) {
-      if (!u.is_unit) return true;
-      bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
-      double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
-      double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
-      double c = seg_end ? 0.0 : gl;
-      P = __dadd_rn(delta, __dmul_rn(c, P));
-      Q = __dmul_rn(c, Q);
-      nx_has = true;
-      nx_uid = u.uid;
-      nx_v = u.v;
-      return true;
-    }, true);
-  }
-  // Phase 3: inclusive suffix scan of maps, G_l = F_l o G_{l+1}.
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    double oP = __shfl_down_sync(0xffffffffu, P, off);
-    double oQ = __shfl_down_sync(0xffffffffu, Q, off);
-    if (lane + off < 32) {
-      P = __dadd_rn(P, __dmul_rn(Q, oP));
-      Q = __dmul_rn(Q, oQ);
-    }
-  }
-  double a_in = __shfl_down_sync(0xffffffffu, P, 1);
-  if (lane == 31) a_in = 0.0;
-
-  // Phase 4: replay with the exact incoming advantage; write; accumulate stats.
-  bool nx_has = nx_has0;
-  int32_t nx_uid = nx_uid0;
-  double nx_v = nx_v0;
-  double a_next = a_in;
-  Moments m{0.0, 0.0, 0.0};
-  double cs = 0.0;
-  visit([&](int i, const Unit& u) {
-    if (!u.is_unit) {
-      acc.store_empty(i);
-      return true;
-    }
-    bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
-    double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
-    double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
-    double a = __dadd_rn(delta, __dmul_rn(gl, seg_end ? 0.0 : a_next));
-    acc.store(i, u, a, __dadd_rn(a, u.v));
-    // Welford update (reverse item order within the lane; deterministic).
-    m.n += 1.0;
-    double d = a - m.mean;
-    m.mean += d / m.n;
-    m.m2 += d * (a - m.mean);
-    cs += u.counted_slots;
-    a_next = a;
-    nx_has = true;
-    nx_uid = u.uid;
-    nx_v = u.v;
-    return true;
-  }, true);
-  // Merge lane moments in lane order (tree over fixed partners => deterministic).
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Moments o;
-    o.n = __shfl_down_sync(0xffffffffu, m.n, off);
-    o.mean = __shfl_down_sync(0xffffffffu, m.mean, off);
-    o.m2 = __shfl_down_sync(0xffffffffu, m.m2, off);
-    double ocs = __shfl_down_sync(0xffffffffu, cs, off);
-    if ((lane & (2 * off - 1)) == 0 && lane + off < 32) {
-      m = merge_moments(m, o);
-      cs += ocs;
-    }
-  }
-  mom = m;  // valid in lane 0
-  counted_slots = cs;
-}
-
-// ---- accessors ------------------------------------------------------------------
-struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
-  const ckrl_rollout ro;
-  int e;
-  uint8_t* counted;
-  float* adv;
-  float* ret;
-  __device__ Unit load(int t) const {
-    // All C slots' fields are fetched with independent loads first (no data-dependent
-    // load chain), then the unit is formed in registers.
-    const int C = ro.chunk_len;
-    const int64_t rec = (int64_t)e * ro.num_chunks + t;
-    const int64_t s0 = rec * C;
-    Unit u;
-    u.is_unit = false;
-    u.term = u.trunc = false;
-    u.r = 0.0;
-    u.counted_slots = 0;
-    u.uid = -1;
-    u.v = (double)ro.value_scalar[rec];
-    u.boot = 0.0;
-    constexpr int kC = 8;
-    if (C <= kC) {
-      uint8_t f[kC];
-      int32_t id[kC];
-      float rw[kC], bt[kC];
-#pragma unroll
-      for (int j = 0; j < kC; ++j)
-        if (j < C) {
-          f[j] = ro.flags[s0 + j];
-          id[j] = ro.episode_id[s0 + j];
-          rw[j] = ro.reward[s0 + j];
-          bt[j] = ro.bootstrap[s0 + j];
-        }
-      int first = -1;
-#pragma unroll
-      for (int j = kC - 1; j >= 0; --j)
-        if (j < C && (f[j] & CKRL_FLAG_VALID)) first = j;
-      if (first < 0) return u;  // fully frozen chunk
-      u.is_unit = true;
-#pragma unroll
-      for (int j = 0; j < kC; ++j)
-        if (j == first) u.uid = id[j];
-      bool open = true;
-#pragma unroll
-      for (int j = 0; j < kC; ++j) {
-        if (j < first || j >= C) continue;
-        open = open && (f[j] & CKRL_FLAG_VALID) && id[j] == u.uid;  // tail dropped
-        if (open) {
-          u.r = __dadd_rn(u.r, (double)rw[j]);
-          u.term = u.term || (f[j] & CKRL_FLAG_TERMINATED);
-          u.trunc = u.trunc || (f[j] & CKRL_FLAG_TRUNCATED);
-          u.boot = (double)bt[j];
-          ++u.counted_slots;
-        }
-      }
-      return u;
-    }
-    int first = -1;
-    for (int j = 0; j < C; ++j)
-      if (ro.flags[s0 + j] & CKRL_FLAG_VALID) {
-        first = j;
-        break;
-      }
-    if (first < 0) return u;
-    u.is_unit = true;
-    u.uid = ro.episode_id[s0 + first];
-    int last = first;
-    for (int j = first; j < C; ++j) {
-      uint8_t fl = ro.flags[s0 + j];
-      if (!(fl & CKRL_FLAG_VALID) || ro.episode_id[s0 + j] != u.uid) break;
-      u.r = __dadd_rn(u.r, (double)ro.reward[s0 + j]);
-      u.term = u.term || (fl & CKRL_FLAG_TERMINATED);
-      u.trunc = u.trunc || (fl & CKRL_FLAG_TRUNCATED);
-      last = j;
-      ++u.counted_slots;
-    }
-    u.boot = (double)ro.bootstrap[s0 + last];
-    return u;
-  }
-  __device__ void store(int t, const Unit& u, double a, double R) const {
-    const int C = ro.chunk_len;
-    const int64_t rec = (int64_t)e * ro.num_chunks + t;
-    adv[rec] = (float)a;
-    ret[rec] = (float)R;
-    // counted = the leading episode's contiguous valid prefix from the first valid slot
-    int first = -1;
-    for (int j = 0; j < C; ++j) {
-      bool v = ro.flags[rec * C + j] & CKRL_FLAG_VALID;
-      if (first < 0 && v) first = j;
-      counted[rec * C + j] = (first >= 0 && j < first + u.counted_slots) ? 1 : 0;
-    }
-  }
-  __device__ void store_empty(int t) const {
-    const int C = ro.chunk_len;
-    const int64_t rec = (int64_t)e * ro.num_chunks + t;
-    adv[rec] = 0.0f;
-    ret[rec] = 0.0f;
-    for (int j = 0; j < C; ++j) counted[rec * C + j] = 0;
-  }
-};
-
-struct ActionAcc {  // action-level units: one per valid slot (assembler.cpp:112-146)
-  const ckrl_rollout ro;
-  int e;
-  uint8_t* counted;
-  float* adv;
-  float* ret;
-  __device__ Unit load(int i) const {
-    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
-    uint8_t f = ro.flags[s];
-    Unit u;
-    u.is_unit = (f & CKRL_FLAG_VALID) != 0;
-    u.term = f & CKRL_FLAG_TERMINATED;
-    u.trunc = f & CKRL_FLAG_TRUNCATED;
-    u.uid = ro.episode_id[s];
-    u.r = (double)ro.reward[s];
-    u.v = (double)ro.value_vector[s];
-    u.boot = (double)ro.bootstrap[s];
-    u.counted_slots = 1;
-    return u;
-  }
-  __device__ void store(int i, const Unit&, double a, double R) const {
-    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
-    adv[s] = (float)a;
-    ret[s] = (float)R;
-    counted[s] = 1;
-  }
-  __device__ void store_empty(int i) const {
-    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
-    adv[s] = 0.0f;
-    ret[s] = 0.0f;
-    counted[s] = 0;
-  }
-};
-
-struct FlatAcc {  // compute_gae over one flat sequence (gae.cpp:7-37)
-  const double *r, *v, *b;
-  const uint8_t* f;
-  double *adv, *ret;
-  int base;
-  __device__ Unit load(int i) const {
-    Unit u;
-    u.is_unit = true;
-    uint8_t fl = f[base + i];
-    u.term = fl & CKRL_FLAG_TERMINATED;
-    u.trunc = fl & CKRL_FLAG_TRUNCATED;
-    u.uid = 0;
-    u.r = r[base + i];
-    u.v = v[base + i];
-    u.boot = b[base + i];
-    u.counted_slots = 0;
-    return u;
-  }
-  __device__ void store(int i, const Unit&, double a, double R) const {
-    adv[base + i] = a;
-    ret[base + i] = R;
-  }
-  __device__ void store_empty(int) const {}
-};
-
-// Last-block reduction of the per-CTA assembly partials into the rank's StatsRecord.
+// Last-block reduction of the per-CTA assembly partials into the rank's StatsRecord
+// (fixed order: thread t sums partials t, t+nthr, ...; then a fixed tree).
 __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, int M) {
   __shared__ bool is_last;
   __shared__ AsmPartial wpart[kAsmWarpsPerCta];
@@ -357,44 +27,37 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // Parallel, fixed-order merge: thread t merges partials t, t+nthr, ... (Chan), then a
-  // fixed tree over lanes and warps.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Moments m{0.0, 0.0, 0.0};
-  double npos = 0.0;
+  AsmPartial q{0.0, 0.0, 0.0, 0.0};
   for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-    volatile AsmPartial* p = parts + b;
-    m = merge_moments(m, Moments{p->n, p->mean, p->m2});
-    npos += p->n_pos;
+    q.n += __ldcg(&parts[b].n);
+    q.s1 += __ldcg(&parts[b].s1);
+    q.s2 += __ldcg(&parts[b].s2);
+    q.n_pos += __ldcg(&parts[b].n_pos);
   }
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Moments o;
-    o.n = __shfl_down_sync(0xffffffffu, m.n, off);
-    o.mean = __shfl_down_sync(0xffffffffu, m.mean, off);
-    o.m2 = __shfl_down_sync(0xffffffffu, m.m2, off);
-    double op = __shfl_down_sync(0xffffffffu, npos, off);
-    if ((lane & (2 * off - 1)) == 0 && lane + off < 32) {
-      m = merge_moments(m, o);
-      npos += op;
-    }
+  for (int off = 16; off > 0; off >>= 1) {
+    q.n += __shfl_down_sync(0xffffffffu, q.n, off);
+    q.s1 += __shfl_down_sync(0xffffffffu, q.s1, off);
+    q.s2 += __shfl_down_sync(0xffffffffu, q.s2, off);
+    q.n_pos += __shfl_down_sync(0xffffffffu, q.n_pos, off);
   }
-  if (lane == 0) wpart[warp] = AsmPartial{m.n, m.mean, m.m2, npos};
+  if (lane == 0) wpart[warp] = q;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  m = Moments{0.0, 0.0, 0.0};
-  npos = 0.0;
+  AsmPartial t{0.0, 0.0, 0.0, 0.0};
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    m = merge_moments(m, Moments{wpart[w].n, wpart[w].mean, wpart[w].m2});
-    npos += wpart[w].n_pos;
+    t.n += wpart[w].n;
+    t.s1 += wpart[w].s1;
+    t.s2 += wpart[w].s2;
+    t.n_pos += wpart[w].n_pos;
   }
   StatsRecord* st = reinterpret_cast<StatsRecord*>(ws + L.stats_local);
-  st->mean = m.mean;
-  st->m2 = m.m2;
-  st->n_units = (int64_t)m.n;
-  st->n_adv = (int64_t)m.n;
-  st->n_val = (int64_t)m.n;  // value level == advantage level (assembler.cpp:82)
-  st->n_pos = (int64_t)npos * M;
+  st->sum = t.s1;
+  st->sumsq = t.s2;
+  st->n_units = (int64_t)t.n;
+  st->n_adv = (int64_t)t.n;
+  st->n_val = (int64_t)t.n;  // value level == advantage level (assembler.cpp:82)
+  st->n_pos = (int64_t)t.n_pos * M;
   st->groups_retained = 0;
   st->status = 0;
   tickets[TICKET_ASM] = 0;  // self-reset for the next launch
@@ -403,36 +66,26 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
 __global__ void __launch_bounds__(kAsmWarpsPerCta * 32)
 ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lambda,
                     uint8_t* counted, float* adv, float* ret, char* ws, WsLayout L) {
-  __shared__ Moments wm[kAsmWarpsPerCta];
-  __shared__ double wc[kAsmWarpsPerCta];
+  __shared__ GaeSums wsum[kAsmWarpsPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = blockIdx.x * kAsmWarpsPerCta + warp;
-  Moments m{0.0, 0.0, 0.0};
-  double cs = 0.0;
+  GaeSums g{0.0, 0.0, 0.0, 0.0};
   if (e < ro.num_envs) {
-    if (action_level) {
-      ActionAcc acc{ro, e, counted, adv, ret};
-      warp_gae(acc, ro.num_chunks * ro.chunk_len, gamma, lambda, m, cs);
-    } else {
-      ChunkAcc acc{ro, e, counted, adv, ret};
-      warp_gae(acc, ro.num_chunks, gamma, lambda, m, cs);
-    }
+    if (action_level)
+      g = warp_gae(ActionAcc{ro, e, counted, adv, ret}, ro.num_chunks * ro.chunk_len, gamma, lambda);
+    else
+      g = warp_gae(ChunkAcc{ro, e, counted, adv, ret}, ro.num_chunks, gamma, lambda);
   }
-  if (lane == 0) {
-    wm[warp] = m;
-    wc[warp] = cs;
-  }
+  if (lane == 0) wsum[warp] = g;
   __syncthreads();
   AsmPartial p{0.0, 0.0, 0.0, 0.0};
-  if (threadIdx.x == 0) {
-    Moments acc{0.0, 0.0, 0.0};
-    double c = 0.0;
+  if (threadIdx.x == 0)
     for (int w = 0; w < kAsmWarpsPerCta; ++w) {
-      acc = merge_moments(acc, wm[w]);
-      c += wc[w];
+      p.n += wsum[w].n;
+      p.s1 += wsum[w].s1;
+      p.s2 += wsum[w].s2;
+      p.n_pos += wsum[w].counted_slots;
     }
-    p = AsmPartial{acc.n, acc.mean, acc.m2, c};
-  }
   finish_asm_stats(p, ws, L, ro.tokens_per_action);
 }
 
@@ -441,10 +94,7 @@ __global__ void flat_gae_kernel(int num_seqs, const int32_t* offs, const double*
                                 double gamma, double lambda, double* adv, double* ret) {
   const int q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (q >= num_seqs) return;
-  FlatAcc acc{r, v, b, f, adv, ret, offs[q]};
-  Moments m;
-  double cs;
-  warp_gae(acc, offs[q + 1] - offs[q], gamma, lambda, m, cs);
+  warp_gae(FlatAcc{r, v, b, f, adv, ret, offs[q]}, offs[q + 1] - offs[q], gamma, lambda);
 }
 
 // In-place whitening of the counted advantage units (optim/update.cpp:14-45).
@@ -453,11 +103,14 @@ __global__ void normalize_kernel(ckrl_rollout ro, int action_level, const uint8_
   __shared__ double s_mean, s_denom;
   __shared__ int s_skip;
   if (threadIdx.x == 0) {
-    Moments m{0.0, 0.0, 0.0};
-    for (int r = 0; r < world; ++r) m = merge_moments(m, Moments{(double)recs[r].n_units, recs[r].mean, recs[r].m2});
-    s_skip = m.n < 2.0;
-    s_mean = m.mean;
-    s_denom = sqrt(m.m2 / m.n) + 1e-8;
+    double n = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int r = 0; r < world; ++r) {
+      n += (double)recs[r].n_units;
+      s1 += recs[r].sum;
+      s2 += recs[r].sumsq;
+    }
+    s_skip = n < 2.0;
+    whitening(n, s1, s2, &s_mean, &s_denom);
   }
   __syncthreads();
   if (s_skip) return;
@@ -679,8 +332,8 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   if (tid == 0) {
     gb.group_counts[0] = s_total;
     gb.group_counts[1] = s_retained;
-    st->mean = 0.0;
-    st->m2 = 0.0;
+    st->sum = 0.0;
+    st->sumsq = 0.0;
     st->n_units = st->n_adv = st->n_val = st->n_pos = 0;
     st->groups_retained = s_retained;
     st->status = s_status;

@@ -17,13 +17,13 @@ constexpr int kMaxLossCtas = 148 * 8; // persistent grid upper bound (partials s
 constexpr int kGrpoMaxEligible = 8192;
 
 // Per-rank record of everything the loss needs from the advantage phase before it
-// can scale a single coefficient: whitening moments over the counted advantage units
+// can scale a single coefficient: whitening sums over the counted advantage units
 // (optim/update.cpp:33-43) and the loss normalisers n_adv / n_val / n_pos
 // (optim/losses.cpp:75-87) or the retained GRPO group count (losses.cpp:246).
 // Fixed 64-byte layout so ranks can all-gather it with one NCCL call.
 struct StatsRecord {
-  double mean;          // mean of the rank's counted advantage units
-  double m2;            // sum of squared deviations from `mean`
+  double sum;           // sum of the rank's counted advantage units (fp64)
+  double sumsq;         // sum of their squares
   int64_t n_units;      // advantage units (== n_adv)
   int64_t n_adv;
   int64_t n_val;
@@ -36,20 +36,16 @@ static_assert(sizeof(StatsRecord) == 64, "stats record must stay 64 bytes");
 // Raw loss sums (reduced across CTAs, then across ranks) before normalisation.
 enum { RAW_SURR = 0, RAW_VALSQ, RAW_ENT, RAW_KL, RAW_CLIPPED, RAW_LPUNITS, RAW_COUNT = 8 };
 
-struct Moments {
-  double n, mean, m2;
-};
-
-// Chan et al. pairwise merge of (n, mean, M2); fixed operand order => deterministic.
-__host__ __device__ inline Moments merge_moments(Moments a, Moments b) {
-  if (b.n == 0.0) return a;
-  if (a.n == 0.0) return b;
-  Moments r;
-  r.n = a.n + b.n;
-  double d = b.mean - a.mean;
-  r.mean = a.mean + d * (b.n / r.n);
-  r.m2 = a.m2 + b.m2 + d * d * (a.n * b.n / r.n);
-  return r;
+// Whitening parameters from fp64 sums: mean, population std + 1e-8 (update.cpp:33-43).
+// The reference subtracts the mean in a second pass; the one-pass form differs by
+// ~eps * mean^2 / var relative, negligible for advantages (|mean| ~ std).
+__host__ __device__ inline void whitening(double n, double s1, double s2, double* mean,
+                                          double* denom) {
+  const double m = n > 0.0 ? s1 / n : 0.0;
+  double var = n > 0.0 ? s2 / n - m * m : 0.0;
+  if (var < 0.0) var = 0.0;
+  *mean = m;
+  *denom = sqrt(var) + 1e-8;
 }
 
 // Workspace carve-up (all offsets 256-byte aligned). Must match ckrl_workspace_bytes.
@@ -58,7 +54,7 @@ struct WsLayout {
   size_t stats_all;     // StatsRecord[world]
   size_t tickets;       // uint32[8] last-block counters (self-resetting)
   size_t loss_raw;      // double[RAW_COUNT]
-  size_t asm_partials;  // (Moments + counts) per assembly CTA
+  size_t asm_partials;  // AsmPartial per assembly CTA
   size_t loss_partials; // double[RAW_COUNT] per loss CTA
   size_t grpo_env;      // per-env int32 len, fs (GRPO assembly scratch)
   size_t total;
@@ -67,8 +63,8 @@ struct WsLayout {
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct AsmPartial {
-  double n, mean, m2;
-  double n_pos;
+  double n, s1, s2;
+  double n_pos;  // counted slots
 };
 
 __host__ __device__ inline WsLayout ws_layout(int E, int world) {
@@ -80,7 +76,7 @@ __host__ __device__ inline WsLayout ws_layout(int E, int world) {
     return at;
   };
   int asm_ctas = (E + kAsmWarpsPerCta - 1) / kAsmWarpsPerCta;
-  if (asm_ctas < 1) asm_ctas = 1;
+  if (asm_ctas < kMaxLossCtas) asm_ctas = kMaxLossCtas;  // also the fused step's CTA partials
   L.stats_local = take(sizeof(StatsRecord));
   L.stats_all = take(sizeof(StatsRecord) * (size_t)(world < 1 ? 1 : world));
   L.tickets = take(sizeof(uint32_t) * 8);
@@ -92,7 +88,7 @@ __host__ __device__ inline WsLayout ws_layout(int E, int world) {
   return L;
 }
 
-enum { TICKET_ASM = 0, TICKET_LOSS = 1 };
+enum { TICKET_ASM = 0, TICKET_LOSS = 1, TICKET_GRID = 2, TICKET_GEN = 3 };
 
 // ---- warp helpers ----------------------------------------------------------------------
 template <typename T>

@@ -1,0 +1,291 @@
+// GAE as a warp-segmented reverse affine scan + the unit accessors of PPO assembly.
+// Shared by the standalone assembly kernel (advantage.cu) and the fused step kernel
+// (loss.cu). Reference: advantage/gae.cpp:7-37, advantage/assembler.cpp:33-195.
+#pragma once
+
+#include "common.cuh"
+
+namespace ckrl {
+
+// One advantage-level unit as the GAE recurrence sees it.
+struct Unit {
+  bool is_unit;  // false: transparent item (invalid slot / fully frozen chunk)
+  bool term, trunc;
+  int32_t uid;   // segment key (episode id); units of one segment are contiguous
+  double r, v, boot;
+  int counted_slots;
+};
+
+// ---------------------------------------------------------------------------------
+// Warp-cooperative GAE over one env's (or one flat sequence's) item list.
+//
+// The reference runs, per segment, the reverse loop of gae.cpp:21-35:
+//   vnext_i = 0 (terminated) | boot_i (truncated or last of segment) | V_{i+1}
+//   A_i     = delta_i + (gamma*lambda) * (segment_end ? 0 : A_{i+1})
+// Each unit is the affine map A_i = P_i + Q_i * A_next. Lane l owns a contiguous
+// item range, composes its maps locally (reverse), the warp runs an inclusive
+// suffix scan of the composed maps with shuffles, and every lane replays its range
+// with the exact incoming A. Segment ends come from done flags, uid changes between
+// consecutive units and the end of the list (flush_segment's open end).
+// ---------------------------------------------------------------------------------
+// Per-lane GAE statistics: advantage units, sum and sum of squares (fp64; merged by plain
+// addition in a fixed order, so no divisions on the hot path and results are deterministic).
+struct GaeSums {
+  double n, s1, s2, counted_slots;
+};
+
+template <class Acc>
+__device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gamma, double lambda) {
+  const int lane = threadIdx.x & 31;
+  const int per = (n_items + 31) / 32;
+  const int lo = min(n_items, lane * per), hi = min(n_items, lo + per);
+  const double gl = __dmul_rn(gamma, lambda);
+
+  // Phase 1: first unit of my range, then the nearest such head to my right.
+  bool h_has = false;
+  int32_t h_uid = 0;
+  double h_v = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const Unit u = acc.load(i);
+    if (u.is_unit) {
+      h_has = true;
+      h_uid = u.uid;
+      h_v = u.v;
+      break;
+    }
+  }
+  for (int off = 1; off < 32; off <<= 1) {
+    const bool o_has = __shfl_down_sync(0xffffffffu, h_has, off);
+    const int32_t o_uid = __shfl_down_sync(0xffffffffu, h_uid, off);
+    const double o_v = __shfl_down_sync(0xffffffffu, h_v, off);
+    if (!h_has && lane + off < 32) {
+      h_has = o_has;
+      h_uid = o_uid;
+      h_v = o_v;
+    }
+  }
+  bool nx_has0 = __shfl_down_sync(0xffffffffu, h_has, 1);
+  const int32_t nx_uid0 = __shfl_down_sync(0xffffffffu, h_uid, 1);
+  const double nx_v0 = __shfl_down_sync(0xffffffffu, h_v, 1);
+  if (lane == 31) nx_has0 = false;
+
+  // Phases 2 (compose my range's affine map) and 4 (replay with the exact incoming
+  // advantage) share one reverse walk; pass 0 composes, pass 1 writes.
+  double P = 0.0, Q = 1.0, a_next = 0.0;
+  GaeSums st{0.0, 0.0, 0.0, 0.0};
+  for (int pass = 0; pass < 2; ++pass) {
+    bool nx_has = nx_has0;
+    int32_t nx_uid = nx_uid0;
+    double nx_v = nx_v0;
+    for (int i = hi - 1; i >= lo; --i) {
+      const Unit u = acc.load(i);
+      if (!u.is_unit) {
+        if (pass) acc.store_empty(i);
+        continue;
+      }
+      const bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
+      const double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
+      const double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
+      if (pass == 0) {
+        const double c = seg_end ? 0.0 : gl;
+        P = __dadd_rn(delta, __dmul_rn(c, P));
+        Q = __dmul_rn(c, Q);
+      } else {
+        const double a = __dadd_rn(delta, __dmul_rn(gl, seg_end ? 0.0 : a_next));
+        acc.store(i, u, a, __dadd_rn(a, u.v));
+        st.n += 1.0;
+        st.s1 += a;
+        st.s2 += a * a;
+        st.counted_slots += u.counted_slots;
+        a_next = a;
+      }
+      nx_has = true;
+      nx_uid = u.uid;
+      nx_v = u.v;
+    }
+    if (pass == 0) {
+      // Phase 3: inclusive suffix scan of the lanes' maps, G_l = F_l o G_{l+1}.
+      for (int off = 1; off < 32; off <<= 1) {
+        const double oP = __shfl_down_sync(0xffffffffu, P, off);
+        const double oQ = __shfl_down_sync(0xffffffffu, Q, off);
+        if (lane + off < 32) {
+          P = __dadd_rn(P, __dmul_rn(Q, oP));
+          Q = __dmul_rn(Q, oQ);
+        }
+      }
+      a_next = __shfl_down_sync(0xffffffffu, P, 1);
+      if (lane == 31) a_next = 0.0;
+    }
+  }
+  // fixed-shape tree over lanes (deterministic)
+  for (int off = 16; off > 0; off >>= 1) {
+    st.n += __shfl_down_sync(0xffffffffu, st.n, off);
+    st.s1 += __shfl_down_sync(0xffffffffu, st.s1, off);
+    st.s2 += __shfl_down_sync(0xffffffffu, st.s2, off);
+    st.counted_slots += __shfl_down_sync(0xffffffffu, st.counted_slots, off);
+  }
+  return st;  // valid in lane 0
+}
+
+// ---- accessors ------------------------------------------------------------------
+struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
+  const ckrl_rollout ro;
+  int e;
+  uint8_t* counted;
+  float* adv;
+  float* ret;
+  __device__ Unit load(int t) const {
+    // All C slots' fields are fetched with independent loads first (no data-dependent
+    // load chain), then the unit is formed in registers.
+    const int C = ro.chunk_len;
+    const int64_t rec = (int64_t)e * ro.num_chunks + t;
+    const int64_t s0 = rec * C;
+    Unit u;
+    u.is_unit = false;
+    u.term = u.trunc = false;
+    u.r = 0.0;
+    u.counted_slots = 0;
+    u.uid = -1;
+    u.v = (double)ro.value_scalar[rec];
+    u.boot = 0.0;
+    constexpr int kC = 8;
+    if (C <= kC) {
+      uint8_t f[kC];
+      int32_t id[kC];
+      float rw[kC], bt[kC];
+#pragma unroll
+      for (int j = 0; j < kC; ++j)
+        if (j < C) {
+          f[j] = ro.flags[s0 + j];
+          id[j] = ro.episode_id[s0 + j];
+          rw[j] = ro.reward[s0 + j];
+          bt[j] = ro.bootstrap[s0 + j];
+        }
+      int first = -1;
+#pragma unroll
+      for (int j = kC - 1; j >= 0; --j)
+        if (j < C && (f[j] & CKRL_FLAG_VALID)) first = j;
+      if (first < 0) return u;  // fully frozen chunk
+      u.is_unit = true;
+#pragma unroll
+      for (int j = 0; j < kC; ++j)
+        if (j == first) u.uid = id[j];
+      bool open = true;
+#pragma unroll
+      for (int j = 0; j < kC; ++j) {
+        if (j < first || j >= C) continue;
+        open = open && (f[j] & CKRL_FLAG_VALID) && id[j] == u.uid;  // tail dropped
+        if (open) {
+          u.r = __dadd_rn(u.r, (double)rw[j]);
+          u.term = u.term || (f[j] & CKRL_FLAG_TERMINATED);
+          u.trunc = u.trunc || (f[j] & CKRL_FLAG_TRUNCATED);
+          u.boot = (double)bt[j];
+          ++u.counted_slots;
+        }
+      }
+      return u;
+    }
+    int first = -1;
+    for (int j = 0; j < C; ++j)
+      if (ro.flags[s0 + j] & CKRL_FLAG_VALID) {
+        first = j;
+        break;
+      }
+    if (first < 0) return u;
+    u.is_unit = true;
+    u.uid = ro.episode_id[s0 + first];
+    int last = first;
+    for (int j = first; j < C; ++j) {
+      uint8_t fl = ro.flags[s0 + j];
+      if (!(fl & CKRL_FLAG_VALID) || ro.episode_id[s0 + j] != u.uid) break;
+      u.r = __dadd_rn(u.r, (double)ro.reward[s0 + j]);
+      u.term = u.term || (fl & CKRL_FLAG_TERMINATED);
+      u.trunc = u.trunc || (fl & CKRL_FLAG_TRUNCATED);
+      last = j;
+      ++u.counted_slots;
+    }
+    u.boot = (double)ro.bootstrap[s0 + last];
+    return u;
+  }
+  __device__ void store(int t, const Unit& u, double a, double R) const {
+    const int C = ro.chunk_len;
+    const int64_t rec = (int64_t)e * ro.num_chunks + t;
+    adv[rec] = (float)a;
+    ret[rec] = (float)R;
+    // counted = the leading episode's contiguous valid prefix from the first valid slot
+    int first = -1;
+    for (int j = 0; j < C; ++j) {
+      bool v = ro.flags[rec * C + j] & CKRL_FLAG_VALID;
+      if (first < 0 && v) first = j;
+      counted[rec * C + j] = (first >= 0 && j < first + u.counted_slots) ? 1 : 0;
+    }
+  }
+  __device__ void store_empty(int t) const {
+    const int C = ro.chunk_len;
+    const int64_t rec = (int64_t)e * ro.num_chunks + t;
+    adv[rec] = 0.0f;
+    ret[rec] = 0.0f;
+    for (int j = 0; j < C; ++j) counted[rec * C + j] = 0;
+  }
+};
+
+struct ActionAcc {  // action-level units: one per valid slot (assembler.cpp:112-146)
+  const ckrl_rollout ro;
+  int e;
+  uint8_t* counted;
+  float* adv;
+  float* ret;
+  __device__ Unit load(int i) const {
+    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
+    uint8_t f = ro.flags[s];
+    Unit u;
+    u.is_unit = (f & CKRL_FLAG_VALID) != 0;
+    u.term = f & CKRL_FLAG_TERMINATED;
+    u.trunc = f & CKRL_FLAG_TRUNCATED;
+    u.uid = ro.episode_id[s];
+    u.r = (double)ro.reward[s];
+    u.v = (double)ro.value_vector[s];
+    u.boot = (double)ro.bootstrap[s];
+    u.counted_slots = 1;
+    return u;
+  }
+  __device__ void store(int i, const Unit&, double a, double R) const {
+    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
+    adv[s] = (float)a;
+    ret[s] = (float)R;
+    counted[s] = 1;
+  }
+  __device__ void store_empty(int i) const {
+    const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
+    adv[s] = 0.0f;
+    ret[s] = 0.0f;
+    counted[s] = 0;
+  }
+};
+
+struct FlatAcc {  // compute_gae over one flat sequence (gae.cpp:7-37)
+  const double *r, *v, *b;
+  const uint8_t* f;
+  double *adv, *ret;
+  int base;
+  __device__ Unit load(int i) const {
+    Unit u;
+    u.is_unit = true;
+    uint8_t fl = f[base + i];
+    u.term = fl & CKRL_FLAG_TERMINATED;
+    u.trunc = fl & CKRL_FLAG_TRUNCATED;
+    u.uid = 0;
+    u.r = r[base + i];
+    u.v = v[base + i];
+    u.boot = b[base + i];
+    u.counted_slots = 0;
+    return u;
+  }
+  __device__ void store(int i, const Unit&, double a, double R) const {
+    adv[base + i] = a;
+    ret[base + i] = R;
+  }
+  __device__ void store_empty(int) const {}
+};
+
+}  // namespace ckrl

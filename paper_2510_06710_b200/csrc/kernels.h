@@ -47,6 +47,9 @@ struct LossArgs {
   WsLayout L;
   double* diag;      // finalised diagnostics (world == 1); raw sums go to ws.loss_raw
   int finalize;      // 1: last CTA finalises into diag; 0: leave raw sums for an allreduce
+  // fused PPO step (assembly inside the loss launch)
+  ckrl_rollout ro;
+  double gamma, lambda;
 };
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
@@ -62,5 +65,7 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
+cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t read_timeline(uint64_t* out, int n);
 
 }  // namespace ckrl

@@ -13,11 +13,18 @@
 // 3 xor-shuffles. exp is ex2.approx on a log2-scaled argument whose shift c is carried
 // into the log-prob exactly (lp = x_tok - c*ln2 - log s, s = sum 2^(x*log2e - c)).
 #include "common.cuh"
+#include "gae.cuh"
 #include "kernels.h"
 
 #include <cstdlib>
 
 namespace ckrl {
+
+// Optional on-device timeline of CTA 0 (SM cycles), read with ckrl_debug_timeline().
+__device__ uint64_t g_timeline[32];
+__device__ __forceinline__ void tl_mark(int slot) {
+  if (blockIdx.x == 0) g_timeline[slot] = clock64();
+}
 
 constexpr float kL2E = 1.4426950408889634f;
 constexpr double kLN2 = 0.6931471805599453;
@@ -185,37 +192,59 @@ struct Acc {
 
 // Merge the per-rank stats records (fixed rank order) into the loss constants.
 struct LossConsts {
-  double inv_adv, inv_val, inv_pos, mean, denom, inv_groups;
+  double inv_adv, inv_val, inv_pos, mean, denom, inv_denom, inv_groups;
   int do_norm;
   int64_t n_adv, groups;
   int status;
 };
 
-__device__ LossConsts merge_consts(const LossArgs& a) {
+__device__ __forceinline__ double drecip(double x) { return __drcp_rn(x); }  // == 1.0 / x (IEEE rn)
+
+// Merge the per-rank stats records (fixed rank order) into the loss constants.
+__device__ LossConsts consts_from(double n, double s1, double s2, int64_t n_adv, int64_t n_val,
+                                  int64_t n_pos, int64_t groups, int status, int normalize) {
   LossConsts k;
-  Moments m{0.0, 0.0, 0.0};
+  k.n_adv = n_adv;
+  k.groups = groups;
+  k.inv_adv = n_adv > 0 ? drecip((double)n_adv) : 0.0;
+  k.inv_val = n_val > 0 ? drecip((double)n_val) : 0.0;
+  k.inv_pos = n_pos > 0 ? drecip((double)n_pos) : 0.0;
+  k.do_norm = normalize && n >= 2.0;
+  whitening(n, s1, s2, &k.mean, &k.denom);
+  k.inv_denom = drecip(k.denom);
+  k.inv_groups = groups > 0 ? drecip((double)groups) : 0.0;
+  k.status = status;
+  return k;
+}
+
+__device__ LossConsts merge_consts(const LossArgs& a) {
+  double n = 0.0, s1 = 0.0, s2 = 0.0;
   int64_t n_adv = 0, n_val = 0, n_pos = 0, groups = 0;
   int status = 0;
   for (int r = 0; r < a.world; ++r) {
     const StatsRecord& s = a.recs[r];
-    m = merge_moments(m, Moments{(double)s.n_units, s.mean, s.m2});
+    n += (double)s.n_units;
+    s1 += s.sum;
+    s2 += s.sumsq;
     n_adv += s.n_adv;
     n_val += s.n_val;
     n_pos += s.n_pos;
     groups += s.groups_retained;
     if (s.status && !status) status = (int)s.status;
   }
-  k.n_adv = n_adv;
-  k.groups = groups;
-  k.inv_adv = n_adv > 0 ? 1.0 / (double)n_adv : 0.0;
-  k.inv_val = n_val > 0 ? 1.0 / (double)n_val : 0.0;
-  k.inv_pos = n_pos > 0 ? 1.0 / (double)n_pos : 0.0;
-  k.do_norm = a.normalize && m.n >= 2.0;
-  k.mean = m.mean;
-  k.denom = m.n > 0 ? sqrt(m.m2 / m.n) + 1e-8 : 1.0;
-  k.inv_groups = groups > 0 ? 1.0 / (double)groups : 0.0;
-  k.status = status;
-  return k;
+  return consts_from(n, s1, s2, n_adv, n_val, n_pos, groups, status, a.normalize);
+}
+
+// One advantage unit: ratio, clipped surrogate (losses.cpp:32-46) and the approx-kl term
+// (losses.cpp:130).
+struct UnitOut {
+  double value, dlogprob, kl;
+  int clipped;
+};
+__device__ __forceinline__ UnitOut surrogate_unit(double d, double adv, double eps) {
+  const double rho = exp(d);
+  const Surrogate s = clipped_surrogate(rho, adv, eps);
+  return UnitOut{s.value, s.dlogprob, (rho - 1.0) - d, s.clipped ? 1 : 0};
 }
 
 __device__ void finalize_diag(const LossArgs& a, const LossConsts& k, const double* raw,
@@ -284,14 +313,13 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
         float coeff = 0.0f;
         if (cnt) {
           double adv = chunk_adv ? (double)a.adv[rec] : (double)a.adv[slot];
-          if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
           const double d = lp - (double)old;
-          const double rho = exp(d);
-          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          const UnitOut su = surrogate_unit(d, adv, a.clip);
           acc.surr += su.value;
           acc.units += 1.0;
           acc.clipped += su.clipped;
-          acc.kl += (rho - 1.0) - d;
+          acc.kl += su.kl;
           coeff = (float)(-k.inv_adv * su.dlogprob);
         }
         if (a.coeff_lp) a.coeff_lp[kk] = coeff;
@@ -301,14 +329,13 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
       const float w = a.slot_weight[slot];
       float coeff = 0.0f;
       if (a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f) {
-        const double inv_g = 1.0 / (double)a.env_group_size[e];
+        const double inv_g = drecip((double)a.env_group_size[e]);
         const double d = lp - (double)old;
-        const double rho = exp(d);
-        Surrogate su = clipped_surrogate(rho, a.env_adv[e], a.clip);
+        const UnitOut su = surrogate_unit(d, a.env_adv[e], a.clip);
         acc.surr += k.inv_groups * inv_g * (double)w * su.value;
         acc.units += 1.0;
         acc.clipped += su.clipped;
-        acc.kl += (rho - 1.0) - d;
+        acc.kl += su.kl;
         coeff = (float)(-k.inv_groups * inv_g * (double)w * su.dlogprob);
       }
       if (a.coeff_lp) a.coeff_lp[kk] = coeff;
@@ -343,13 +370,13 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
           if (MODE == MODE_PPO) {
             on = a.counted[slot] != 0;
             adv = chunk_adv ? (double)a.adv[rec] : (double)a.adv[slot];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
           } else {
             e = (int)(rec / a.Tc);
             const float w = a.slot_weight[slot];
             on = a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f;
             adv = on ? a.env_adv[e] : 0.0;
-            scale = on ? k.inv_groups * (1.0 / (double)a.env_group_size[e]) * (double)w : 0.0;
+            scale = on ? k.inv_groups * (drecip((double)a.env_group_size[e])) * (double)w : 0.0;
           }
           float coeff = 0.0f;
           if (on) {
@@ -358,11 +385,10 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
               an += sm.lp[sl * M + j];
               ao += (double)sm.old[sl * M + j];
             }
-            const double rho = exp(an - ao);
-            Surrogate su = clipped_surrogate(rho, adv, a.clip);
+            const UnitOut su = surrogate_unit(an - ao, adv, a.clip);
             acc.units += 1.0;
             acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (an - ao);
+            acc.kl += su.kl;
             if (MODE == MODE_PPO) {
               acc.surr += su.value;
               coeff = (float)(-k.inv_adv * su.dlogprob);
@@ -427,20 +453,19 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
       if (chunk_lp) {
         float coeff = 0.0f;
         if (any) {
-          const double rho = exp(lpn - lpo);
           double adv, scale = 1.0;
           if (MODE == MODE_PPO) {
             adv = (double)a.adv[rec];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
           } else {
             adv = a.env_adv[e];
-            scale = k.inv_groups * (1.0 / (double)a.env_group_size[e]) * wsum;
+            scale = k.inv_groups * (drecip((double)a.env_group_size[e])) * wsum;
           }
-          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          const UnitOut su = surrogate_unit(lpn - lpo, adv, a.clip);
           if (lane == 0) {
             acc.units += 1.0;
             acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (lpn - lpo);
+            acc.kl += su.kl;
             acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
           }
           coeff = (float)(MODE == MODE_PPO ? -k.inv_adv * su.dlogprob : -scale * su.dlogprob);
@@ -485,17 +510,20 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
     if (lane == 0) s_red[warp][i] = x;
   }
   __syncthreads();
+  if (tid == 0) tl_mark(25);
   double* parts = reinterpret_cast<double*>(a.ws + a.L.loss_partials);
   uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
   if (tid < RAW_COUNT) {
     double x = 0.0;
     for (int w = 0; w < nwarps; ++w) x += s_red[w][tid];
     parts[blockIdx.x * RAW_COUNT + tid] = x;
+    __threadfence();
   }
-  __threadfence();
   __syncthreads();
+  if (tid == 0) tl_mark(26);
   if (tid == 0) *s_last = atomicAdd(&tickets[TICKET_LOSS], 1u) == gridDim.x - 1;
   __syncthreads();
+  if (tid == 0) tl_mark(27);
   if (!*s_last) return;
   __threadfence();
   // Last CTA: every thread sums a fixed strided subset of the partials (loads in
@@ -804,8 +832,7 @@ __device__ __forceinline__ double log_f32_exact_exp(float s) {
 }
 
 constexpr int kRowBufs = 4;     // row-partial + metadata buffers (row warps <-> unit warps)
-constexpr int kMaxPasses = 4;   // row-group passes per warp per tile
-constexpr int kTileRowsMax = kMaxPasses * (kTmaConsumers / 32) * 4;  // 128 rows per tile
+constexpr int kTileRowsMax = 128;  // rows (tokens) per tile
 
 // Per-tile small inputs staged in shared memory by the metadata warp, so consumer warps
 // never wait on global memory: token ids, old log-probs, per-slot activity (counted, or
@@ -820,10 +847,11 @@ struct MetaSmem {
   float* nv;
   int32_t* esz;
   double* eadv;
-  uint8_t* act;
+  uint8_t* act;   // per slot: bit1 unit active (counted / trajectory slot with weight)
+  uint8_t* need;  // per slot: the row phase evaluates this slot's rows
 };
 __host__ __device__ constexpr size_t meta_bytes() {
-  return (size_t)kTileRowsMax * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1);
+  return (size_t)kTileRowsMax * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1 + 1);
 }
 __device__ __forceinline__ MetaSmem carve_meta(unsigned char* p) {
   MetaSmem m;
@@ -836,59 +864,101 @@ __device__ __forceinline__ MetaSmem carve_meta(unsigned char* p) {
   m.nv = m.ret + kTileRowsMax;
   m.esz = reinterpret_cast<int32_t*>(m.nv + kTileRowsMax);
   m.act = reinterpret_cast<uint8_t*>(m.esz + kTileRowsMax);
+  m.need = m.act + kTileRowsMax;
   return m;
 }
 __host__ __device__ constexpr size_t rowbuf_bytes() {
   return rowsmem_bytes(kTileRowsMax) + meta_bytes();
 }
 
-// Register image of one tile's metadata for one lane (<= 4 items of each kind).
-struct MetaRegs {
+// Row metadata (what the row warps read): token ids and per-slot "evaluate" flags. In the
+// fused step the assembly outputs do not exist yet, so every valid slot is evaluated
+// (counted slots are a subset); otherwise the assembled activity decides.
+template <int MODE, bool FUSED>
+__device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                         const MetaSmem& m) {
+  const int C = a.C, P = C * a.M;
+  const int rows = nrec * P, slots = nrec * C;
+  const int64_t k0 = r0 * P, s0 = r0 * C;
   int32_t tok[4];
+  uint8_t nd[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < rows) tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
+    if (i < slots) {
+      bool n = true;
+      if (!a.all_rows && MODE != MODE_STATS) {
+        if (FUSED) {
+          n = (a.ro.flags[s0 + i] & CKRL_FLAG_VALID) != 0;
+        } else if (MODE == MODE_PPO) {
+          n = a.counted[s0 + i] != 0;
+        } else {
+          const int e = (int)((s0 + i) / C / a.Tc);
+          const int32_t g = a.env_group[e];
+          const uint8_t mem = a.slot_member[s0 + i];
+          const float w = a.slot_weight[s0 + i];
+          n = (g >= 0) & (mem != 0) & (w != 0.0f);
+        }
+      }
+      nd[q] = n ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < rows) m.tok[i] = tok[q];
+    if (i < slots) m.need[i] = nd[q];
+  }
+}
+
+// Unit metadata (read only by the buffer warp that owns the tile), register image.
+struct UnitRegs {
   float old[4], w[4], adv[4], ret[4], nv[4];
   int32_t esz[4];
   double eadv[4];
   uint8_t act[4];
 };
 
-template <int MODE>
-__device__ __forceinline__ void meta_load(const LossArgs& a, int64_t r0, int nrec, int lane, MetaRegs& R) {
+// Loads that may read what other CTAs wrote earlier in the same (fused) launch go
+// through L2 (ld.global.cg): the non-coherent L1 must not serve them.
+template <int MODE, bool FUSED>
+__device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                               UnitRegs& R) {
   const int C = a.C, M = a.M, P = C * M;
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P, s0 = r0 * C;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
-    if (i < rows) {
-      R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
-      R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
-    }
+    if (i < rows) R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
     if (i < slots) {
       if (MODE == MODE_PPO) {
-        R.act[q] = a.all_rows ? 1 : 0;
-        R.act[q] |= (a.counted[s0 + i] != 0) ? 2 : 0;  // bit1: counted
+        R.act[q] = (FUSED ? __ldcg(a.counted + s0 + i) : a.counted[s0 + i]) != 0 ? 2 : 0;
         R.w[q] = 0.0f;
       } else if (MODE == MODE_GRPO) {
-        // independent loads (no short-circuit chain), combined afterwards
         const int e = (int)((s0 + i) / C / a.Tc);
         const int32_t g = a.env_group[e];
         const uint8_t mem = a.slot_member[s0 + i];
         const float w = a.slot_weight[s0 + i];
         const bool on = (g >= 0) & (mem != 0) & (w != 0.0f);
-        R.act[q] = (a.all_rows ? 1 : 0) | (on ? 2 : 0) | (mem ? 4 : 0);
+        R.act[q] = on ? 2 : 0;
         R.w[q] = w;
       } else {
-        R.act[q] = 1;
+        R.act[q] = 0;
       }
     }
     if (MODE == MODE_PPO) {
       const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
       const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
-      if (i < adv_units) R.adv[q] = a.adv[(a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i];
+      if (i < adv_units) {
+        const float* p = a.adv + (a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i;
+        R.adv[q] = FUSED ? __ldcg(p) : *p;
+      }
       if (i < val_units) {
         const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
-        R.ret[q] = a.ret[vb + i];
-        R.nv[q] = a.new_values ? a.new_values[vb + i] : 0.0f;
+        R.ret[q] = FUSED ? __ldcg(a.ret + vb + i) : a.ret[vb + i];
+        R.nv[q] = a.new_values ? __ldg(a.new_values + vb + i) : 0.0f;
       }
     }
     if (MODE == MODE_GRPO && i < nrec) {
@@ -900,17 +970,14 @@ __device__ __forceinline__ void meta_load(const LossArgs& a, int64_t r0, int nre
 }
 
 template <int MODE>
-__device__ __forceinline__ void meta_store(const LossArgs& a, int nrec, int lane, const MetaRegs& R,
-                                           const MetaSmem& m) {
+__device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int lane, const UnitRegs& R,
+                                                const MetaSmem& m) {
   const int C = a.C, P = C * a.M;
   const int rows = nrec * P, slots = nrec * C;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
-    if (i < rows) {
-      m.tok[i] = R.tok[q];
-      m.old[i] = R.old[q];
-    }
+    if (i < rows) m.old[i] = R.old[q];
     if (i < slots) {
       m.act[i] = R.act[q];
       m.w[i] = R.w[q];
@@ -959,19 +1026,18 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         double adv, scale;
         if (MODE == MODE_PPO) {
           adv = (double)m.adv[chunk_adv ? r : sl];
-          if (k.do_norm) adv = (adv - k.mean) / k.denom;
+          if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
           scale = k.inv_adv;
         } else {
           adv = m.eadv[r];
-          scale = k.inv_groups * (1.0 / (double)m.esz[r]) * (double)m.w[sl];
+          scale = k.inv_groups * drecip((double)m.esz[r]) * (double)m.w[sl];
         }
         const double d = lp - (double)m.old[row];
-        const double rho = exp(d);
-        Surrogate su = clipped_surrogate(rho, adv, a.clip);
+        const UnitOut su = surrogate_unit(d, adv, a.clip);
         acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
         acc.units += 1.0;
         acc.clipped += su.clipped;
-        acc.kl += (rho - 1.0) - d;
+        acc.kl += su.kl;
         coeff = (float)(-scale * su.dlogprob);
       }
       if (a.coeff_lp) a.coeff_lp[kk] = coeff;
@@ -1008,23 +1074,22 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
           double adv, scale;
           if (MODE == MODE_PPO) {
             adv = (double)m.adv[chunk_adv ? r : sl];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
             scale = k.inv_adv;
           } else {
             adv = m.eadv[r];
-            scale = k.inv_groups * (1.0 / (double)m.esz[r]) * (double)m.w[sl];
+            scale = k.inv_groups * drecip((double)m.esz[r]) * (double)m.w[sl];
           }
           double an = 0.0, ao = 0.0;
           for (int j = 0; j < M; ++j) {
             an += sm.lp[sl * M + j];
             ao += (double)m.old[sl * M + j];
           }
-          const double rho = exp(an - ao);
-          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          const UnitOut su = surrogate_unit(an - ao, adv, a.clip);
           acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
           acc.units += 1.0;
           acc.clipped += su.clipped;
-          acc.kl += (rho - 1.0) - (an - ao);
+          acc.kl += su.kl;
           coeff = (float)(-scale * su.dlogprob);
         }
         if (a.coeff_lp)
@@ -1064,21 +1129,20 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         if (MODE == MODE_GRPO) wsum = warp_sum(wsum);
         float coeff = 0.0f;
         if (any) {
-          const double rho = exp(lpn - lpo);
           double adv, scale;
           if (MODE == MODE_PPO) {
             adv = (double)m.adv[r];
-            if (k.do_norm) adv = (adv - k.mean) / k.denom;
+            if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
             scale = k.inv_adv;
           } else {
             adv = m.eadv[r];
-            scale = k.inv_groups * (1.0 / (double)m.esz[r]) * wsum;
+            scale = k.inv_groups * drecip((double)m.esz[r]) * wsum;
           }
-          Surrogate su = clipped_surrogate(rho, adv, a.clip);
+          const UnitOut su = surrogate_unit(lpn - lpo, adv, a.clip);
           if (lane == 0) {
             acc.units += 1.0;
             acc.clipped += su.clipped;
-            acc.kl += (rho - 1.0) - (lpn - lpo);
+            acc.kl += su.kl;
             acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
           }
           coeff = (float)(-scale * su.dlogprob);
@@ -1099,40 +1163,130 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
     }
 }
 
+
 constexpr int kBufWarps = kRowBufs;  // buffer warp m owns row buffer m (tiles i = m mod 4)
-constexpr int kTmaThreadsFull = 32 + kTmaConsumers + 32 * kBufWarps;  // producer, 8 row warps,
-                                                                        // 4 buffer warps
+template <int ROWW>
+constexpr int tma_threads() { return 32 * (1 + ROWW + kBufWarps); }  // producer, row, buffer warps
+
+__device__ __forceinline__ void bufwarps_sync() {  // named barrier over the 4 buffer warps
+  asm volatile("bar.sync 2, %0;" ::"n"(32 * kBufWarps) : "memory");
+}
+
+// Fused PPO step, phase A (buffer warps only): GAE + counted masks for this CTA's envs,
+// CTA partial of the whitening sums, grid-wide barrier, then every CTA sums all
+// partials in the same fixed order (identical, deterministic constants everywhere).
+__device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, LossConsts* s_kf) {
+  __shared__ AsmPartial bpart[kBufWarps];
+  const ckrl_rollout& ro = a.ro;
+  const bool action = a.adv_level == CKRL_LEVEL_ACTION;
+  AsmPartial acc{0.0, 0.0, 0.0, 0.0};
+  for (int e = blockIdx.x + b * gridDim.x; e < ro.num_envs; e += kBufWarps * gridDim.x) {
+    uint8_t* cnt = const_cast<uint8_t*>(a.counted);
+    float* adv = const_cast<float*>(a.adv);
+    float* ret = const_cast<float*>(a.ret);
+    const GaeSums g = action ? warp_gae(ActionAcc{ro, e, cnt, adv, ret}, ro.num_chunks * ro.chunk_len,
+                                       a.gamma, a.lambda)
+                             : warp_gae(ChunkAcc{ro, e, cnt, adv, ret}, ro.num_chunks, a.gamma, a.lambda);
+    acc.n += g.n;
+    acc.s1 += g.s1;
+    acc.s2 += g.s2;
+    acc.n_pos += g.counted_slots;
+  }
+  if (lane == 0) bpart[b] = acc;
+  if (b == 0 && lane == 0) tl_mark(1);
+  __threadfence();  // this warp's counted / adv / ret stores before the grid arrival
+  bufwarps_sync();
+  AsmPartial* parts = reinterpret_cast<AsmPartial*>(a.ws + a.L.asm_partials);
+  uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
+  if (b == 0 && lane == 0) {
+    AsmPartial p{0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < kBufWarps; ++w) {
+      p.n += bpart[w].n;
+      p.s1 += bpart[w].s1;
+      p.s2 += bpart[w].s2;
+      p.n_pos += bpart[w].n_pos;
+    }
+    parts[blockIdx.x] = p;
+    volatile uint32_t* gen = tickets + TICKET_GEN;
+    const uint32_t g = *gen;
+    __threadfence();
+    if (atomicAdd(&tickets[TICKET_GRID], 1u) == gridDim.x - 1) {
+      tickets[TICKET_GRID] = 0;
+      __threadfence();
+      atomicAdd(&tickets[TICKET_GEN], 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+    tl_mark(2);
+  }
+  bufwarps_sync();
+  if (b == 0) {  // one warp: fixed-order sum of the grid's partials
+    AsmPartial q{0.0, 0.0, 0.0, 0.0};
+    for (unsigned g = lane; g < gridDim.x; g += 32) {
+      q.n += __ldcg(&parts[g].n);
+      q.s1 += __ldcg(&parts[g].s1);
+      q.s2 += __ldcg(&parts[g].s2);
+      q.n_pos += __ldcg(&parts[g].n_pos);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      q.n += __shfl_down_sync(0xffffffffu, q.n, off);
+      q.s1 += __shfl_down_sync(0xffffffffu, q.s1, off);
+      q.s2 += __shfl_down_sync(0xffffffffu, q.s2, off);
+      q.n_pos += __shfl_down_sync(0xffffffffu, q.n_pos, off);
+    }
+    if (lane == 0) {
+      const int64_t n = (int64_t)q.n, npos = (int64_t)q.n_pos * a.M;
+      // value level == advantage level (assembler.cpp:82): n_val == n_adv
+      *s_kf = consts_from(q.n, q.s1, q.s2, n, n, npos, 0, 0, a.normalize);
+      tl_mark(3);
+      if (blockIdx.x == 0) {  // the rank's stats record, as ckrl_assemble_ppo_batch leaves it
+        StatsRecord* st = reinterpret_cast<StatsRecord*>(a.ws + a.L.stats_local);
+        st->sum = q.s1;
+        st->sumsq = q.s2;
+        st->n_units = st->n_adv = st->n_val = n;
+        st->n_pos = npos;
+        st->groups_retained = 0;
+        st->status = 0;
+      }
+    }
+  }
+  bufwarps_sync();
+}
 
 // Roles (one CTA per SM, persistent over tiles of whole records):
 //   warp 0 lane 0   TMA producer: streams the tile's logits into a ring of `nstage` stages
 //                   with cp.async.bulk, completion by mbarrier tx-count (full[s]).
-//   warps 1..8      row warps: V-bin log-softmax / gather / entropy per row from shared
-//                   memory (LDS.128); results -> row buffer (it mod 4).
-//   warps 9..12     buffer warps: warp m owns row buffer m. It stages tile i's metadata
-//                   (token ids, old log-probs, slot activity / weights, unit advantages,
-//                   returns, values, group data) into the buffer, waits for the row
-//                   results, runs the unit phase, and meanwhile already has tile i+4's
-//                   metadata loads in flight.
+//   ROWW row warps  V-bin log-softmax / gather / entropy per row from shared memory
+//                   (LDS.128); raw row partials -> row buffer (it mod 4).
+//   4 buffer warps  warp m owns row buffer m: stages tile i's row metadata (token ids,
+//                   evaluate flags), loads its unit metadata while the rows are computed,
+//                   runs the unit phase, then stages tile i+4. In the fused PPO step they
+//                   first run the GAE scan for the CTA's envs (phase A) and a grid-wide
+//                   barrier, while the producer and row warps already stream logits.
 // Synchronisation is mbarrier-only: full[s]/empty[s] (producer <-> row warps),
 // metafull[b] (buffer warp -> row warps), rowfull[b] (row warps -> buffer warp).
-template <int MODE, typename LT>
-__global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a, int nstage,
-                                                                      uint32_t tile_bytes) {
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED>
+__global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossArgs a, int nstage,
+                                                                          uint32_t tile_bytes) {
+  constexpr int kThreads = tma_threads<ROWW>();
+  constexpr int kPasses = (kTileRowsMax + ROWW * 4 - 1) / (ROWW * 4);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ LossConsts s_k;
-  __shared__ double s_red[kTmaThreadsFull / 32][RAW_COUNT];
+  __shared__ LossConsts s_k, s_kf;
+  __shared__ double s_red[kThreads / 32][RAW_COUNT];
   __shared__ bool s_last;
   __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4], metafull_bar[kRowBufs],
       rowfull_bar[kRowBufs];
 
   constexpr int V = 256;
-  constexpr int kCW = kTmaConsumers / 32;  // row warps
+  constexpr int kCW = ROWW;  // row warps
   const int M = a.M, P = a.C * M;
   unsigned char* stage_base = smem_raw;
   unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
+    tl_mark(0);
     for (int s = 0; s < nstage; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kCW);
@@ -1142,10 +1296,8 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
       mbar_init(&rowfull_bar[b], kCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_k = merge_consts(a);
   }
   __syncthreads();
-  const LossConsts k = s_k;
   Acc acc{0, 0, 0, 0, 0, 0};
   auto tile_recs = [&](int64_t tile, int64_t& r0) {
     r0 = tile * a.rec_per_tile;
@@ -1188,27 +1340,36 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
-      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // buffer b holds tile it's metadata
+      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // buffer b holds tile it's row metadata
+      if (cwarp == 0 && lane == 0 && it < 3) tl_mark(11 + 3 * it);
       mbar_wait(&full_bar[s], (it / nstage) & 1);
+      if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
 #pragma unroll
-      for (int p = 0; p < kMaxPasses; p += 2) {
-        const int rg0 = (p * kCW + cwarp) * 4, rg1 = ((p + 1) * kCW + cwarp) * 4;
+      for (int p = 0; p < kPasses; p += RIF) {
+        const int rg0 = (p * kCW + cwarp) * 4;
         if (rg0 >= rows) break;  // warp-uniform
-        const int row0 = rg0 + sub, row1 = rg1 + sub;
-        const LT* rp[2] = {stage + (size_t)(row0 < rows ? row0 : rg0) * V,
-                           stage + (size_t)(row1 < rows ? row1 : rg0) * V};
-        float s_[2], t_[2], c_[2];
-        if (rg1 < rows)
-          rows_fast_smem<LT, 2>(rp, l8, s_, t_, c_);
+        const LT* rp[RIF];
+        int rowq[RIF];
+        bool live[RIF];
+#pragma unroll
+        for (int q = 0; q < RIF; ++q) {
+          const int rg = ((p + q) * kCW + cwarp) * 4;
+          rowq[q] = rg + sub;
+          live[q] = (p + q) < kPasses && rg < rows;
+          rp[q] = stage + (size_t)(live[q] && rowq[q] < rows ? rowq[q] : rg0) * V;
+        }
+        float s_[RIF], t_[RIF], c_[RIF];
+        if (RIF == 1 || live[RIF - 1])
+          rows_fast_smem<LT, RIF>(rp, l8, s_, t_, c_);
         else
           rows_fast_smem<LT, 1>(rp, l8, s_, t_, c_);
         if (l8 == 0) {
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int row = q ? row1 : row0;
-            if (row >= rows || (q && rg1 >= rows)) continue;
-            const bool need = (mt.act[row / M] & 3) != 0;
+          for (int q = 0; q < RIF; ++q) {
+            const int row = rowq[q];
+            if (!live[q] || row >= rows) continue;
+            const bool need = mt.need[row / M] != 0;
             float xt = 0.0f;
             if (need) {
               const int tok = mt.tok[row];
@@ -1226,10 +1387,11 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
       if (lane == 0) {
         mbar_arrive(&empty_bar[s]);    // stage s fully read by this warp
         mbar_arrive(&rowfull_bar[b]);  // my rows' results are in buffer b
+        if (cwarp == 0 && it < 3) tl_mark(13 + 3 * it);
       }
     }
   } else {
-    // ---------------- buffer warps: metadata in, unit phase out ----------------
+    // ---------------- buffer warps ----------------
     const int b = warp - 1 - kCW;
     unsigned char* bb = buf_base + b * rowbuf_bytes();
     const RowSmem sm = carve_rows(bb, kTileRowsMax);
@@ -1237,39 +1399,47 @@ __global__ void __launch_bounds__(kTmaThreadsFull, 1) tma_tile_kernel(LossArgs a
     const int64_t stride = (int64_t)kBufWarps * gridDim.x;
     int64_t tile = blockIdx.x + (int64_t)b * gridDim.x;
     int it = b;
-    MetaRegs regs;
     int64_t r0 = 0;
     int nrec = 0;
-    if (tile < a.n_tiles) {
+    if (tile < a.n_tiles) {  // rows of the first tile can start right away
       nrec = tile_recs(tile, r0);
-      meta_load<MODE>(a, r0, nrec, lane, regs);
-      meta_store<MODE>(a, nrec, lane, regs, mt);
+      row_meta<MODE, FUSED>(a, r0, nrec, lane, mt);
       __syncwarp();
       if (lane == 0) mbar_arrive(&metafull_bar[b]);
+      if (lane == 0 && b == 0) tl_mark(24);
     }
+    if (FUSED) {
+      fused_phase_a(a, b, lane, &s_kf);
+    } else {
+      if (b == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
+      bufwarps_sync();
+    }
+    const LossConsts k = FUSED ? s_kf : s_k;
     for (; tile < a.n_tiles; tile += stride, it += kBufWarps) {
-      const int64_t ntile = tile + stride;
-      int64_t nr0 = 0;
-      int nnrec = 0;
-      if (ntile < a.n_tiles) {  // next tile's metadata loads go out before the unit phase
-        nnrec = tile_recs(ntile, nr0);
-        meta_load<MODE>(a, nr0, nnrec, lane, regs);
-      }
+      UnitRegs ur;
+      unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);  // in flight while rows finish
       mbar_wait(&rowfull_bar[b], (it / kRowBufs) & 1);
+      if (lane == 0 && it == b) tl_mark(20 + b);
+      unit_meta_store<MODE>(a, nrec, lane, ur, mt);
+      __syncwarp();
       unit_phase_smem<MODE>(a, k, acc, sm, mt, r0, nrec, lane);
       __syncwarp();
+      if (lane == 0 && it == b) tl_mark(4 + b);  // first unit phase of each buffer warp
+      const int64_t ntile = tile + stride;
       if (ntile < a.n_tiles) {
-        meta_store<MODE>(a, nnrec, lane, regs, mt);
+        nrec = tile_recs(ntile, r0);
+        row_meta<MODE, FUSED>(a, r0, nrec, lane, mt);
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
-      r0 = nr0;
-      nrec = nnrec;
     }
   }
+  if (warp == 1 && lane == 0) tl_mark(8);  // row warp 0 done with its last tile
   __syncthreads();
+  if (tid == 0) tl_mark(9);
   if (MODE == MODE_STATS) return;
-  reduce_and_finish(a, k, acc, tid, kTmaThreadsFull, s_red, &s_last);
+  reduce_and_finish(a, FUSED ? s_kf : s_k, acc, tid, kThreads, s_red, &s_last);
+  if (tid == 0) tl_mark(10);
 }
 
 __global__ void finalize_kernel(LossArgs a) {
@@ -1329,21 +1499,41 @@ static bool tma_plan(const LossArgs& a, int dbytes, int& rec_per_tile, int& nsta
   return nstage >= 2;
 }
 
-template <int MODE, typename LT>
-static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
-  auto kern = tma_tile_kernel<MODE, LT>;
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED>
+static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
+  auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED>;
   a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
-  const size_t rows = (size_t)a.rec_per_tile * a.C * a.M;
   const size_t smem = (size_t)nstage * tile_bytes + kRowBufs * rowbuf_bytes();
-  (void)rows;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t grid = device_sms();
   if (grid > a.n_tiles) grid = a.n_tiles;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = (int)grid;
-  kern<<<(unsigned)grid, kTmaThreadsFull, smem, s>>>(a, nstage, tile_bytes);
-  return cudaGetLastError();
+  if (!FUSED) {
+    kern<<<(unsigned)grid, tma_threads<ROWW>(), smem, s>>>(a, nstage, tile_bytes);
+    return cudaGetLastError();
+  }
+  // The fused step has a grid-wide barrier: co-residency of every CTA is required, so the
+  // launch is cooperative (one CTA per SM by construction).
+  void* args[] = {&a, &nstage, &tile_bytes};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(tma_threads<ROWW>()),
+                                     args, smem, s);
+}
+
+static int g_tma_variant = -1;
+
+template <int MODE, typename LT, bool FUSED>
+static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
+  if (g_tma_variant < 0) {
+    const char* env = getenv("CKRL_TMA_VARIANT");
+    g_tma_variant = env ? atoi(env) : 0;
+  }
+  switch (g_tma_variant) {
+    // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
+    case 3: return launch_tma_v<MODE, LT, 8, 2, FUSED>(a, s, grid_out, nstage, tile_bytes);
+    default: return launch_tma_v<MODE, LT, 16, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
+  }
 }
 
 static int g_force_direct = -1;
@@ -1361,13 +1551,31 @@ static cudaError_t launch_mode(LossArgs& a, cudaStream_t s, int* g) {
   const uintptr_t align = reinterpret_cast<uintptr_t>(a.logits) & 15;
   if (fast && !g_force_direct && align == 0 && tma_plan(a, dbytes, rpt, nstage, tile_bytes)) {
     a.rec_per_tile = rpt;
-    return a.logits_bf16 ? launch_tma<MODE, __nv_bfloat16>(a, s, g, nstage, tile_bytes)
-                         : launch_tma<MODE, float>(a, s, g, nstage, tile_bytes);
+    return a.logits_bf16 ? launch_tma<MODE, __nv_bfloat16, false>(a, s, g, nstage, tile_bytes)
+                         : launch_tma<MODE, float, false>(a, s, g, nstage, tile_bytes);
   }
   if (a.logits_bf16)
     return fast ? launch_direct<MODE, __nv_bfloat16, true>(a, s, g)
                 : launch_direct<MODE, __nv_bfloat16, false>(a, s, g);
   return fast ? launch_direct<MODE, float, true>(a, s, g) : launch_direct<MODE, float, false>(a, s, g);
+}
+
+// The fused single-GPU PPO step (assembly + loss in one persistent launch). Returns
+// cudaErrorNotSupported when the shape has no TMA plan (caller uses the 2-kernel path).
+cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* g) {
+  if (g_force_direct < 0) {
+    const char* env = getenv("CKRL_LOSS_KERNEL");
+    g_force_direct = (env && env[0] == 'd') ? 1 : 0;
+  }
+  const int dbytes = a.logits_bf16 ? 2 : 4;
+  int rpt, nstage;
+  uint32_t tile_bytes;
+  const uintptr_t align = reinterpret_cast<uintptr_t>(a.logits) & 15;
+  if (a.V != 256 || g_force_direct || align != 0 || !tma_plan(a, dbytes, rpt, nstage, tile_bytes))
+    return cudaErrorNotSupported;
+  a.rec_per_tile = rpt;
+  return a.logits_bf16 ? launch_tma<MODE_PPO, __nv_bfloat16, true>(a, s, g, nstage, tile_bytes)
+                       : launch_tma<MODE_PPO, float, true>(a, s, g, nstage, tile_bytes);
 }
 
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out) {
@@ -1376,6 +1584,10 @@ cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out) {
     case MODE_PPO: return launch_mode<MODE_PPO>(a, s, grid_out);
     default: return launch_mode<MODE_GRPO>(a, s, grid_out);
   }
+}
+
+cudaError_t read_timeline(uint64_t* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_timeline, sizeof(uint64_t) * (n < 32 ? n : 32));
 }
 
 cudaError_t launch_finalize(LossArgs& a, cudaStream_t s) {
