@@ -1,0 +1,65 @@
+"""Live pinning against the unmodified reference (oracle/_ref, built from /root/reference
+where it exists): fresh reference rollouts in every rollout mode, the oracle must reproduce
+assemble/normalize/loss bit-for-bit, and its per-position gradient coefficients replayed
+through the reference's own PolicyNet::accumulate_*_gradient must reproduce ppo_loss /
+grpo_loss's grad_out bit-for-bit."""
+import numpy as np
+import pytest
+
+from oracle.bindings import RefScenario, ref_available
+
+pytestmark = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (no /root/reference)")
+
+MODES = {
+    "partial": dict(auto_reset=1),
+    "deferred": dict(auto_reset=1, deferred_reset=1),
+    "fixedlen": dict(auto_reset=1, ignore_terminations=1),
+    "scripted": dict(env_kind=1, success_step=2, auto_reset=1),
+}
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
+@pytest.mark.parametrize("seed", [1, 2])
+def test_ppo_bitexact_and_gradient_replay(oracle, mode, seed):
+    sc = RefScenario(num_envs=5, num_chunks=5, chunk_length=3, max_episode_steps=6, env_seed=seed,
+                     sample_seed=seed + 100, net_seed=seed + 7, **MODES[mode])
+    d = sc.export()
+    for spec in [(0, 0, 0), (0, 1, 0), (0, 2, 0), (1, 1, 1), (1, 2, 1)]:
+        r = sc.ppo(spec, want_grad=True)
+        st, counted, adv, ret = oracle.assemble_ppo(d, spec, 0.99, 0.95)
+        assert st == 0
+        np.testing.assert_array_equal(counted, r["counted"])
+        np.testing.assert_array_equal(adv, r["adv_raw"])
+        advn = oracle.normalize_advantages(counted, adv, spec[0])
+        np.testing.assert_array_equal(advn, r["adv_norm"])
+        nv = d["new_value_scalar"] if spec[2] == 0 else d["new_value_vector"]
+        st, diag, clp, cent, cval = oracle.ppo_loss(d, spec, counted, advn, ret, d["logits"], nv, 0.2, 0.5, 0.01)
+        np.testing.assert_array_equal(diag, r["diag"])
+        g = sc.replay_ppo_grad(spec[2], counted, clp, cent, cval)
+        np.testing.assert_array_equal(g, r["grad"])
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+@pytest.mark.parametrize("ln", [True, False])
+def test_grpo_bitexact_and_gradient_replay(oracle, seed, ln):
+    sc = RefScenario(num_envs=12, group_size=4, use_fixed_reset_state_ids=1, auto_reset=0,
+                     deferred_reset=1, max_episode_steps=6, num_chunks=3, chunk_length=2,
+                     reward_shaping=seed % 2, env_seed=seed, net_seed=seed + 3)
+    d = sc.export()
+    for spec in [(0, 0, 0), (0, 1, 0), (0, 2, 0)]:
+        r = sc.grpo(spec, length_normalized=ln, want_grad=True)
+        st, a = oracle.assemble_grpo(d, spec, length_normalized=ln)
+        assert st == r["status"] or (st == 0 and r["status"] == 8)
+        for k in ("env_group", "env_member", "env_episode", "env_adv", "slot_weight", "slot_member"):
+            np.testing.assert_array_equal(a[k], r[k])
+        st, diag, coeff = oracle.grpo_loss(d, spec[1], a, d["logits"], 0.2)
+        assert st == r["status"]
+        if st == 0:
+            np.testing.assert_array_equal(diag, r["diag"])
+            np.testing.assert_array_equal(sc.replay_grpo_grad(spec, coeff, length_normalized=ln), r["grad"])
+
+
+def test_reference_rejects_what_the_abi_rejects():
+    sc = RefScenario()
+    assert sc.ppo((1, 0, 1))["status"] == 1   # UnsupportedCombination (action adv, chunk lp)
+    assert sc.ppo((0, 2, 1))["status"] == 12  # ConfigError (value level != advantage level)
