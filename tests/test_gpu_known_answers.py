@@ -88,7 +88,7 @@ def test_grpo_degenerate_group_without_eps():
 
 
 def ppo_loss_case(spec, rho_log, adv, clip=0.2):
-    d, logits, counted, a = ppo_case(tuple(int(x) for x in spec), rho_log, adv)
+    d, logits, counted, a = ppo_case((int(spec.advantage_level), int(spec.logprob_level), int(spec.value_level)), rho_log, adv)
     ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], 3)
     ws = Workspace(1)
     batch = PpoBatch(spec=spec, counted=dev(counted, torch.uint8), advantages=dev(a),
