@@ -11,7 +11,7 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libckrl.so")
+LIB_PATH = os.environ.get("CKRL_LIB") or os.path.join(HERE, "libckrl.so")
 
 LEVEL_CHUNK, LEVEL_ACTION, LEVEL_TOKEN = 0, 1, 2
 DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32 = 0, 1, 2, 3

@@ -366,6 +366,17 @@ static bool fused_enabled() {
   return on == 1;
 }
 
+// Overlapped (PDL) PPO step on/off (CKRL_ASM_SMS=0 disables). The assembly CTAs co-reside
+// with the loss kernel's CTAs, so no SMs are reserved (reserved_sms = 0 below).
+static int overlap_sms() {
+  static int n = -1;
+  if (n < 0) {
+    const char* env = getenv("CKRL_ASM_SMS");
+    n = env ? atoi(env) : 1;
+  }
+  return n;
+}
+
 static LossArgs ppo_args(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
                          const ckrl_policy_outputs* po, const ckrl_granularity* spec,
                          const ckrl_ppo_params* p, ckrl_loss_outputs* out, double* diag, void* ws,
@@ -521,6 +532,21 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
     if (e == cudaSuccess) return CKRL_OK;
     if (e != cudaErrorNotSupported) return fail(CKRL_ERR_CUDA, std::string("fused step: ") + cudaGetErrorString(e));
     cudaGetLastError();
+  }
+  if (world == 1 && overlap_sms() > 0 && po->logits_dtype >= 0) {
+    // Overlapped step: assembly on `overlap_sms()` SMs, the loss kernel launched as its
+    // programmatic dependent on the others — logits stream while the GAE scan runs.
+    const int rs = overlap_sms();
+    CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
+                                  gae->lambda, *b, w, L, s, rs));
+    LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
+                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1);
+    a.pdl = 1;
+    a.reserved_sms = 0;
+    (void)rs;
+    a.ro = *ro;
+    CKRL_CUDA(launch_tile(a, s, nullptr));
+    return CKRL_OK;
   }
   CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
                                 gae->lambda, *b, w, L, s));

@@ -9,6 +9,8 @@
 #include "gae.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace ckrl {
 
 // Last-block reduction of the per-CTA assembly partials into the rank's StatsRecord
@@ -63,24 +65,43 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   tickets[TICKET_ASM] = 0;  // self-reset for the next launch
 }
 
-__global__ void __launch_bounds__(kAsmWarpsPerCta * 32)
+// Two schedules: thread-per-env serial walk (short envs: <= kSerialItems items, the common
+// case — exact reference operation order) or warp-per-env affine scan (long envs). With
+// programmatic dependent launch the kernel lets the loss kernel start right away
+// (griddepcontrol.launch_dependents); the loss streams logits while this runs and its unit
+// phases wait for completion. The serial schedule's CTAs are small enough to co-reside
+// with the loss kernel's CTAs.
+template <bool SERIAL>
+__global__ void __launch_bounds__(128, 6)  // <= 85 regs: co-resides with a loss CTA
 ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lambda,
                     uint8_t* counted, float* adv, float* ret, char* ws, WsLayout L) {
-  __shared__ GaeSums wsum[kAsmWarpsPerCta];
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ GaeSums wsum[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int e = blockIdx.x * kAsmWarpsPerCta + warp;
+  const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
   GaeSums g{0.0, 0.0, 0.0, 0.0};
-  if (e < ro.num_envs) {
-    if (action_level)
-      g = warp_gae(ActionAcc{ro, e, counted, adv, ret}, ro.num_chunks * ro.chunk_len, gamma, lambda);
-    else
-      g = warp_gae(ChunkAcc{ro, e, counted, adv, ret}, ro.num_chunks, gamma, lambda);
+  if (SERIAL) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < ro.num_envs)
+      g = action_level ? serial_gae(ActionAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda)
+                       : serial_gae(ChunkAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda);
+    for (int off = 16; off > 0; off >>= 1) {
+      g.n += __shfl_down_sync(0xffffffffu, g.n, off);
+      g.s1 += __shfl_down_sync(0xffffffffu, g.s1, off);
+      g.s2 += __shfl_down_sync(0xffffffffu, g.s2, off);
+      g.counted_slots += __shfl_down_sync(0xffffffffu, g.counted_slots, off);
+    }
+  } else {
+    const int e = blockIdx.x * 4 + warp;
+    if (e < ro.num_envs)
+      g = action_level ? env_gae(ActionAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda)
+                       : env_gae(ChunkAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda);
   }
   if (lane == 0) wsum[warp] = g;
   __syncthreads();
   AsmPartial p{0.0, 0.0, 0.0, 0.0};
   if (threadIdx.x == 0)
-    for (int w = 0; w < kAsmWarpsPerCta; ++w) {
+    for (int w = 0; w < 4; ++w) {
       p.n += wsum[w].n;
       p.s1 += wsum[w].s1;
       p.s2 += wsum[w].s2;
@@ -385,13 +406,28 @@ __global__ void grpo_weights_kernel(ckrl_rollout ro, int length_normalized, ckrl
 }
 
 // ---- launchers ---------------------------------------------------------------------
+static bool serial_gae_enabled() {  // thread-per-env schedule (measured slower; opt-in)
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("CKRL_SERIAL_GAE");
+    on = (env && env[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
                                 double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
-                                cudaStream_t s) {
-  int grid = (ro.num_envs + kAsmWarpsPerCta - 1) / kAsmWarpsPerCta;
-  ppo_assemble_kernel<<<grid, kAsmWarpsPerCta * 32, 0, s>>>(ro, action_level, gamma, lambda,
-                                                             b.counted, b.advantages, b.returns,
-                                                             ws, L);
+                                cudaStream_t s, int /*reserved_sms*/) {
+  const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
+  if (serial_gae_enabled() && n_items <= kSerialItems) {
+    const int grid = (ro.num_envs + 127) / 128;
+    ppo_assemble_kernel<true><<<grid > 0 ? grid : 1, 128, 0, s>>>(
+        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
+  } else {
+    const int grid = (ro.num_envs + 3) / 4;
+    ppo_assemble_kernel<false><<<grid > 0 ? grid : 1, 128, 0, s>>>(
+        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
+  }
   return cudaGetLastError();
 }
 

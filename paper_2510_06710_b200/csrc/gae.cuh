@@ -127,6 +127,152 @@ __device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gam
   return st;  // valid in lane 0
 }
 
+// Register-resident variant: lane l owns items [l*K, l*K+K), all loaded once up front
+// (independent loads: one memory round trip), then the same scan as warp_gae.
+template <int K, class Acc>
+__device__ __noinline__ GaeSums warp_gae_regs(const Acc& acc, int n_items, double gamma, double lambda) {
+  const int lane = threadIdx.x & 31;
+  const int lo = lane * K;
+  const double gl = __dmul_rn(gamma, lambda);
+  Unit u[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    if (lo + q < n_items) {
+      u[q] = acc.load(lo + q);
+    } else {
+      u[q].is_unit = false;
+    }
+  }
+  bool h_has = false;
+  int32_t h_uid = 0;
+  double h_v = 0.0;
+#pragma unroll
+  for (int q = K - 1; q >= 0; --q)
+    if (u[q].is_unit) {
+      h_has = true;
+      h_uid = u[q].uid;
+      h_v = u[q].v;
+    }
+  for (int off = 1; off < 32; off <<= 1) {
+    const bool o_has = __shfl_down_sync(0xffffffffu, h_has, off);
+    const int32_t o_uid = __shfl_down_sync(0xffffffffu, h_uid, off);
+    const double o_v = __shfl_down_sync(0xffffffffu, h_v, off);
+    if (!h_has && lane + off < 32) {
+      h_has = o_has;
+      h_uid = o_uid;
+      h_v = o_v;
+    }
+  }
+  bool nx_has0 = __shfl_down_sync(0xffffffffu, h_has, 1);
+  const int32_t nx_uid0 = __shfl_down_sync(0xffffffffu, h_uid, 1);
+  const double nx_v0 = __shfl_down_sync(0xffffffffu, h_v, 1);
+  if (lane == 31) nx_has0 = false;
+  // per-item seg_end / delta (reverse, within the lane)
+  double delta[K];
+  bool segend[K];
+  {
+    bool nx_has = nx_has0;
+    int32_t nx_uid = nx_uid0;
+    double nx_v = nx_v0;
+#pragma unroll
+    for (int q = K - 1; q >= 0; --q) {
+      delta[q] = 0.0;
+      segend[q] = true;
+      if (!u[q].is_unit) continue;
+      segend[q] = u[q].term || u[q].trunc || !nx_has || nx_uid != u[q].uid;
+      const double vnext = u[q].term ? 0.0 : ((u[q].trunc || segend[q]) ? u[q].boot : nx_v);
+      delta[q] = __dadd_rn(__dadd_rn(u[q].r, __dmul_rn(gamma, vnext)), -u[q].v);
+      nx_has = true;
+      nx_uid = u[q].uid;
+      nx_v = u[q].v;
+    }
+  }
+  double P = 0.0, Q = 1.0;
+#pragma unroll
+  for (int q = K - 1; q >= 0; --q)
+    if (u[q].is_unit) {
+      const double c = segend[q] ? 0.0 : gl;
+      P = __dadd_rn(delta[q], __dmul_rn(c, P));
+      Q = __dmul_rn(c, Q);
+    }
+  for (int off = 1; off < 32; off <<= 1) {
+    const double oP = __shfl_down_sync(0xffffffffu, P, off);
+    const double oQ = __shfl_down_sync(0xffffffffu, Q, off);
+    if (lane + off < 32) {
+      P = __dadd_rn(P, __dmul_rn(Q, oP));
+      Q = __dmul_rn(Q, oQ);
+    }
+  }
+  double a_next = __shfl_down_sync(0xffffffffu, P, 1);
+  if (lane == 31) a_next = 0.0;
+  GaeSums st{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = K - 1; q >= 0; --q) {
+    if (lo + q >= n_items) continue;
+    if (!u[q].is_unit) {
+      acc.store_empty(lo + q);
+      continue;
+    }
+    const double a = __dadd_rn(delta[q], __dmul_rn(gl, segend[q] ? 0.0 : a_next));
+    acc.store(lo + q, u[q], a, __dadd_rn(a, u[q].v));
+    st.n += 1.0;
+    st.s1 += a;
+    st.s2 += a * a;
+    st.counted_slots += u[q].counted_slots;
+    a_next = a;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    st.n += __shfl_down_sync(0xffffffffu, st.n, off);
+    st.s1 += __shfl_down_sync(0xffffffffu, st.s1, off);
+    st.s2 += __shfl_down_sync(0xffffffffu, st.s2, off);
+    st.counted_slots += __shfl_down_sync(0xffffffffu, st.counted_slots, off);
+  }
+  return st;
+}
+
+// Dispatch on items per lane: register-resident for <= 4 items per lane, else re-reading.
+template <class Acc>
+__device__ __forceinline__ GaeSums env_gae(const Acc& acc, int n_items, double gamma, double lambda) {
+  if (n_items <= 32) return warp_gae_regs<1>(acc, n_items, gamma, lambda);
+  if (n_items <= 128) return warp_gae_regs<4>(acc, n_items, gamma, lambda);
+  return warp_gae(acc, n_items, gamma, lambda);
+}
+
+// Thread-per-env GAE for short item lists: one reverse walk, the reference's exact
+// operation order (gae.cpp:21-35 per segment) — bit-identical advantages — and no
+// shuffles. Used when an env has at most kSerialItems items.
+constexpr int kSerialItems = 256;
+
+template <class Acc>
+__device__ __forceinline__ GaeSums serial_gae(const Acc& acc, int n_items, double gamma, double lambda) {
+  const double gl = __dmul_rn(gamma, lambda);
+  GaeSums st{0.0, 0.0, 0.0, 0.0};
+  bool nx_has = false;
+  int32_t nx_uid = 0;
+  double nx_v = 0.0, a_next = 0.0;
+  for (int i = n_items - 1; i >= 0; --i) {
+    const Unit u = acc.load(i);
+    if (!u.is_unit) {
+      acc.store_empty(i);
+      continue;
+    }
+    const bool seg_end = u.term || u.trunc || !nx_has || nx_uid != u.uid;
+    const double vnext = u.term ? 0.0 : ((u.trunc || seg_end) ? u.boot : nx_v);
+    const double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
+    const double a = __dadd_rn(delta, __dmul_rn(gl, seg_end ? 0.0 : a_next));
+    acc.store(i, u, a, __dadd_rn(a, u.v));
+    st.n += 1.0;
+    st.s1 += a;
+    st.s2 += a * a;
+    st.counted_slots += u.counted_slots;
+    a_next = a;
+    nx_has = true;
+    nx_uid = u.uid;
+    nx_v = u.v;
+  }
+  return st;
+}
+
 // ---- accessors ------------------------------------------------------------------
 struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   const ckrl_rollout ro;

@@ -50,11 +50,15 @@ struct LossArgs {
   // fused PPO step (assembly inside the loss launch)
   ckrl_rollout ro;
   double gamma, lambda;
+  // overlapped step: the assembly kernel is still running on `reserved_sms` SMs when this
+  // kernel starts (programmatic dependent launch)
+  int pdl;
+  int reserved_sms;
 };
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
                                 double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
-                                cudaStream_t s);
+                                cudaStream_t s, int reserved_sms = 0);
 cudaError_t launch_flat_gae(int num_seqs, const int32_t* offs, const double* r, const double* v,
                             const double* b, const uint8_t* f, double gamma, double lambda,
                             double* adv, double* ret, cudaStream_t s);

@@ -241,10 +241,37 @@ struct UnitOut {
   double value, dlogprob, kl;
   int clipped;
 };
+// For |d| < 0.5 (almost every unit: d is the new-minus-old log-ratio) rho - 1 and the kl term
+// come from one Horner polynomial, exp(d) - 1 - d = d^2 * sum_{k>=2} d^(k-2)/k! (truncated
+// at k = 17, error < 1e-20): cheaper than libdevice exp and free of the cancellation in
+// (rho - 1) - d. Otherwise exp().
 __device__ __forceinline__ UnitOut surrogate_unit(double d, double adv, double eps) {
-  const double rho = exp(d);
+  double rho, kl;
+  if (fabs(d) < 0.5) {
+    double p = 1.0 / 355687428096000.0;                 // 1/17!
+    p = fma(p, d, 1.0 / 20922789888000.0);              // 1/16!
+    p = fma(p, d, 1.0 / 1307674368000.0);
+    p = fma(p, d, 1.0 / 87178291200.0);
+    p = fma(p, d, 1.0 / 6227020800.0);
+    p = fma(p, d, 1.0 / 479001600.0);
+    p = fma(p, d, 1.0 / 39916800.0);
+    p = fma(p, d, 1.0 / 3628800.0);
+    p = fma(p, d, 1.0 / 362880.0);
+    p = fma(p, d, 1.0 / 40320.0);
+    p = fma(p, d, 1.0 / 5040.0);
+    p = fma(p, d, 1.0 / 720.0);
+    p = fma(p, d, 1.0 / 120.0);
+    p = fma(p, d, 1.0 / 24.0);
+    p = fma(p, d, 1.0 / 6.0);
+    p = fma(p, d, 0.5);
+    kl = d * d * p;          // exp(d) - 1 - d
+    rho = 1.0 + (d + kl);
+  } else {
+    rho = exp(d);
+    kl = (rho - 1.0) - d;
+  }
   const Surrogate s = clipped_surrogate(rho, adv, eps);
-  return UnitOut{s.value, s.dlogprob, (rho - 1.0) - d, s.clipped ? 1 : 0};
+  return UnitOut{s.value, s.dlogprob, kl, s.clipped ? 1 : 0};
 }
 
 __device__ void finalize_diag(const LossArgs& a, const LossConsts& k, const double* raw,
@@ -589,7 +616,7 @@ __device__ __forceinline__ bool row_needed(const LossArgs& a, int mode, int64_t 
 // ---------------------------------------------------------------------------------
 template <int MODE, typename LT, bool FAST>
 __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ LossConsts s_k;
   __shared__ double s_red[kLossThreads / 32][RAW_COUNT];
   __shared__ bool s_last;
@@ -652,7 +679,6 @@ __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
 //     one consumer barrier per tile is needed.
 // ---------------------------------------------------------------------------------
 constexpr int kTmaConsumers = kLossThreads;      // 8 consumer warps
-constexpr int kTmaThreads = kTmaConsumers + 32;  // + producer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -876,7 +902,7 @@ __host__ __device__ constexpr size_t rowbuf_bytes() {
 // (counted slots are a subset); otherwise the assembled activity decides.
 template <int MODE, bool FUSED>
 __device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec, int lane,
-                                         const MetaSmem& m) {
+                                         const MetaSmem& m, bool from_flags) {
   const int C = a.C, P = C * a.M;
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P, s0 = r0 * C;
@@ -889,7 +915,7 @@ __device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec
     if (i < slots) {
       bool n = true;
       if (!a.all_rows && MODE != MODE_STATS) {
-        if (FUSED) {
+        if (FUSED || from_flags) {  // assembly outputs not available yet: every valid slot
           n = (a.ro.flags[s0 + i] & CKRL_FLAG_VALID) != 0;
         } else if (MODE == MODE_PPO) {
           n = a.counted[s0 + i] != 0;
@@ -934,7 +960,7 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
     if (i < rows) R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
     if (i < slots) {
       if (MODE == MODE_PPO) {
-        R.act[q] = (FUSED ? __ldcg(a.counted + s0 + i) : a.counted[s0 + i]) != 0 ? 2 : 0;
+        R.act[q] = __ldcg(a.counted + s0 + i) != 0 ? 2 : 0;
         R.w[q] = 0.0f;
       } else if (MODE == MODE_GRPO) {
         const int e = (int)((s0 + i) / C / a.Tc);
@@ -953,11 +979,11 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
       const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
       if (i < adv_units) {
         const float* p = a.adv + (a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i;
-        R.adv[q] = FUSED ? __ldcg(p) : *p;
+        R.adv[q] = __ldcg(p);
       }
       if (i < val_units) {
         const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
-        R.ret[q] = FUSED ? __ldcg(a.ret + vb + i) : a.ret[vb + i];
+        R.ret[q] = __ldcg(a.ret + vb + i);
         R.nv[q] = a.new_values ? __ldg(a.new_values + vb + i) : 0.0f;
       }
     }
@@ -1184,9 +1210,9 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
     uint8_t* cnt = const_cast<uint8_t*>(a.counted);
     float* adv = const_cast<float*>(a.adv);
     float* ret = const_cast<float*>(a.ret);
-    const GaeSums g = action ? warp_gae(ActionAcc{ro, e, cnt, adv, ret}, ro.num_chunks * ro.chunk_len,
-                                       a.gamma, a.lambda)
-                             : warp_gae(ChunkAcc{ro, e, cnt, adv, ret}, ro.num_chunks, a.gamma, a.lambda);
+    const GaeSums g = action ? env_gae(ActionAcc{ro, e, cnt, adv, ret}, ro.num_chunks * ro.chunk_len,
+                                      a.gamma, a.lambda)
+                             : env_gae(ChunkAcc{ro, e, cnt, adv, ret}, ro.num_chunks, a.gamma, a.lambda);
     acc.n += g.n;
     acc.s1 += g.s1;
     acc.s2 += g.s2;
@@ -1403,7 +1429,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
     int nrec = 0;
     if (tile < a.n_tiles) {  // rows of the first tile can start right away
       nrec = tile_recs(tile, r0);
-      row_meta<MODE, FUSED>(a, r0, nrec, lane, mt);
+      row_meta<MODE, FUSED>(a, r0, nrec, lane, mt, a.pdl != 0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&metafull_bar[b]);
       if (lane == 0 && b == 0) tl_mark(24);
@@ -1411,6 +1437,9 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
     if (FUSED) {
       fused_phase_a(a, b, lane, &s_kf);
     } else {
+      // overlapped step: the assembly kernel's outputs (stats record, counted, advantages)
+      // are consumed only from here on (no-op when not launched as a PDL dependent)
+      if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
       if (b == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
       bufwarps_sync();
     }
@@ -1428,7 +1457,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
       const int64_t ntile = tile + stride;
       if (ntile < a.n_tiles) {
         nrec = tile_recs(ntile, r0);
-        row_meta<MODE, FUSED>(a, r0, nrec, lane, mt);
+        row_meta<MODE, FUSED>(a, r0, nrec, lane, mt, a.pdl != 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
@@ -1510,6 +1539,19 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
   if (grid > a.n_tiles) grid = a.n_tiles;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = (int)grid;
+  if (!FUSED && a.pdl) {  // programmatic dependent of the assembly kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(tma_threads<ROWW>());
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, nstage, tile_bytes);
+  }
   if (!FUSED) {
     kern<<<(unsigned)grid, tma_threads<ROWW>(), smem, s>>>(a, nstage, tile_bytes);
     return cudaGetLastError();
