@@ -275,6 +275,70 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
  * [10] reduction done. Synchronises the device. */
 int32_t ckrl_debug_timeline(uint64_t* out, int32_t n);
 
+/* ---- (e) rollout pipeline on CUDA streams / events (cfg5) ----------------------------- */
+
+/* VecEnvConfig (envsim/vec_env.hpp:16-35) + the rollout's reset mode. */
+typedef struct {
+  int32_t kind; /* 0 toy_reach, 1 scripted */
+  int32_t num_envs, max_episode_steps, auto_reset, ignore_terminations, use_fixed_reset_state_ids;
+  int32_t chunk_len, grid_size, reward_shaping, num_reset_states, success_step;
+  int32_t deferred_reset; /* ResetMode::Deferred (rollout.hpp:19) */
+  uint64_t seed;
+} ckrl_env_config;
+
+/* PolicyDescriptor (policy/policy_net.hpp:15-26); parameters are the reference's flat f64
+ * layout (policy_net.cpp:107-152), device memory. */
+typedef struct {
+  int32_t obs_dim, hidden, trunk_layers, value_hidden, vocab, chunk_len, tokens_per_action;
+} ckrl_policy_desc;
+
+/* RolloutSpec (placement/rollout.hpp:16-22) + pipeline depth k (PlacementPlan::pipeline_stage_num). */
+typedef struct {
+  ckrl_env_config env;
+  ckrl_policy_desc policy;
+  int32_t num_chunks;
+  int32_t stages;                 /* k: env partitions, must divide num_envs */
+  uint64_t sample_seed;
+  const int32_t* reset_state_ids; /* [num_envs] device, or NULL */
+} ckrl_pipeline_spec;
+
+/* The epoch's slab in the ckrl_rollout layout (f32 for the loss, f64 copies for exact
+ * comparison with the reference) + the merged episode table. Device pointers. */
+typedef struct {
+  int32_t* tokens;            /* [E][T][C][M] */
+  float* old_logprob;         /* [E][T][C][M] */
+  double* old_logprob_f64;
+  float* reward;              /* [E][T][C] */
+  double* reward_f64;
+  uint8_t* flags;             /* [E][T][C] */
+  int32_t* episode_id;        /* [E][T][C] */
+  float* value_scalar;        /* [E][T] */
+  double* value_scalar_f64;
+  float* value_vector;        /* [E][T][C] */
+  double* value_vector_f64;
+  float* boot_scalar;         /* [E][T][C] scalar head on post_obs */
+  double* boot_scalar_f64;
+  float* boot_vector0;        /* [E][T][C] vector head [0] on post_obs */
+  double* boot_vector0_f64;
+  int32_t* episode_count;     /* [1] */
+  int32_t *ep_env_id, *ep_episode_id, *ep_start, *ep_length; /* [E*(T*C+1)] capacity */
+  double* ep_total_reward;
+  int32_t* ep_first_success;
+  uint8_t* ep_complete;
+  int32_t *ep_task, *ep_reset_id;
+  int32_t* status;            /* [1] device error word (BadResetId) */
+} ckrl_pipeline_outputs;
+
+int64_t ckrl_policy_num_params(const ckrl_policy_desc* desc);
+size_t ckrl_pipeline_workspace_bytes(const ckrl_pipeline_spec* spec);
+/* One rollout epoch (StageSim / StageGen / merge_stages, placement/rollout.cpp:11-109;
+ * RealBackend::run_rollout_epoch, real_backend.cpp:59-138): k stage partitions, gen and
+ * sim kernels on two streams with per-stage event hand-offs; the slab is identical for
+ * every k. Work is ordered after prior work on `stream`, and `stream` waits for it. */
+int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* spec, const double* params,
+                          ckrl_pipeline_outputs* out, void* workspace, size_t workspace_bytes,
+                          ckrl_stream_t stream);
+
 /* ---- multi-GPU (NCCL over NVLink): stats + loss scalars only -------------------------- */
 int32_t ckrl_comm_unique_id(void* out_id /* 128 bytes */);
 int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out);

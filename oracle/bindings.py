@@ -239,7 +239,7 @@ def _ref_lib():
         lib = C.CDLL(REF_SO)
         lib.refx_create.restype = C.c_void_p
         lib.refx_last_error.restype = C.c_char_p
-        for n in ("refx_export", "refx_export_episodes", "refx_ppo", "refx_grpo",
+        for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo", "refx_grpo",
                   "refx_replay_ppo_grad", "refx_replay_grpo_grad"):
             getattr(lib, n).restype = C.c_int
         for n in ("refx_bench_ppo", "refx_bench_grpo"):
@@ -299,6 +299,13 @@ class RefScenario:
         if not with_logits:
             d.pop("logits")
         return d
+
+    def params(self):
+        """(snapshot params f64, reset ids int32 or None) of the rollout."""
+        p = np.zeros(self.n_params)
+        ids = np.zeros(self.E, np.int32)
+        has = self.lib.refx_export_params(C.c_void_p(self.h), _p(p), _p(ids))
+        return p, (ids if has else None)
 
     def ppo(self, spec, gamma=0.99, lam=0.95, normalize=True, clip=0.2, vcoef=0.5, ecoef=0.01,
             want_grad=False):

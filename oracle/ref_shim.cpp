@@ -41,6 +41,7 @@ struct Scenario {
   policy::PolicyNet snapshot; // rollout (old) policy: sampled tokens, old logprobs, bootstraps
   policy::PolicyNet current;  // policy under optimisation: new logits / values
   TrajectorySlab slab;
+  std::vector<int> reset_ids; // RolloutSpec::reset_state_ids (empty: none)
   int E = 0, Tc = 0, C = 0, M = 0, V = 0;
 };
 
@@ -179,7 +180,8 @@ void* refx_create(const refx_cfg* cfg, int* status) {
       placement::GenBatch b = gen.generate(stages[0].first_env_id(), obs);
       obs = stages[0].execute(b);
     }
-    auto* s = new Scenario{snap, cur, placement::merge_stages(spec, stages)};
+    auto* s = new Scenario{snap, cur, placement::merge_stages(spec, stages),
+                           spec.reset_state_ids.value_or(std::vector<int>{})};
     // merge_stages probes M from the env (hard-coded 2); the policy defines it here.
     s->slab.tokens_per_action = desc.M;
     s->E = ec.num_envs;
@@ -207,6 +209,18 @@ void refx_dims(void* h, long long* dims) {
   dims[4] = s->V;
   dims[5] = static_cast<long long>(s->slab.episodes.size());
   dims[6] = static_cast<long long>(s->current.num_params());
+}
+
+// The rollout policy's flat parameter vector (policy_net.cpp:107-152 order) and the
+// spec's reset ids, so the CUDA pipeline can replay the same rollout.
+int refx_export_params(void* h, double* snapshot_params, int32_t* reset_ids) {
+  auto* s = static_cast<Scenario*>(h);
+  const std::vector<double>& p = s->snapshot.params();
+  std::memcpy(snapshot_params, p.data(), sizeof(double) * p.size());
+  if (reset_ids)
+    for (int e = 0; e < s->E; ++e)
+      reset_ids[e] = s->reset_ids.empty() ? -1 : s->reset_ids[static_cast<std::size_t>(e)];
+  return s->reset_ids.empty() ? 0 : 1;
 }
 
 // SoA export. Layout per include/ckrl.h: [E][Tc][C][M](...[V]).

@@ -80,6 +80,35 @@ class LossOutputs(C.Structure):
                 ("token_logprob", vp), ("token_entropy", vp)]
 
 
+class EnvConfig(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "kind", "num_envs", "max_episode_steps", "auto_reset", "ignore_terminations",
+        "use_fixed_reset_state_ids", "chunk_len", "grid_size", "reward_shaping",
+        "num_reset_states", "success_step", "deferred_reset")] + [("seed", C.c_uint64)]
+
+
+class PolicyDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("obs_dim", "hidden", "trunk_layers", "value_hidden",
+                                         "vocab", "chunk_len", "tokens_per_action")]
+
+
+class PipelineSpec(C.Structure):
+    _fields_ = [("env", EnvConfig), ("policy", PolicyDesc), ("num_chunks", C.c_int32),
+                ("stages", C.c_int32), ("sample_seed", C.c_uint64), ("reset_state_ids", vp)]
+
+
+PIPELINE_OUTPUT_FIELDS = (
+    "tokens", "old_logprob", "old_logprob_f64", "reward", "reward_f64", "flags", "episode_id",
+    "value_scalar", "value_scalar_f64", "value_vector", "value_vector_f64", "boot_scalar",
+    "boot_scalar_f64", "boot_vector0", "boot_vector0_f64", "episode_count", "ep_env_id",
+    "ep_episode_id", "ep_start", "ep_length", "ep_total_reward", "ep_first_success",
+    "ep_complete", "ep_task", "ep_reset_id", "status")
+
+
+class PipelineOutputs(C.Structure):
+    _fields_ = [(n, vp) for n in PIPELINE_OUTPUT_FIELDS]
+
+
 # (name, restype, argtypes) for every exported symbol of ckrl.h
 P = C.POINTER
 SIGNATURES = {
@@ -113,6 +142,10 @@ SIGNATURES = {
                                    P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
     "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
     "ckrl_debug_timeline": (C.c_int32, [vp, C.c_int32]),
+    "ckrl_policy_num_params": (C.c_int64, [P(PolicyDesc)]),
+    "ckrl_pipeline_workspace_bytes": (C.c_size_t, [P(PipelineSpec)]),
+    "ckrl_pipeline_run": (C.c_int32, [P(PipelineSpec), vp, P(PipelineOutputs), vp, C.c_size_t,
+                                      vp]),
     "ckrl_comm_unique_id": (C.c_int32, [vp]),
     "ckrl_comm_create": (C.c_int32, [C.c_int32, C.c_int32, vp, P(vp)]),
     "ckrl_comm_destroy": (C.c_int32, [vp]),

@@ -619,6 +619,44 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
   return CKRL_OK;
 }
 
+int64_t ckrl_policy_num_params(const ckrl_policy_desc* d) { return d ? policy_num_params(*d) : -1; }
+
+static int32_t check_pipeline(const ckrl_pipeline_spec* sp) {
+  CKRL_REQUIRE(sp != nullptr, CKRL_ERR_INVALID_ARGUMENT, "pipeline spec is null");
+  const ckrl_env_config& e = sp->env;
+  const ckrl_policy_desc& p = sp->policy;
+  CKRL_REQUIRE(e.kind == 0 || e.kind == 1, CKRL_ERR_CONFIG, "unknown env kind");
+  CKRL_REQUIRE(e.num_envs >= 1, CKRL_ERR_CONFIG, "VecEnv needs at least one env");
+  // vec_env.cpp:324-327, rollout.cpp:11-17
+  CKRL_REQUIRE(sp->stages >= 1 && e.num_envs % sp->stages == 0, CKRL_ERR_CONFIG,
+               "pipeline stage count must divide num_envs");
+  CKRL_REQUIRE(p.obs_dim == (e.kind == 0 ? 6 : 2), CKRL_ERR_LENGTH_MISMATCH, "observation dimension mismatch");
+  CKRL_REQUIRE(p.chunk_len == e.chunk_len, CKRL_ERR_LENGTH_MISMATCH, "chunk length mismatch");
+  CKRL_REQUIRE(p.tokens_per_action >= 2 || e.kind == 1, CKRL_ERR_CONFIG, "toy_reach needs 2 tokens per action");
+  CKRL_REQUIRE(p.hidden >= 1 && p.value_hidden >= 1 && p.vocab >= 1 && p.trunk_layers >= 0 &&
+                   sp->num_chunks >= 1 && e.max_episode_steps >= 1 && e.grid_size >= 2,
+               CKRL_ERR_CONFIG, "bad pipeline dimensions");
+  CKRL_REQUIRE(!e.use_fixed_reset_state_ids || sp->reset_state_ids, CKRL_ERR_BAD_RESET_ID,
+               "use_fixed_reset_state_ids requires reset_state_ids");
+  return CKRL_OK;
+}
+
+size_t ckrl_pipeline_workspace_bytes(const ckrl_pipeline_spec* sp) {
+  return check_pipeline(sp) == CKRL_OK ? pipeline_ws_bytes(*sp) : 0;
+}
+
+int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* sp, const double* params,
+                          ckrl_pipeline_outputs* out, void* ws, size_t ws_bytes,
+                          ckrl_stream_t stream) {
+  int32_t st = check_pipeline(sp);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  CKRL_REQUIRE(params && out && ws, CKRL_ERR_INVALID_ARGUMENT, "params / outputs / workspace required");
+  CKRL_REQUIRE(ws_bytes >= pipeline_ws_bytes(*sp), CKRL_ERR_INVALID_ARGUMENT, "pipeline workspace too small");
+  CKRL_CUDA(pipeline_run(*sp, params, *out, (char*)ws, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
 int32_t ckrl_debug_timeline(uint64_t* out, int32_t n) {
   CKRL_REQUIRE(out && n > 0, CKRL_ERR_INVALID_ARGUMENT, "bad timeline buffer");
   CKRL_CUDA(cudaDeviceSynchronize());

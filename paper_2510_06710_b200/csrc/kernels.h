@@ -71,5 +71,9 @@ cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t read_timeline(uint64_t* out, int n);
+size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp);
+int64_t policy_num_params(const ckrl_policy_desc& d);
+cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckrl_pipeline_outputs& out,
+                         char* ws, cudaStream_t stream);
 
 }  // namespace ckrl
