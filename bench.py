@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    p.add_argument("--stages", default="1,2,4", help="cfg5: pipeline depths k to time")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -238,7 +239,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        if args.config == "cfg5":
+            run_reference_pipeline(args, rank, world)
+        else:
+            run_reference(args, rank, world)
+        return
+    if args.config == "cfg5":
+        bench_pipeline(args, rank, world, local)
         return
 
     import numpy as np
@@ -424,6 +431,182 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- cfg5 pipeline
+CFG5 = dict(num_envs=256, num_chunks=10, chunk_len=8, tokens_per_action=7, vocab=256,
+            hidden=32, trunk_layers=1, value_hidden=16, grid_size=8, max_episode_steps=40)
+
+
+def cfg5_specs(num_envs, seed=0):
+    from paper_2510_06710_b200.pipeline import EnvConfig, PolicyDescriptor
+    c = CFG5
+    env = EnvConfig(kind=0, num_envs=num_envs, max_episode_steps=c["max_episode_steps"],
+                    chunk_len=c["chunk_len"], grid_size=c["grid_size"], reward_shaping=True,
+                    seed=seed)
+    pol = PolicyDescriptor(obs_dim=6, hidden=c["hidden"], trunk_layers=c["trunk_layers"],
+                           value_hidden=c["value_hidden"], vocab=c["vocab"],
+                           chunk_len=c["chunk_len"], tokens_per_action=c["tokens_per_action"])
+    return env, pol
+
+
+def cfg5_workload(world, ks):
+    c = CFG5
+    return {"workload": "cfg5: hybrid fine-grained pipeline, rollout (ToyReach env + "
+                        f"{c['hidden']}-wide policy, V={c['vocab']}, M={c['tokens_per_action']}) -> "
+                        "GAE -> PPO loss per epoch", "envs_per_gpu": c["num_envs"],
+            "steps_per_env": c["num_chunks"] * c["chunk_len"], "chunk": c["chunk_len"],
+            "action_dim": c["tokens_per_action"], "bins": c["vocab"], "stages": ks,
+            "global_envs": c["num_envs"] * world, "parallelism": f"env-sharded x{world}",
+            "l2": "slab is produced by the rollout inside the step (no replay of cached inputs)"}
+
+
+def bench_pipeline(args, rank, world, local):
+    """cfg5: one step = one epoch: GPU rollout through the k-stage stream pipeline
+    (gen / sim kernels, event hand-offs) -> assemble_ppo_batch -> fused PPO loss, with the
+    rollout policy's logits as the current policy's (first PPO epoch: ratio 1)."""
+    import torch
+    import paper_2510_06710_b200 as ck
+    from paper_2510_06710_b200 import optim
+    from paper_2510_06710_b200.core import (GaeParams, GranularitySpec, Level, PolicyOutputs,
+                                            PpoParams)
+    from paper_2510_06710_b200.pipeline import RolloutPipeline, random_params
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ck.lib()
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2510_06710_b200 import dist as ckdist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = ckdist.Comm.from_torch()
+    E, T, Cn = CFG5["num_envs"], CFG5["num_chunks"], CFG5["chunk_len"]
+    env, pol = cfg5_specs(E, seed=1000 + rank)
+    params = random_params(pol, seed=7, device=dev)
+    spec = GranularitySpec(Level.Chunk, Level.Chunk, Level.Chunk)
+    ks = [int(k) for k in args.stages.split(",") if E % int(k) == 0]
+    stream = torch.cuda.current_stream()
+    res = {}
+    for k in ks:
+        pipe = RolloutPipeline(env, pol, T, stages=k, sample_seed=77 + rank, device=dev,
+                               keep_logits=True)
+        pipe.launch(params)
+        torch.cuda.synchronize()
+        from paper_2510_06710_b200.pipeline import RolloutEpoch
+        ep = RolloutEpoch(t=dict(pipe.out), episodes=None, vocab=pol.vocab)
+        ro = ep.buffer(Level.Chunk)
+        outs = PolicyOutputs(pipe.out["logits"], pipe.out["value_scalar"])
+        step = optim.PpoStep(ro, GaeParams(0.99, 0.95), spec, PpoParams(0.2, 0.5, 0.01, True),
+                             comm=comm)
+
+        def epoch():
+            pipe.launch(params)
+            step(ro, outs)
+        for _ in range(max(3, args.warmup)):
+            epoch()
+        torch.cuda.synchronize()
+        K = max(1, min(args.steps, 20))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(K):
+                epoch()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        # rollout alone (the pipeline's share of the epoch)
+        r0.record(stream)
+        for _ in range(K):
+            pipe.launch(params)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rms = r0.elapsed_time(r1) / K
+        if world > 1:
+            t = torch.tensor([ms, rms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms, rms = (float(x) for x in t.tolist())
+        # e2e: parameters host->device (pinned) each epoch, loss scalars back
+        hp = params.cpu().pin_memory()
+        out = torch.empty(8, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(K):
+            params.copy_(hp, non_blocking=True)
+            epoch()
+            out.copy_(step.diag, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / K
+        steps_per_epoch = world * E * T * Cn
+        res[k] = {"value": steps_per_epoch / (ms * 1e-3), "ms_per_step": ms,
+                  "rollout_ms": rms, "e2e_value": steps_per_epoch / (ems * 1e-3),
+                  "h2d": hp.numel() * 8, "clocks": clk.summary(), "steps": K,
+                  "diag": step.diagnostics()}
+    if rank != 0:
+        return
+    best = max(res, key=lambda k: res[k]["value"])
+    r = res[best]
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": "env-steps/s", "n_gpus": world,
+        "steps": r["steps"], "warmup": max(3, args.warmup), "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic (random-init policy parameters)",
+        "config": {**cfg5_workload(world, ks), "reported_stages": best},
+        "pipeline": {str(k): {"env_steps_per_s": v["value"], "ms_per_epoch": v["ms_per_step"],
+                              "rollout_ms": v["rollout_ms"]} for k, v in res.items()},
+        "e2e": {"value": r["e2e_value"], "unit": "env-steps/s", "h2d_bytes_per_step": r["h2d"],
+                "d2h_bytes_per_step": 64},
+        "gpu_launches": r["steps"] * (1 + T * best * 2 + 2 + 2),
+        "clocks": r["clocks"],
+        "diagnostics": {kk: r["diag"][kk] for kk in ("loss", "value_loss", "entropy", "units")},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference_pipeline(args, rank, world):
+    """cfg5 reference arm: the reference's own rollout (StageSim / StageGen / merge_stages,
+    single-threaded as RealBackend's per-stage loop) + assemble + PPO loss, on a bounded
+    env sample of the cfg5 workload."""
+    if rank != 0:
+        return
+    from oracle import bindings
+    c = CFG5
+    n_env = 16
+    kw = dict(num_envs=n_env, num_chunks=c["num_chunks"], chunk_length=c["chunk_len"],
+              vocab=c["vocab"], tokens_per_action=c["tokens_per_action"], hidden=c["hidden"],
+              trunk_layers=c["trunk_layers"], value_hidden=c["value_hidden"],
+              grid_size=c["grid_size"], max_episode_steps=c["max_episode_steps"],
+              reward_shaping=1)
+    times = []
+    steps = max(1, min(args.steps, 5))
+    for i in range(max(0, min(args.warmup, 1)) + steps):
+        t0 = time.perf_counter()
+        sc = bindings.RefScenario(**kw, env_seed=100 + i)
+        sc.bench_ppo((0, 0, 0), 1, 1)
+        dt = time.perf_counter() - t0
+        if i >= min(args.warmup, 1):
+            times.append(dt)
+    per = sum(times) / len(times)
+    value = n_env * c["num_chunks"] * c["chunk_len"] / per
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "env-steps/s",
+            "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+            "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cfg5_workload(world, [1]),
+            "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": 1,
+                             "kind": "reference",
+                             "sample": f"{n_env} of {c['num_envs']} envs x {c['num_chunks']} "
+                                       "chunks: reference rollout + assemble + ppo_loss, 1 thread "
+                                       "(also exports the slab; an upper bound on its time)"},
+            "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def e2e_timing(args, cfg, rep, step, run, R, dev, world):

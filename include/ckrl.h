@@ -327,6 +327,8 @@ typedef struct {
   uint8_t* ep_complete;
   int32_t *ep_task, *ep_reset_id;
   int32_t* status;            /* [1] device error word (BadResetId) */
+  float* logits;              /* optional [E][T][C][M][V]: the rollout policy's logits (the
+                                 current policy's at the first PPO epoch), or NULL */
 } ckrl_pipeline_outputs;
 
 int64_t ckrl_policy_num_params(const ckrl_policy_desc* desc);

@@ -102,7 +102,7 @@ PIPELINE_OUTPUT_FIELDS = (
     "value_scalar", "value_scalar_f64", "value_vector", "value_vector_f64", "boot_scalar",
     "boot_scalar_f64", "boot_vector0", "boot_vector0_f64", "episode_count", "ep_env_id",
     "ep_episode_id", "ep_start", "ep_length", "ep_total_reward", "ep_first_success",
-    "ep_complete", "ep_task", "ep_reset_id", "status")
+    "ep_complete", "ep_task", "ep_reset_id", "status", "logits")
 
 
 class PipelineOutputs(C.Structure):

@@ -124,6 +124,10 @@ struct PipeArgs {
   EnvState st;
   ckrl_pipeline_outputs out;
   double* post_obs;  // [E][T][C][D]
+  const double* packed;  // transposed weight copies (packed_layout)
+  struct {
+    int64_t win, trunk, wpol, v1, v2, c1, c2, c3;
+  } pk;
 };
 
 __device__ void observe(const PipeArgs& a, int e, double* o) {
@@ -294,157 +298,300 @@ __global__ void env_chunk_kernel(PipeArgs a, int first, int count, int t) {
   observe(a, e, s.obs + (int64_t)e * D);
 }
 
-// ---- policy (policy_net.cpp:197-403), one warp per env --------------------------------
-// Row r of a matvec is owned by lane r % 32 and summed in column order (the reference's
-// order); vectors are exchanged through the warp's shared-memory slice.
-struct WarpScratch {
-  double *x, *h, *lg, *u1, *u2;
+// ---- policy (policy_net.cpp:197-403) ------------------------------------------------------
+// Products and sums are rounded separately (no FMA contraction), as the reference's x86-64
+// build computes them; only exp / log / tanh can differ from glibc (<= 1 ulp).
+__device__ __forceinline__ double madd(double s, double a, double b) { return __dadd_rn(s, __dmul_rn(a, b)); }
+
+// out[r] = act(sum_c W[r][c] in[c] (+ bias[r])) from the transposed copy WT[c][r]: row r is
+// summed in column order (the reference's order) by one thread; consecutive threads read
+// consecutive rows, so every weight load is coalesced.
+__device__ void matvec_t(const double* WT, const double* bias, int rows, int cols, const double* in,
+                         double* out, bool tanh_act, int tid, int nth) {
+  for (int r = tid; r < rows; r += nth) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < cols; ++c) s = madd(s, __ldg(WT + (int64_t)c * rows + r), in[c]);
+    const double v = bias ? __dadd_rn(s, __ldg(bias + r)) : s;
+    out[r] = tanh_act ? tanh(v) : v;
+  }
+}
+
+// Transposed copies of every weight matrix (W[rows][cols] -> WT[cols][rows]), built once per
+// run into the workspace; biases and embeddings are read in place.
+struct PackSeg {
+  int64_t src, dst;
+  int rows, cols;
+};
+constexpr int kMaxPackSegs = 8 + 64;
+
+struct PackTable {
+  PackSeg seg[kMaxPackSegs];
+  int n;
+  int64_t total;
+};
+
+__global__ void pack_kernel(const double* params, double* packed, PackTable tab) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tab.total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int q = 0;
+    int64_t base = 0;
+    while (q + 1 < tab.n && i >= base + (int64_t)tab.seg[q].rows * tab.seg[q].cols) {
+      base += (int64_t)tab.seg[q].rows * tab.seg[q].cols;
+      ++q;
+    }
+    const PackSeg& g = tab.seg[q];
+    const int64_t j = i - base;  // index in W (row-major)
+    const int64_t r = j / g.cols, c = j % g.cols;
+    packed[g.dst + c * g.rows + r] = params[g.src + j];
+  }
+}
+
+struct Packed {
+  int64_t win, trunk, wpol, v1, v2, c1, c2, c3, total;
+};
+
+Packed packed_layout(const PolicyLayout& L, PackTable* tab) {
+  Packed k;
+  int64_t off = 0;
+  int n = 0;
+  auto add = [&](int64_t src, int rows, int cols) {
+    const int64_t at = off;
+    if (tab) tab->seg[n] = PackSeg{src, at, rows, cols};
+    ++n;
+    off += (int64_t)rows * cols;
+    return at;
+  };
+  k.win = add(L.w_in, L.H, L.D);
+  k.trunk = off;
+  for (int l = 0; l < L.L; ++l) add(L.trunk + (int64_t)l * ((int64_t)L.H * L.H + L.H), L.H, L.H);
+  k.wpol = add(L.w_pol, L.V, L.H);
+  k.v1 = add(L.v1_w, L.Hv, L.H);
+  k.v2 = add(L.v2_w, L.Hv, L.Hv);
+  k.c1 = add(L.c1_w, L.Hv, L.H);
+  k.c2 = add(L.c2_w, L.Hv, L.Hv);
+  k.c3 = add(L.c3_w, L.C, L.Hv);
+  k.total = off;
+  if (tab) {
+    tab->n = n;
+    tab->total = off;
+  }
+  return k;
+}
+
+// Shared-memory slice of one env's policy evaluation (doubles, then the token prefix).
+struct PolScratch {
+  double *x, *h, *lg, *ex, *u1, *u2, *vs, *f0, *red, *embc;
   int32_t* prefix;
 };
 
-__device__ void matvec_rows(const double* W, const double* bias, int rows, int cols, const double* in,
-                            double* out, bool tanh_act, int lane) {
-  for (int r = lane; r < rows; r += 32) {
-    const double* row = W + (int64_t)r * cols;
-    double s = 0.0;
-    for (int c = 0; c < cols; ++c) s += row[c] * in[c];
-    out[r] = tanh_act ? tanh(s + bias[r]) : s + (bias ? bias[r] : 0.0);
-  }
-  __syncwarp();
+__host__ __device__ inline size_t pol_scratch_doubles(const PolicyLayout& L, bool emb_cache) {
+  return (size_t)2 * L.H + 2 * L.V + 2 * L.Hv + (L.C + 1) + L.H + 8 + (emb_cache ? (size_t)L.P * L.H : 0) +
+         ((size_t)L.P + 1) / 2 + 1;
 }
 
-// trunk_forward (policy_net.cpp:197-228): feature into ws.h (or ws.x when L == 0)
-__device__ const double* trunk(const PipeArgs& a, const double* p, const double* obs, int pos,
-                               const WarpScratch& w, int lane) {
+__device__ PolScratch carve(double* base, const PolicyLayout& L, bool emb_cache) {
+  PolScratch w;
+  w.x = base;
+  w.h = w.x + L.H;
+  w.lg = w.h + L.H;
+  w.ex = w.lg + L.V;
+  w.u1 = w.ex + L.V;
+  w.u2 = w.u1 + L.Hv;
+  w.vs = w.u2 + L.Hv;
+  w.f0 = w.vs + L.C + 1;
+  w.red = w.f0 + L.H;
+  w.embc = w.red + 8;
+  w.prefix = reinterpret_cast<int32_t*>(w.embc + (emb_cache ? (size_t)L.P * L.H : 0));
+  return w;
+}
+
+// trunk layers (policy_net.cpp:214-226) on x -> feature pointer; block- or warp-synchronous
+template <bool BLOCK>
+__device__ const double* trunk_layers(const PipeArgs& a, const double* pk, const PolScratch& w, int tid,
+                                      int nth) {
   const PolicyLayout& L = a.pl;
-  for (int hh = lane; hh < L.H; hh += 32) {
-    const double* row = p + L.w_in + (int64_t)hh * L.D;
-    double s = 0.0;
-    for (int c = 0; c < L.D; ++c) s += row[c] * obs[c];
-    s += p[L.b_in + hh] + p[L.pos_bias + (int64_t)pos * L.H + hh];
-    for (int k = 0; k < pos; ++k) s += p[L.emb + ((int64_t)k * L.V + w.prefix[k]) * L.H + hh];
-    w.x[hh] = s;
-  }
-  __syncwarp();
   const double* in = w.x;
   double* out = w.h;
   for (int l = 0; l < L.L; ++l) {
-    const int64_t base = L.trunk + (int64_t)l * ((int64_t)L.H * L.H + L.H);
-    matvec_rows(p + base, p + base + (int64_t)L.H * L.H, L.H, L.H, in, out, true, lane);
-    const double* tmp = in;
+    const int64_t bias = L.trunk + (int64_t)l * ((int64_t)L.H * L.H + L.H) + (int64_t)L.H * L.H;
+    matvec_t(pk + a.pk.trunk + (int64_t)l * L.H * L.H, a.params + bias, L.H, L.H, in, out, true, tid, nth);
+    if (BLOCK) __syncthreads(); else __syncwarp();
+    double* t = const_cast<double*>(in);
     in = out;
-    out = const_cast<double*>(tmp);
+    out = t;
   }
   return in;
 }
 
-__device__ void value_head(const PipeArgs& a, const double* p, const double* f, bool scalar,
-                           const WarpScratch& w, int lane, double* out) {
+// value (policy_net.cpp:336-372): both heads on the feature f
+template <bool BLOCK>
+__device__ void value_heads(const PipeArgs& a, const double* pk, const double* f, const PolScratch& w,
+                            int tid, int nth, double* scalar_out, double* vec_out) {
   const PolicyLayout& L = a.pl;
-  const int64_t w1 = scalar ? L.v1_w : L.c1_w, b1 = scalar ? L.v1_b : L.c1_b;
-  const int64_t w2 = scalar ? L.v2_w : L.c2_w, b2 = scalar ? L.v2_b : L.c2_b;
-  const int64_t w3 = scalar ? L.v3_w : L.c3_w, b3 = scalar ? L.v3_b : L.c3_b;
-  matvec_rows(p + w1, p + b1, L.Hv, L.H, f, w.u1, true, lane);
-  matvec_rows(p + w2, p + b2, L.Hv, L.Hv, w.u1, w.u2, true, lane);
-  matvec_rows(p + w3, p + b3, scalar ? 1 : L.C, L.Hv, w.u2, out, false, lane);
+  const double* p = a.params;
+  matvec_t(pk + a.pk.v1, p + L.v1_b, L.Hv, L.H, f, w.u1, true, tid, nth);
+  if (BLOCK) __syncthreads(); else __syncwarp();
+  matvec_t(pk + a.pk.v2, p + L.v2_b, L.Hv, L.Hv, w.u1, w.u2, true, tid, nth);
+  if (BLOCK) __syncthreads(); else __syncwarp();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int c = 0; c < L.Hv; ++c) s = madd(s, p[L.v3_w + c], w.u2[c]);
+    *scalar_out = __dadd_rn(s, p[L.v3_b]);
+  }
+  if (BLOCK) __syncthreads(); else __syncwarp();
+  matvec_t(pk + a.pk.c1, p + L.c1_b, L.Hv, L.H, f, w.u1, true, tid, nth);
+  if (BLOCK) __syncthreads(); else __syncwarp();
+  matvec_t(pk + a.pk.c2, p + L.c2_b, L.Hv, L.Hv, w.u1, w.u2, true, tid, nth);
+  if (BLOCK) __syncthreads(); else __syncwarp();
+  matvec_t(pk + a.pk.c3, p + L.c3_b, L.C, L.Hv, w.u2, vec_out, false, tid, nth);
+  if (BLOCK) __syncthreads(); else __syncwarp();
 }
 
-// StageGen::generate (rollout.cpp:68-83): sample_chunk + scalar and vector values
-__global__ void gen_kernel(PipeArgs a, int first, int count, int t) {
+constexpr int kGenThreads = 128;
+
+// StageGen::generate (rollout.cpp:68-83) for one env per CTA: sample_chunk
+// (policy_net.cpp:286-331) token by token, then the scalar and vector values of the obs.
+__global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first, int count, int t) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PolicyLayout& L = a.pl;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int e = first + blockIdx.x * (blockDim.x >> 5) + warp;
-  const int per_warp = 2 * L.H + L.V + 2 * L.Hv + L.C + 1;
-  WarpScratch w;
-  double* base = reinterpret_cast<double*>(smem) + (int64_t)warp * (per_warp + (L.P + 1) / 2 + 1);
-  w.x = base;
-  w.h = w.x + L.H;
-  w.lg = w.h + L.H;
-  w.u1 = w.lg + L.V;
-  w.u2 = w.u1 + L.Hv;
-  w.prefix = reinterpret_cast<int32_t*>(w.u2 + L.Hv + L.C + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int e = first + blockIdx.x;
   if (e >= first + count) return;
+  const PolScratch w = carve(reinterpret_cast<double*>(smem), L, true);
   const double* p = a.params;
+  const double* pk = a.packed;
   const double* obs = a.st.obs + (int64_t)e * L.D;
-  uint64_t rng = a.st.samp[e];
   const int64_t rec = (int64_t)e * a.T + t;
+  uint64_t rng = tid == 0 ? a.st.samp[e] : 0;
   for (int pos = 0; pos < L.P; ++pos) {
-    const double* f = trunk(a, p, obs, pos, w, lane);
-    matvec_rows(p + L.w_pol, p + L.b_pol, L.V, L.H, f, w.lg, false, lane);
-    // log_softmax (policy_net.cpp:90-102) and inverse-CDF draw (:306-316), in order
-    int tok = L.V - 1;
-    double lp = 0.0;
-    if (lane == 0) {
-      double mx = w.lg[0];
-      for (int v = 0; v < L.V; ++v) mx = w.lg[v] > mx ? w.lg[v] : mx;
+    // trunk input (policy_net.cpp:197-212): W_in obs + (b_in + pos_bias) + sum_k emb[k][tok_k]
+    for (int hh = tid; hh < L.H; hh += kGenThreads) {
+      double s = 0.0;
+      for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
+      s = __dadd_rn(s, __dadd_rn(__ldg(p + L.b_in + hh), __ldg(p + L.pos_bias + (int64_t)pos * L.H + hh)));
+#pragma unroll 8
+      for (int k = 0; k < pos; ++k) s = __dadd_rn(s, w.embc[k * L.H + hh]);
+      w.x[hh] = s;
+    }
+    __syncthreads();
+    const double* f = trunk_layers<true>(a, pk, w, tid, kGenThreads);
+    if (pos == 0)
+      for (int hh = tid; hh < L.H; hh += kGenThreads) w.f0[hh] = f[hh];
+    // logits (logits_from_feature) + block max
+    matvec_t(pk + a.pk.wpol, p + L.b_pol, L.V, L.H, f, w.lg, false, tid, kGenThreads);
+    double mx = -INFINITY;
+    for (int v = tid; v < L.V; v += kGenThreads) mx = fmax(mx, w.lg[v]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) w.red[warp] = mx;
+    __syncthreads();
+    mx = fmax(fmax(w.red[0], w.red[1]), fmax(w.red[2], w.red[3]));
+    // log_softmax (policy_net.cpp:90-102): exps in parallel, the sum in v order on thread 0
+    for (int v = tid; v < L.V; v += kGenThreads) w.ex[v] = exp(__dsub_rn(w.lg[v], mx));
+    if (a.out.logits) {
+      float* dst = a.out.logits + (rec * L.P + pos) * (int64_t)L.V;
+      for (int v = tid; v < L.V; v += kGenThreads) dst[v] = (float)w.lg[v];
+    }
+    __syncthreads();
+    if (tid == 0) {
       double sum = 0.0;
-      for (int v = 0; v < L.V; ++v) sum += exp(w.lg[v] - mx);
-      const double lse = mx + log(sum);
+#pragma unroll 8
+      for (int v = 0; v < L.V; ++v) sum = __dadd_rn(sum, w.ex[v]);
+      w.red[4] = __dadd_rn(mx, log(sum));
+    }
+    __syncthreads();
+    const double lse = w.red[4];
+    for (int v = tid; v < L.V; v += kGenThreads) w.ex[v] = exp(__dsub_rn(w.lg[v], lse));
+    __syncthreads();
+    // inverse-CDF draw (policy_net.cpp:306-316)
+    if (tid == 0) {
       const double u = rng_double(rng);
+      // blocks of 8: the loads leave the dependency chain, one branch per block. The running
+      // sum never decreases, so the block whose last partial sum exceeds u holds the token.
       double acc = 0.0;
-      for (int v = 0; v < L.V; ++v) {
-        acc += exp(w.lg[v] - lse);
-        if (u < acc) {
-          tok = v;
+      int tok = L.V - 1;
+      bool found = false;
+      int v = 0;
+      for (; v + 8 <= L.V; v += 8) {
+        double c[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[q] = w.ex[v + q];
+        c[0] = __dadd_rn(acc, c[0]);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) c[q] = __dadd_rn(c[q - 1], c[q]);
+        if (u < c[7]) {
+          int q = 7;
+#pragma unroll
+          for (int qq = 6; qq >= 0; --qq)
+            if (u < c[qq]) q = qq;
+          tok = v + q;
+          found = true;
           break;
         }
+        acc = c[7];
       }
-      lp = w.lg[tok] - lse;
-      w.prefix[pos] = tok;
+      for (; !found && v < L.V; ++v) {
+        acc = __dadd_rn(acc, w.ex[v]);
+        if (u < acc) {
+          tok = v;
+          found = true;
+        }
+      }
+      const double lp = __dsub_rn(w.lg[tok], lse);
       const int64_t k = rec * L.P + pos;
       a.out.tokens[k] = tok;
       a.out.old_logprob[k] = (float)lp;
       a.out.old_logprob_f64[k] = lp;
+      w.prefix[pos] = tok;
     }
-    __syncwarp();
+    __syncthreads();
+    const int tok = w.prefix[pos];
+    for (int hh = tid; hh < L.H; hh += kGenThreads)
+      w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
+    // the next position's trunk input reads embc[pos][hh] from the same thread
   }
-  if (lane == 0) a.st.samp[e] = rng;
-  // value heads on the chunk's observation (trunk at position 0, no prefix)
-  const double* f = trunk(a, p, obs, 0, w, lane);
-  double* vs = w.u2 + L.Hv;  // scalar, then C vector entries
-  value_head(a, p, f, true, w, lane, vs);
-  if (lane == 0) {
-    a.out.value_scalar[rec] = (float)vs[0];
-    a.out.value_scalar_f64[rec] = vs[0];
+  if (tid == 0) a.st.samp[e] = rng;
+  __syncthreads();
+  // StageGen's value calls re-run the trunk on the obs with an empty prefix: f0
+  value_heads<true>(a, pk, w.f0, w, tid, kGenThreads, w.vs, w.vs + 1);
+  if (tid == 0) {
+    a.out.value_scalar[rec] = (float)w.vs[0];
+    a.out.value_scalar_f64[rec] = w.vs[0];
   }
-  __syncwarp();
-  value_head(a, p, f, false, w, lane, vs);  // same feature: value() recomputes it identically
-  for (int c = lane; c < L.C; c += 32) {
-    a.out.value_vector[rec * L.C + c] = (float)vs[c];
-    a.out.value_vector_f64[rec * L.C + c] = vs[c];
+  for (int c = tid; c < L.C; c += kGenThreads) {
+    a.out.value_vector[rec * L.C + c] = (float)w.vs[1 + c];
+    a.out.value_vector_f64[rec * L.C + c] = w.vs[1 + c];
   }
 }
 
-// bootstrap values V(post_obs[slot]) for both heads (assembler.cpp:114-118, 148-152)
-__global__ void boot_kernel(PipeArgs a, int64_t nslots) {
+// bootstrap values V(post_obs[slot]) for both heads (assembler.cpp:114-118, 148-152), one
+// warp per slot
+constexpr int kBootWarps = 4;
+__global__ void __launch_bounds__(32 * kBootWarps) boot_kernel(PipeArgs a, int64_t nslots) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PolicyLayout& L = a.pl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t sl = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  const int per_warp = 2 * L.H + L.V + 2 * L.Hv + L.C + 1;
-  WarpScratch w;
-  double* base = reinterpret_cast<double*>(smem) + (int64_t)warp * (per_warp + (L.P + 1) / 2 + 1);
-  w.x = base;
-  w.h = w.x + L.H;
-  w.lg = w.h + L.H;
-  w.u1 = w.lg + L.V;
-  w.u2 = w.u1 + L.Hv;
-  w.prefix = reinterpret_cast<int32_t*>(w.u2 + L.Hv + L.C + 1);
+  const int64_t sl = (int64_t)blockIdx.x * kBootWarps + warp;
+  const PolScratch w =
+      carve(reinterpret_cast<double*>(smem) + (size_t)warp * pol_scratch_doubles(L, false), L, false);
   if (sl >= nslots) return;
+  const double* p = a.params;
+  const double* pk = a.packed;
   const double* obs = a.post_obs + sl * L.D;
-  double* vs = w.u2 + L.Hv;
-  const double* f = trunk(a, a.params, obs, 0, w, lane);
-  value_head(a, a.params, f, true, w, lane, vs);
-  if (lane == 0) {
-    a.out.boot_scalar[sl] = (float)vs[0];
-    a.out.boot_scalar_f64[sl] = vs[0];
+  for (int hh = lane; hh < L.H; hh += 32) {
+    double s = 0.0;
+    for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
+    w.x[hh] = __dadd_rn(s, __dadd_rn(p[L.b_in + hh], p[L.pos_bias + hh]));
   }
   __syncwarp();
-  value_head(a, a.params, f, false, w, lane, vs);
+  const double* f = trunk_layers<false>(a, pk, w, lane, 32);
+  value_heads<false>(a, pk, f, w, lane, 32, w.vs, w.vs + 1);
   if (lane == 0) {
-    a.out.boot_vector0[sl] = (float)vs[0];
-    a.out.boot_vector0_f64[sl] = vs[0];
+    a.out.boot_scalar[sl] = (float)w.vs[0];
+    a.out.boot_scalar_f64[sl] = w.vs[0];
+    a.out.boot_vector0[sl] = (float)w.vs[1];
+    a.out.boot_vector0_f64[sl] = w.vs[1];
   }
 }
 
@@ -490,7 +637,8 @@ __global__ void episodes_kernel(PipeArgs a) {
 }
 
 // ---- workspace ------------------------------------------------------------------------
-size_t pipeline_ws_layout(const ckrl_pipeline_spec& sp, EnvState* st, double** post_obs, char* base) {
+size_t pipeline_ws_layout(const ckrl_pipeline_spec& sp, EnvState* st, double** post_obs, char* base,
+                          double** packed = nullptr) {
   const int E = sp.env.num_envs;
   const int64_t cap = (int64_t)sp.num_chunks * sp.env.chunk_len + 1;
   const int D = sp.policy.obs_dim;
@@ -527,8 +675,10 @@ size_t pipeline_ws_layout(const ckrl_pipeline_spec& sp, EnvState* st, double** p
   s.ep_rid = (int32_t*)take(4 * E * cap);
   s.ep_complete = (uint8_t*)take(E * cap);
   double* po = (double*)take(8 * (size_t)E * sp.num_chunks * sp.env.chunk_len * D);
+  double* pw = (double*)take(8 * (size_t)packed_layout(make_layout(sp.policy), nullptr).total);
   if (st) *st = s;
   if (post_obs) *post_obs = po;
+  if (packed) *packed = pw;
   return off;
 }
 
@@ -536,34 +686,38 @@ size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp) { return pipeline_ws_layo
 int64_t policy_num_params(const ckrl_policy_desc& d) { return make_layout(d).total; }
 
 struct PipeStreams {
-  cudaStream_t gen = nullptr, sim = nullptr;
-  std::vector<cudaEvent_t> obs_ev, act_ev;
-  cudaEvent_t fork = nullptr, join_gen = nullptr, join_sim = nullptr;
+  std::vector<cudaStream_t> stage;
+  std::vector<cudaEvent_t> done;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  size_t gen_smem_set = 0, boot_smem_set = 0;
 };
 
 PipeStreams& pipe_streams(int k) {
-  static std::mutex mu;
   static PipeStreams ps;
-  std::lock_guard<std::mutex> g(mu);
-  if (!ps.gen) {
-    cudaStreamCreateWithFlags(&ps.gen, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&ps.sim, cudaStreamNonBlocking);
+  if (!ps.fork) {
     cudaEventCreateWithFlags(&ps.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ps.join_gen, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ps.join_sim, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ps.join, cudaEventDisableTiming);
   }
-  while ((int)ps.obs_ev.size() < k) {
-    cudaEvent_t a, b;
-    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-    ps.obs_ev.push_back(a);
-    ps.act_ev.push_back(b);
+  while ((int)ps.stage.size() < k) {
+    cudaStream_t st;
+    cudaEvent_t ev;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    ps.stage.push_back(st);
+    ps.done.push_back(ev);
   }
   return ps;
 }
 
+// RealBackend::run_rollout_epoch (real_backend.cpp:59-138) on one GPU: stage s owns envs
+// [s*E/k, (s+1)*E/k) (rollout.cpp:11-17) and its own stream, on which it runs
+// Reset -> (Gen(t) -> Sim(t)) x T; the k stage streams run concurrently, so stage s's env
+// step overlaps stage s'’s policy inference. Bootstrap values and the merged episode table
+// follow once every stage has finished.
 cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckrl_pipeline_outputs& out,
                          char* ws, cudaStream_t stream) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> guard(mu);
   PipeArgs a;
   std::memset(&a, 0, sizeof(a));
   a.env = sp.env;
@@ -574,41 +728,58 @@ cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckr
   a.sample_seed = sp.sample_seed;
   a.reset_ids = sp.reset_state_ids;
   a.out = out;
-  pipeline_ws_layout(sp, &a.st, &a.post_obs, ws);
+  double* packed = nullptr;
+  pipeline_ws_layout(sp, &a.st, &a.post_obs, ws, &packed);
+  a.packed = packed;
+  PackTable tab;
+  std::memset(&tab, 0, sizeof(tab));
+  if (a.pl.L + 7 > kMaxPackSegs) return cudaErrorInvalidValue;
+  const Packed pk = packed_layout(a.pl, &tab);
+  a.pk.win = pk.win;
+  a.pk.trunk = pk.trunk;
+  a.pk.wpol = pk.wpol;
+  a.pk.v1 = pk.v1;
+  a.pk.v2 = pk.v2;
+  a.pk.c1 = pk.c1;
+  a.pk.c2 = pk.c2;
+  a.pk.c3 = pk.c3;
   const int E = sp.env.num_envs, k = sp.stages, per = E / k, T = sp.num_chunks;
-  const int gen_warps = 4;
-  const size_t gen_smem =
-      (size_t)gen_warps * 8 * (2 * a.pl.H + a.pl.V + 2 * a.pl.Hv + a.pl.C + 1 + (a.pl.P + 1) / 2 + 1);
-  cudaError_t err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_smem);
-  if (err != cudaSuccess) return err;
-  err = cudaFuncSetAttribute(boot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_smem);
-  if (err != cudaSuccess) return err;
+  const size_t gen_smem = 8 * pol_scratch_doubles(a.pl, true);
+  const size_t boot_smem = 8 * (size_t)kBootWarps * pol_scratch_doubles(a.pl, false);
+  if (gen_smem > 227 * 1024 || boot_smem > 227 * 1024) return cudaErrorInvalidValue;
   PipeStreams& ps = pipe_streams(k);
-  cudaEventRecord(ps.fork, stream);
-  cudaStreamWaitEvent(ps.gen, ps.fork, 0);
-  cudaStreamWaitEvent(ps.sim, ps.fork, 0);
-  cudaMemsetAsync(out.status, 0, sizeof(int32_t), ps.sim);
-  // Reset (sim side), then per chunk: gen(s,t) after sim(s,t-1); sim(s,t) after gen(s,t).
-  for (int s = 0; s < k; ++s) {
-    env_reset_kernel<<<(per + 127) / 128, 128, 0, ps.sim>>>(a, s * per, per);
-    cudaEventRecord(ps.obs_ev[s], ps.sim);
+  cudaError_t err;
+  if (gen_smem > ps.gen_smem_set) {
+    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_smem)))
+      return err;
+    // the transposed weights are re-read every position: leave most of the SM's 256 KB to L1
+    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    gen_smem * 3 <= 64 * 1024 ? 25 : 100)))
+      return err;
+    ps.gen_smem_set = gen_smem;
   }
-  for (int t = 0; t < T; ++t)
-    for (int s = 0; s < k; ++s) {
-      cudaStreamWaitEvent(ps.gen, ps.obs_ev[s], 0);
-      gen_kernel<<<(per + gen_warps - 1) / gen_warps, 32 * gen_warps, gen_smem, ps.gen>>>(a, s * per, per, t);
-      cudaEventRecord(ps.act_ev[s], ps.gen);
-      cudaStreamWaitEvent(ps.sim, ps.act_ev[s], 0);
-      env_chunk_kernel<<<(per + 127) / 128, 128, 0, ps.sim>>>(a, s * per, per, t);
-      cudaEventRecord(ps.obs_ev[s], ps.sim);
+  if (boot_smem > ps.boot_smem_set) {
+    if ((err = cudaFuncSetAttribute(boot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)boot_smem)))
+      return err;
+    ps.boot_smem_set = boot_smem;
+  }
+  cudaMemsetAsync(out.status, 0, sizeof(int32_t), stream);
+  pack_kernel<<<(unsigned)std::min<int64_t>((tab.total + 255) / 256, 592), 256, 0, stream>>>(params, packed, tab);
+  cudaEventRecord(ps.fork, stream);
+  for (int s = 0; s < k; ++s) {
+    cudaStream_t st = ps.stage[s];
+    cudaStreamWaitEvent(st, ps.fork, 0);
+    env_reset_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per);
+    for (int t = 0; t < T; ++t) {
+      gen_kernel<<<per, kGenThreads, gen_smem, st>>>(a, s * per, per, t);
+      env_chunk_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per, t);
     }
+    cudaEventRecord(ps.done[s], st);
+    cudaStreamWaitEvent(stream, ps.done[s], 0);
+  }
   const int64_t nslots = (int64_t)E * T * sp.env.chunk_len;
-  boot_kernel<<<(unsigned)((nslots + gen_warps - 1) / gen_warps), 32 * gen_warps, gen_smem, ps.sim>>>(a, nslots);
-  episodes_kernel<<<1, 256, 0, ps.sim>>>(a);
-  cudaEventRecord(ps.join_gen, ps.gen);
-  cudaEventRecord(ps.join_sim, ps.sim);
-  cudaStreamWaitEvent(stream, ps.join_gen, 0);
-  cudaStreamWaitEvent(stream, ps.join_sim, 0);
+  boot_kernel<<<(unsigned)((nslots + kBootWarps - 1) / kBootWarps), 32 * kBootWarps, boot_smem, stream>>>(a, nslots);
+  episodes_kernel<<<1, 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

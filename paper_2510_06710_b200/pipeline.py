@@ -100,7 +100,8 @@ class RolloutPipeline:
 
     def __init__(self, env: EnvConfig, policy: PolicyDescriptor, num_chunks: int,
                  stages: int = 1, sample_seed: int = 0,
-                 reset_state_ids: Optional[torch.Tensor] = None, device="cuda"):
+                 reset_state_ids: Optional[torch.Tensor] = None, device="cuda",
+                 keep_logits: bool = False):
         self.env, self.policy, self.num_chunks, self.stages = env, policy, num_chunks, stages
         self.sample_seed = sample_seed
         self.device = torch.device(device)
@@ -113,6 +114,7 @@ class RolloutPipeline:
         if nbytes == 0:  # invalid spec: re-run validation to raise the reference's exception
             _lib.check(self._lib.ckrl_pipeline_run(C.byref(self.spec), None, None, None, 0, None))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.keep_logits = keep_logits
         self.out = self._alloc()
         self.c_out = _lib.PipelineOutputs(*[_ptr(self.out[n])
                                             for n in _lib.PIPELINE_OUTPUT_FIELDS])
@@ -138,6 +140,8 @@ class RolloutPipeline:
                  ep_start=z(cap, i32), ep_length=z(cap, i32), ep_total_reward=z(cap, f64),
                  ep_first_success=z(cap, i32), ep_complete=z(cap, u8), ep_task=z(cap, i32),
                  ep_reset_id=z(cap, i32), status=z(1, i32))
+        o["logits"] = (torch.empty((E, T, Cn, M, self.policy.vocab), dtype=f32, device=dev)
+                       if self.keep_logits else None)
         return o
 
     def launch(self, params: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):

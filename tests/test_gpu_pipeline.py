@@ -94,7 +94,7 @@ def run_pipeline(name, stages, p, ids):
                            reset_state_ids=None if ids is None else torch.tensor(ids))
     ep = pipe.run(torch.tensor(p, dtype=torch.float64, device="cuda"))
     torch.cuda.synchronize()
-    host = {k: v.cpu().numpy() for k, v in ep.t.items()}
+    host = {k: v.cpu().numpy() for k, v in ep.t.items() if v is not None}
     n = int(host["episode_count"][0])
     for k in [k for k in host if k.startswith("ep_")]:
         host[k] = host[k][:n]
@@ -124,6 +124,19 @@ def test_pipeline_vs_reference_rollout(name, ref_cache):
     assert g["ep_env_id"].size == d["ep_env_id"].size, "episode count"
     for k in EPISODE:
         np.testing.assert_array_equal(g[k], d[k].astype(g[k].dtype), err_msg=k)
+
+
+def test_pipeline_logits_output(ref_cache):
+    """keep_logits: the sampled tokens' log-softmax over the stored logits is the old lp."""
+    name = "v256_m7"
+    _, d, p, ids = ref_cache(name)
+    cfg, env, pol = specs_of(SCENARIOS[name])
+    pipe = RolloutPipeline(env, pol, cfg["num_chunks"], sample_seed=cfg["sample_seed"],
+                           keep_logits=True)
+    ep = pipe.run(torch.tensor(p, dtype=torch.float64, device="cuda"))
+    lg = ep.t["logits"].double()
+    lp = torch.log_softmax(lg, -1).gather(-1, ep.t["tokens"].long().unsqueeze(-1)).squeeze(-1)
+    assert_close(lp.cpu().numpy(), d["old_logprob"], 1e-5, "lp from stored logits")
 
 
 @pytest.mark.parametrize("name", sorted(SCENARIOS))
