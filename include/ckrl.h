@@ -217,6 +217,33 @@ int32_t ckrl_assemble_grpo_batch(const ckrl_rollout* rollout, const ckrl_episode
                                  ckrl_grpo_batch* batch, void* workspace, size_t workspace_bytes,
                                  ckrl_stream_t stream);
 
+/* Per-group / per-episode GRPO helpers (advantage/grpo.hpp:32-53), batched: groups are
+ * back-to-back segments of `returns` delimited by group_offsets[num_groups+1]; episodes are
+ * segments of the per-step outputs delimited by step_offsets[num_episodes+1]. All device
+ * pointers; bit-identical to the reference's fp64 arithmetic. Device-side errors
+ * (DegenerateGroup: a group smaller than 2, or zero std with eps_std == 0) are written to
+ * *status (device int32, first error wins; may be NULL). */
+int32_t ckrl_grpo_group_advantage(int32_t num_groups, const int32_t* group_offsets,
+                                  const double* returns, double eps_std, double* advantages,
+                                  int32_t* status, ckrl_stream_t stream);
+/* keep[g] = lower < group_mean_return < upper (strict); group_mean (nullable) receives the
+ * means of group_mean_return (grpo.cpp:30-46). */
+int32_t ckrl_success_rate_filter(int32_t num_groups, const int32_t* group_offsets,
+                                 const double* returns, double lower, double upper,
+                                 uint8_t* keep, double* group_mean, ckrl_stream_t stream);
+/* valid_action_mask / length_norm_weights (grpo.cpp:48-79) per episode; either output may
+ * be NULL. */
+int32_t ckrl_valid_action_mask(int32_t num_episodes, const int64_t* step_offsets,
+                               const uint8_t* success, const int64_t* first_success_step,
+                               uint8_t* mask, ckrl_stream_t stream);
+int32_t ckrl_length_norm_weights(int32_t num_episodes, const int64_t* step_offsets,
+                                 const uint8_t* success, const int64_t* first_success_step,
+                                 int32_t length_normalized, double* weights,
+                                 ckrl_stream_t stream);
+/* slab_success_rate (advantage/assembler.cpp:269-278): success_once fraction over complete
+ * episodes, into *out (device f64). */
+int32_t ckrl_slab_success_rate(const ckrl_episodes* episodes, double* out, ckrl_stream_t stream);
+
 /* ---- (b) fused action-token kernel ---------------------------------------------------- */
 
 /* PolicyNet::evaluate_chunk (policy/policy_net.cpp:333-357) + aggregate_logprob

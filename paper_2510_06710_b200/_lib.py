@@ -142,6 +142,12 @@ SIGNATURES = {
                                    P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
     "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
     "ckrl_debug_timeline": (C.c_int32, [vp, C.c_int32]),
+    "ckrl_grpo_group_advantage": (C.c_int32, [C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
+    "ckrl_success_rate_filter": (C.c_int32, [C.c_int32, vp, vp, C.c_double, C.c_double, vp, vp,
+                                             vp]),
+    "ckrl_valid_action_mask": (C.c_int32, [C.c_int32, vp, vp, vp, vp, vp]),
+    "ckrl_length_norm_weights": (C.c_int32, [C.c_int32, vp, vp, vp, C.c_int32, vp, vp]),
+    "ckrl_slab_success_rate": (C.c_int32, [P(Episodes), vp, vp]),
     "ckrl_policy_num_params": (C.c_int64, [P(PolicyDesc)]),
     "ckrl_pipeline_workspace_bytes": (C.c_size_t, [P(PipelineSpec)]),
     "ckrl_pipeline_run": (C.c_int32, [P(PipelineSpec), vp, P(PipelineOutputs), vp, C.c_size_t,

@@ -619,6 +619,54 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
   return CKRL_OK;
 }
 
+int32_t ckrl_grpo_group_advantage(int32_t G, const int32_t* off, const double* R, double eps,
+                                  double* adv, int32_t* status, ckrl_stream_t stream) {
+  CKRL_REQUIRE(G >= 0 && (G == 0 || (off && R && adv)), CKRL_ERR_INVALID_ARGUMENT, "bad group arguments");
+  int32_t st;
+  if ((st = check_device())) return st;
+  CKRL_CUDA(launch_group_advantage(G, off, R, eps, adv, status, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_success_rate_filter(int32_t G, const int32_t* off, const double* R, double lower,
+                                 double upper, uint8_t* keep, double* mean, ckrl_stream_t stream) {
+  CKRL_REQUIRE(G >= 0 && (G == 0 || (off && R)), CKRL_ERR_INVALID_ARGUMENT, "bad group arguments");
+  int32_t st;
+  if ((st = check_device())) return st;
+  CKRL_CUDA(launch_success_filter(G, off, R, lower, upper, keep, mean, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_valid_action_mask(int32_t n, const int64_t* off, const uint8_t* success,
+                               const int64_t* fs, uint8_t* mask, ckrl_stream_t stream) {
+  CKRL_REQUIRE(n >= 0 && (n == 0 || (off && success && fs)), CKRL_ERR_INVALID_ARGUMENT,
+               "bad episode arguments");
+  int32_t st;
+  if ((st = check_device())) return st;
+  CKRL_CUDA(launch_mask_weights(n, off, success, fs, 1, mask, nullptr, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_length_norm_weights(int32_t n, const int64_t* off, const uint8_t* success,
+                                 const int64_t* fs, int32_t normalized, double* w,
+                                 ckrl_stream_t stream) {
+  CKRL_REQUIRE(n >= 0 && (n == 0 || (off && success && fs)), CKRL_ERR_INVALID_ARGUMENT,
+               "bad episode arguments");
+  int32_t st;
+  if ((st = check_device())) return st;
+  CKRL_CUDA(launch_mask_weights(n, off, success, fs, normalized, nullptr, w, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_slab_success_rate(const ckrl_episodes* eps, double* out, ckrl_stream_t stream) {
+  CKRL_REQUIRE(eps && out && eps->count >= 0 && (eps->count == 0 || (eps->complete && eps->first_success)),
+               CKRL_ERR_INVALID_ARGUMENT, "bad episode table");
+  int32_t st;
+  if ((st = check_device())) return st;
+  CKRL_CUDA(launch_success_rate(eps->count, eps->complete, eps->first_success, out, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
 int64_t ckrl_policy_num_params(const ckrl_policy_desc* d) { return d ? policy_num_params(*d) : -1; }
 
 static int32_t check_pipeline(const ckrl_pipeline_spec* sp) {

@@ -72,6 +72,13 @@ cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t read_timeline(uint64_t* out, int n);
 size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp);
+cudaError_t launch_group_advantage(int G, const int32_t* off, const double* R, double eps, double* adv,
+                                   int32_t* status, cudaStream_t s);
+cudaError_t launch_success_filter(int G, const int32_t* off, const double* R, double lower, double upper,
+                                  uint8_t* keep, double* mean_out, cudaStream_t s);
+cudaError_t launch_mask_weights(int n_eps, const int64_t* off, const uint8_t* success, const int64_t* fs,
+                                int normalized, uint8_t* mask, double* w, cudaStream_t s);
+cudaError_t launch_success_rate(int n, const uint8_t* complete, const int32_t* fs, double* out, cudaStream_t s);
 int64_t policy_num_params(const ckrl_policy_desc& d);
 cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckrl_pipeline_outputs& out,
                          char* ws, cudaStream_t stream);
