@@ -244,6 +244,28 @@ int32_t ckrl_length_norm_weights(int32_t num_episodes, const int64_t* step_offse
  * episodes, into *out (device f64). */
 int32_t ckrl_slab_success_rate(const ckrl_episodes* episodes, double* out, ckrl_stream_t stream);
 
+/* Minibatches. optim::ppo_loss / grpo_loss evaluate a subset of the batch (record_indices /
+ * group_indices, losses.hpp:54-65; drawn by update_ppo / update_grpo, update.cpp:83-160).
+ *
+ * ckrl_select_records gathers records record_index[i] = env * num_chunks + chunk (device
+ * int64, n entries) of (src, src_batch, src_policy) into the caller-allocated buffers of
+ * (dst, dst_batch, dst_policy), laid out as num_envs = n, num_chunks = 1 (the dst arrays
+ * are written; dims/dtypes must match src), and writes the subset's normalisers
+ * (n_adv, n_val, n_pos) into `workspace` (sized for n envs). A following ckrl_ppo_loss on
+ * the dst view with advantage_normalization = 0 is the minibatch loss.
+ *
+ * ckrl_select_groups keeps the envs of the n groups group_index[] (retained-group ordinals,
+ * device int32) in dst_env_group (others -1) and sets the loss's group count to n in
+ * `workspace` (the workspace that holds the GRPO assembly). */
+int32_t ckrl_select_records(const ckrl_rollout* src, const ckrl_ppo_batch* src_batch,
+                            const ckrl_policy_outputs* src_policy, const ckrl_granularity* spec,
+                            int64_t n, const int64_t* record_index, const ckrl_rollout* dst,
+                            const ckrl_ppo_batch* dst_batch, const ckrl_policy_outputs* dst_policy,
+                            void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
+int32_t ckrl_select_groups(int32_t num_envs, const int32_t* src_env_group, int32_t* dst_env_group,
+                           int32_t n, const int32_t* group_index, void* workspace,
+                           size_t workspace_bytes, ckrl_stream_t stream);
+
 /* ---- (b) fused action-token kernel ---------------------------------------------------- */
 
 /* PolicyNet::evaluate_chunk (policy/policy_net.cpp:333-357) + aggregate_logprob

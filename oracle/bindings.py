@@ -239,7 +239,8 @@ def _ref_lib():
         lib = C.CDLL(REF_SO)
         lib.refx_create.restype = C.c_void_p
         lib.refx_last_error.restype = C.c_char_p
-        for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo", "refx_grpo",
+        for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo_subset",
+                  "refx_grpo_subset", "refx_ppo", "refx_grpo",
                   "refx_replay_ppo_grad", "refx_replay_grpo_grad"):
             getattr(lib, n).restype = C.c_int
         for n in ("refx_bench_ppo", "refx_bench_grpo"):
@@ -322,6 +323,27 @@ class RefScenario:
         out["status"] = st
         out["grad"] = grad
         return out
+
+    def ppo_subset(self, spec, idx, gamma=0.99, lam=0.95, normalize=True, clip=0.2, vcoef=0.5,
+                   ecoef=0.01):
+        """ppo_loss over record_indices `idx` (record = env * Tc + chunk)."""
+        ix = np.ascontiguousarray(idx, np.int64)
+        diag = np.zeros(7)
+        st = self.lib.refx_ppo_subset(C.c_void_p(self.h), spec[0], spec[1], spec[2], C.c_double(gamma),
+                                      C.c_double(lam), int(normalize), C.c_double(clip),
+                                      C.c_double(vcoef), C.c_double(ecoef), C.c_longlong(ix.size),
+                                      _p(ix), _p(diag))
+        return st, diag
+
+    def grpo_subset(self, spec, idx, eps_std=1e-8, apply_filter=True, lower=0.0, upper=1.0,
+                    length_normalized=True, min_group_size=2, clip=0.2):
+        ix = np.ascontiguousarray(idx, np.int64)
+        diag = np.zeros(7)
+        st = self.lib.refx_grpo_subset(C.c_void_p(self.h), spec[0], spec[1], spec[2],
+                                       C.c_double(eps_std), int(apply_filter), C.c_double(lower),
+                                       C.c_double(upper), int(length_normalized), min_group_size,
+                                       C.c_double(clip), C.c_longlong(ix.size), _p(ix), _p(diag))
+        return st, diag
 
     def replay_ppo_grad(self, val_level, counted, coeff_lp, coeff_ent, coeff_val):
         g = np.zeros(self.n_params)

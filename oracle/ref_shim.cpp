@@ -392,6 +392,60 @@ int refx_replay_ppo_grad(void* h, int val_level, const uint8_t* counted, const d
   }
 }
 
+// Minibatch forms: ppo_loss over record_indices (whitening once over the whole batch first,
+// update.cpp:66-67) and grpo_loss over group_indices, in the given order.
+int refx_ppo_subset(void* h, int adv_level, int lp_level, int val_level, double gamma, double lambda,
+                    int normalize, double clip_eps, double vcoef, double ecoef, long long n,
+                    const long long* idx, double* diag) {
+  auto* s = static_cast<Scenario*>(h);
+  try {
+    advantage::PpoAssemblyOptions opts;
+    opts.gae = advantage::GaeParams{gamma, lambda};
+    opts.spec = GranularitySpec{level_of(adv_level), level_of(lp_level), level_of(val_level)};
+    advantage::PpoBatch batch = advantage::assemble_ppo_batch(s->slab, s->snapshot, opts);
+    if (normalize)
+      optim::normalize_advantages(batch);
+    optim::PpoParams params;
+    params.clip_eps = clip_eps;
+    params.value_loss_coef = vcoef;
+    params.entropy_coef = ecoef;
+    std::vector<std::size_t> sel(static_cast<std::size_t>(n));
+    for (long long i = 0; i < n; ++i)
+      sel[static_cast<std::size_t>(i)] = static_cast<std::size_t>(idx[i]);
+    diag_out(optim::ppo_loss(s->current, batch, sel, params, nullptr), diag);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
+  }
+}
+
+int refx_grpo_subset(void* h, int adv_level, int lp_level, int val_level, double eps_std, int apply_filter,
+                     double lower, double upper, int length_normalized, int min_group_size,
+                     double clip_eps, long long n, const long long* idx, double* diag) {
+  auto* s = static_cast<Scenario*>(h);
+  try {
+    advantage::GrpoAssemblyOptions o;
+    o.spec = GranularitySpec{level_of(adv_level), level_of(lp_level), level_of(val_level)};
+    o.eps_std = eps_std;
+    o.apply_filter = apply_filter != 0;
+    o.filter_bounds = advantage::FilterBounds{lower, upper};
+    o.length_normalized = length_normalized != 0;
+    o.min_group_size = min_group_size;
+    advantage::GrpoAssemblyResult res = advantage::assemble_grpo_batch(s->slab, o);
+    optim::GrpoParams p;
+    p.clip_eps = clip_eps;
+    std::vector<std::size_t> sel(static_cast<std::size_t>(n));
+    for (long long i = 0; i < n; ++i)
+      sel[static_cast<std::size_t>(i)] = static_cast<std::size_t>(idx[i]);
+    diag_out(optim::grpo_loss(s->current, res.batch, sel, p, nullptr), diag);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
+  }
+}
+
 // assemble_grpo_batch -> grpo_loss over every retained group. Per-env outputs
 // describe the (at most one) retained trajectory each env owns; slot_weight is
 // the trajectory's per-slot weight (0 outside it).

@@ -619,6 +619,42 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
   return CKRL_OK;
 }
 
+int32_t ckrl_select_records(const ckrl_rollout* src, const ckrl_ppo_batch* sb, const ckrl_policy_outputs* sp,
+                            const ckrl_granularity* spec, int64_t n, const int64_t* idx,
+                            const ckrl_rollout* dst, const ckrl_ppo_batch* db, const ckrl_policy_outputs* dp,
+                            void* ws, size_t ws_bytes, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(src, false))) return st;
+  if ((st = check_rollout(dst, false))) return st;
+  CKRL_REQUIRE(sb && db && sp && dp && sp->logits && dp->logits && sb->counted && db->counted &&
+                   sb->advantages && db->advantages && sb->returns && db->returns,
+               CKRL_ERR_INVALID_ARGUMENT, "batches / policy outputs required");
+  CKRL_REQUIRE(n >= 1 && n <= INT32_MAX && idx, CKRL_ERR_INVALID_ARGUMENT, "empty record selection");
+  CKRL_REQUIRE(dst->num_envs == n && dst->num_chunks == 1 && dst->chunk_len == src->chunk_len &&
+                   dst->tokens_per_action == src->tokens_per_action && dst->vocab == src->vocab &&
+                   dst->token_dtype == src->token_dtype && dp->logits_dtype == sp->logits_dtype,
+               CKRL_ERR_LENGTH_MISMATCH, "selection view must be [n][1] with the source's C, M, V, dtypes");
+  CKRL_REQUIRE(!sp->values || dp->values, CKRL_ERR_INVALID_ARGUMENT, "dst values required");
+  if ((st = check_ws(ws, ws_bytes, (int)n, 1))) return st;
+  CKRL_CUDA(launch_select_records(*src, *sb, *sp, spec->advantage_level == CKRL_LEVEL_ACTION,
+                                  spec->value_level == CKRL_LEVEL_ACTION, n, idx, *dst, *db, *dp,
+                                  (char*)ws, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_select_groups(int32_t E, const int32_t* src, int32_t* dst, int32_t n, const int32_t* sel,
+                           void* ws, size_t ws_bytes, ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(E >= 0 && n >= 0 && (E == 0 || (src && dst)) && (n == 0 || sel), CKRL_ERR_INVALID_ARGUMENT,
+               "bad group selection");
+  if ((st = check_ws(ws, ws_bytes, E, 1))) return st;
+  CKRL_CUDA(launch_select_groups(E, src, dst, n, sel, (char*)ws, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
 int32_t ckrl_grpo_group_advantage(int32_t G, const int32_t* off, const double* R, double eps,
                                   double* adv, int32_t* status, ckrl_stream_t stream) {
   CKRL_REQUIRE(G >= 0 && (G == 0 || (off && R && adv)), CKRL_ERR_INVALID_ARGUMENT, "bad group arguments");

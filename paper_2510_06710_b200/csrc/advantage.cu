@@ -468,3 +468,145 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
 }
 
 }  // namespace ckrl
+
+namespace ckrl {
+
+// ---------------------------------------------------------------------------------
+// Minibatch selection. optim::ppo_loss takes record_indices (losses.hpp:54-56) and
+// normalises by the minibatch's own unit counts (losses.cpp:75-87); update_ppo draws
+// those minibatches (update.cpp:83-99). The selected records are gathered into a compact
+// [n][1] layout (16-byte copies for the logits rows) and each CTA contributes its
+// subset partials to the rank's StatsRecord, so a following loss launch on the compact
+// view sees exactly the minibatch's n_adv / n_val / n_pos.
+// ---------------------------------------------------------------------------------
+struct SelectArgs {
+  ckrl_rollout src, dst;
+  ckrl_ppo_batch sb, db;
+  ckrl_policy_outputs sp, dp;
+  int action_level, value_action;
+  int64_t n;
+  const int64_t* idx;
+  char* ws;
+  WsLayout L;
+};
+
+__device__ void copy_bytes(void* dst, const void* src, int64_t bytes) {
+  if (((uintptr_t)dst | (uintptr_t)src | (uintptr_t)bytes) % 16 == 0) {
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) d[i] = __ldg(s + i);
+  } else {
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(src);
+    uint16_t* d = reinterpret_cast<uint16_t*>(dst);
+    for (int64_t i = threadIdx.x; i < bytes / 2; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+__global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
+  const int C = a.src.chunk_len, M = a.src.tokens_per_action, V = a.src.vocab;
+  const int tb = a.src.token_dtype == CKRL_DTYPE_I32 ? 4 : 1;
+  const int lb = a.sp.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4;
+  const int U = a.action_level ? C : 1;
+  const int NV = a.value_action ? C : 1;
+  AsmPartial mine{0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+    const int64_t r = a.idx[i];
+    const int64_t P = (int64_t)C * M;
+    copy_bytes((char*)a.dp.logits + i * P * V * lb, (const char*)a.sp.logits + r * P * V * lb, P * V * lb);
+    const int t = threadIdx.x;
+    for (int k = t; k < P; k += blockDim.x) {
+      if (a.src.tokens) {
+        if (tb == 4)
+          ((int32_t*)a.dst.tokens)[i * P + k] = ((const int32_t*)a.src.tokens)[r * P + k];
+        else
+          ((uint8_t*)a.dst.tokens)[i * P + k] = ((const uint8_t*)a.src.tokens)[r * P + k];
+      }
+      if (a.src.old_logprob) ((float*)a.dst.old_logprob)[i * P + k] = a.src.old_logprob[r * P + k];
+    }
+    for (int j = t; j < C; j += blockDim.x) {
+      ((float*)a.dst.reward)[i * C + j] = a.src.reward[r * C + j];
+      ((uint8_t*)a.dst.flags)[i * C + j] = a.src.flags[r * C + j];
+      ((int32_t*)a.dst.episode_id)[i * C + j] = a.src.episode_id[r * C + j];
+      if (a.src.value_vector) ((float*)a.dst.value_vector)[i * C + j] = a.src.value_vector[r * C + j];
+      if (a.src.bootstrap) ((float*)a.dst.bootstrap)[i * C + j] = a.src.bootstrap[r * C + j];
+      a.db.counted[i * C + j] = a.sb.counted[r * C + j];
+    }
+    for (int u = t; u < U; u += blockDim.x) {
+      a.db.advantages[i * U + u] = a.sb.advantages[r * U + u];
+      a.db.returns[i * U + u] = a.sb.returns[r * U + u];
+    }
+    if (a.sp.values)
+      for (int u = t; u < NV; u += blockDim.x) ((float*)a.dp.values)[i * NV + u] = a.sp.values[r * NV + u];
+    if (t == 0) {
+      if (a.src.value_scalar) ((float*)a.dst.value_scalar)[i] = a.src.value_scalar[r];
+      int cnt = 0;
+      for (int j = 0; j < C; ++j) cnt += a.sb.counted[r * C + j] ? 1 : 0;
+      mine.n_pos += cnt;
+      if (a.action_level) {
+        for (int j = 0; j < C; ++j)
+          if (a.sb.counted[r * C + j]) {
+            const double x = a.sb.advantages[r * C + j];
+            mine.n += 1.0;
+            mine.s1 += x;
+            mine.s2 += x * x;
+          }
+      } else if (cnt) {
+        const double x = a.sb.advantages[r];
+        mine.n += 1.0;
+        mine.s1 += x;
+        mine.s2 += x * x;
+      }
+    }
+    __syncthreads();
+  }
+  // thread 0 holds the CTA's partial; finish_asm_stats reads it from thread 0
+  finish_asm_stats(mine, a.ws, a.L, M);
+}
+
+cudaError_t launch_select_records(const ckrl_rollout& src, const ckrl_ppo_batch& sb, const ckrl_policy_outputs& sp,
+                                  int action_level, int value_action, int64_t n, const int64_t* idx,
+                                  const ckrl_rollout& dst, const ckrl_ppo_batch& db,
+                                  const ckrl_policy_outputs& dp, char* ws, cudaStream_t s) {
+  SelectArgs a;
+  a.src = src;
+  a.dst = dst;
+  a.sb = sb;
+  a.db = db;
+  a.sp = sp;
+  a.dp = dp;
+  a.action_level = action_level;
+  a.value_action = value_action;
+  a.n = n;
+  a.idx = idx;
+  a.ws = ws;
+  a.L = ws_layout((int)n, 1);
+  cudaMemsetAsync(ws + a.L.tickets, 0, sizeof(uint32_t), s);
+  const int grid = (int)(n < 1 ? 1 : (n < kMaxLossCtas ? n : kMaxLossCtas));
+  select_records_kernel<<<grid, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// group_indices of optim::grpo_loss (losses.hpp:63-65): envs of unselected groups leave the
+// batch (env_group = -1) and the normaliser 1/#groups counts the selected ones
+// (losses.cpp:240-245).
+__global__ void select_groups_kernel(int E, const int32_t* src_group, int32_t* dst_group, int n,
+                                     const int32_t* sel, char* ws, WsLayout L) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int g = src_group[e];
+    int out = -1;
+    for (int q = 0; q < n && g >= 0; ++q)
+      if (sel[q] == g) out = g;
+    dst_group[e] = out;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    reinterpret_cast<StatsRecord*>(ws + L.stats_local)->groups_retained = n;
+}
+
+cudaError_t launch_select_groups(int E, const int32_t* src_group, int32_t* dst_group, int n, const int32_t* sel,
+                                 char* ws, cudaStream_t s) {
+  select_groups_kernel<<<(E + 255) / 256 < 1 ? 1 : (E + 255) / 256, 256, 0, s>>>(E, src_group, dst_group, n, sel,
+                                                                                  ws, ws_layout(E, 1));
+  return cudaGetLastError();
+}
+
+}  // namespace ckrl

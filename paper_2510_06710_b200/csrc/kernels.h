@@ -72,6 +72,12 @@ cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t read_timeline(uint64_t* out, int n);
 size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp);
+cudaError_t launch_select_records(const ckrl_rollout& src, const ckrl_ppo_batch& sb, const ckrl_policy_outputs& sp,
+                                  int action_level, int value_action, int64_t n, const int64_t* idx,
+                                  const ckrl_rollout& dst, const ckrl_ppo_batch& db,
+                                  const ckrl_policy_outputs& dp, char* ws, cudaStream_t s);
+cudaError_t launch_select_groups(int E, const int32_t* src_group, int32_t* dst_group, int n, const int32_t* sel,
+                                 char* ws, cudaStream_t s);
 cudaError_t launch_group_advantage(int G, const int32_t* off, const double* R, double eps, double* adv,
                                    int32_t* status, cudaStream_t s);
 cudaError_t launch_success_filter(int G, const int32_t* off, const double* R, double lower, double upper,

@@ -59,6 +59,69 @@ def grpo_loss(rollout: RolloutBuffer, policy: PolicyOutputs, batch: GrpoBatch,
     return diag
 
 
+def ppo_loss_minibatch(rollout: RolloutBuffer, policy: PolicyOutputs, batch: PpoBatch,
+                       record_indices, params: PpoParams = PpoParams(), stream=None) -> dict:
+    """ppo_loss (losses.cpp:62-232) over `record_indices` (record = env * Tc + chunk), the
+    minibatch form update_ppo drives (update.cpp:83-99). Like the reference, the batch's
+    advantages are used as they are: whiten them once beforehand with
+    normalize_advantages (update.cpp:66-67). Returns the host diagnostics."""
+    E, Tc, Cn, M = rollout.shape
+    dev = rollout.tokens.device
+    idx = torch.as_tensor(record_indices, dtype=torch.int64).to(dev).contiguous()
+    n = idx.numel()
+    V = rollout.vocab
+    spec = batch.spec
+    ulen = Cn if spec.advantage_level == Level.Action else 1
+    vlen = Cn if spec.value_level == Level.Action else 1
+    f32 = dict(dtype=torch.float32, device=dev)
+    sub = RolloutBuffer(tokens=torch.empty((n, 1, Cn, M), dtype=rollout.tokens.dtype, device=dev),
+                        old_logprob=torch.empty((n, 1, Cn, M), **f32),
+                        reward=torch.empty((n, 1, Cn), **f32),
+                        flags=torch.empty((n, 1, Cn), dtype=torch.uint8, device=dev),
+                        episode_id=torch.empty((n, 1, Cn), dtype=torch.int32, device=dev),
+                        value_scalar=torch.empty((n, 1), **f32),
+                        value_vector=torch.empty((n, 1, Cn), **f32),
+                        bootstrap=torch.empty((n, 1, Cn), **f32), vocab=V)
+    ws = Workspace(n, 1, dev)
+    sb = PpoBatch(spec=spec, counted=torch.empty((n, 1, Cn), dtype=torch.uint8, device=dev),
+                  advantages=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), **f32),
+                  returns=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), **f32), workspace=ws)
+    sp = PolicyOutputs(torch.empty((n, 1, Cn, M, V), dtype=policy.logits.dtype, device=dev),
+                       torch.empty((n, 1, vlen) if vlen > 1 else (n, 1), **f32)
+                       if policy.values is not None else None)
+    _lib.check(_lib.lib().ckrl_select_records(
+        C.byref(rollout.c()), C.byref(batch.c()), C.byref(policy.c()), C.byref(spec.c()), n,
+        C.c_void_p(idx.data_ptr()), C.byref(sub.c()), C.byref(sb.c()), C.byref(sp.c()), ws.ptr,
+        ws.bytes, stream_ptr(stream)))
+    p = PpoParams(params.clip_eps, params.value_loss_coef, params.entropy_coef, False)
+    return read_diagnostics(ppo_loss(sub, sp, sb, p, stream=stream), stream)
+
+
+def grpo_loss_minibatch(rollout: RolloutBuffer, policy: PolicyOutputs, batch: GrpoBatch,
+                        group_indices, params: GrpoParams = GrpoParams(), stream=None) -> dict:
+    """grpo_loss (losses.cpp:234-331) over `group_indices` (retained-group ordinals in
+    GroupKey order), the minibatch form of update_grpo (update.cpp:123-160). Raises
+    SkipUpdate on an empty selection like the reference."""
+    from .errors import SkipUpdate
+    dev = rollout.tokens.device
+    sel = torch.as_tensor(group_indices, dtype=torch.int32).to(dev).contiguous()
+    if sel.numel() == 0:
+        raise SkipUpdate("grpo_loss: no groups selected")
+    ws = Workspace(batch.workspace.num_envs, 1, dev)
+    ws.tensor.copy_(batch.workspace.tensor)
+    env_group = torch.empty_like(batch.env_group)
+    E = batch.env_group.numel()
+    _lib.check(_lib.lib().ckrl_select_groups(E, C.c_void_p(batch.env_group.data_ptr()),
+                                             C.c_void_p(env_group.data_ptr()), sel.numel(),
+                                             C.c_void_p(sel.data_ptr()), ws.ptr, ws.bytes,
+                                             stream_ptr(stream)))
+    sub = GrpoBatch(spec=batch.spec, env_group=env_group, env_member=batch.env_member,
+                    env_episode=batch.env_episode, env_advantage=batch.env_advantage,
+                    env_group_size=batch.env_group_size, slot_weight=batch.slot_weight,
+                    slot_member=batch.slot_member, group_counts=batch.group_counts, workspace=ws)
+    return read_diagnostics(grpo_loss(rollout, policy, sub, params, stream=stream), stream)
+
+
 class PpoStep:
     """The measured hot path: assemble_ppo_batch -> [NCCL stats all-gather] -> fused loss.
     Buffers are allocated once; __call__ only launches kernels (2 per step on 1 GPU)."""
