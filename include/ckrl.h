@@ -262,9 +262,19 @@ int32_t ckrl_select_records(const ckrl_rollout* src, const ckrl_ppo_batch* src_b
                             int64_t n, const int64_t* record_index, const ckrl_rollout* dst,
                             const ckrl_ppo_batch* dst_batch, const ckrl_policy_outputs* dst_policy,
                             void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
+/* (src_policy->logits / ->values may be NULL when the dst buffers are already filled, e.g.
+ * by a caller that evaluated its policy only on the selected records.) */
 int32_t ckrl_select_groups(int32_t num_envs, const int32_t* src_env_group, int32_t* dst_env_group,
                            int32_t n, const int32_t* group_index, void* workspace,
                            size_t workspace_bytes, ckrl_stream_t stream);
+
+/* Reads the rank's 64-byte stats record from a workspace after an assembly (synchronises
+ * `stream`): {sum, sumsq} (f64), {n_units, n_adv, n_val, n_pos, groups_retained, status}
+ * (int64). Returns the device-detected status (e.g. DegenerateGroup from the GRPO assembly,
+ * assembler.cpp:247-252) as the call's status. */
+int32_t ckrl_read_stats(const void* workspace, size_t workspace_bytes, int32_t num_envs,
+                        double* sums_out /* [2] */, int64_t* counts_out /* [6] */,
+                        ckrl_stream_t stream);
 
 /* ---- (b) fused action-token kernel ---------------------------------------------------- */
 

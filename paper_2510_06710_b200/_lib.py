@@ -145,6 +145,7 @@ SIGNATURES = {
     "ckrl_select_records": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
                                         C.c_int64, vp, P(Rollout), P(PpoBatchC), P(PolicyOutputs), vp,
                                         C.c_size_t, vp]),
+    "ckrl_read_stats": (C.c_int32, [vp, C.c_size_t, C.c_int32, vp, vp, vp]),
     "ckrl_select_groups": (C.c_int32, [C.c_int32, vp, vp, C.c_int32, vp, vp, C.c_size_t, vp]),
     "ckrl_grpo_group_advantage": (C.c_int32, [C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
     "ckrl_success_rate_filter": (C.c_int32, [C.c_int32, vp, vp, C.c_double, C.c_double, vp, vp,

@@ -628,7 +628,7 @@ int32_t ckrl_select_records(const ckrl_rollout* src, const ckrl_ppo_batch* sb, c
   if ((st = check_device())) return st;
   if ((st = check_rollout(src, false))) return st;
   if ((st = check_rollout(dst, false))) return st;
-  CKRL_REQUIRE(sb && db && sp && dp && sp->logits && dp->logits && sb->counted && db->counted &&
+  CKRL_REQUIRE(sb && db && sp && dp && dp->logits && sb->counted && db->counted &&
                    sb->advantages && db->advantages && sb->returns && db->returns,
                CKRL_ERR_INVALID_ARGUMENT, "batches / policy outputs required");
   CKRL_REQUIRE(n >= 1 && n <= INT32_MAX && idx, CKRL_ERR_INVALID_ARGUMENT, "empty record selection");
@@ -641,6 +641,32 @@ int32_t ckrl_select_records(const ckrl_rollout* src, const ckrl_ppo_batch* sb, c
   CKRL_CUDA(launch_select_records(*src, *sb, *sp, spec->advantage_level == CKRL_LEVEL_ACTION,
                                   spec->value_level == CKRL_LEVEL_ACTION, n, idx, *dst, *db, *dp,
                                   (char*)ws, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_read_stats(const void* ws, size_t ws_bytes, int32_t E, double* sums, int64_t* counts,
+                        ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  if ((st = check_ws(const_cast<void*>(ws), ws_bytes, E, 1))) return st;
+  StatsRecord r;
+  CKRL_CUDA(cudaMemcpyAsync(&r, (const char*)ws + ws_layout(E, 1).stats_local, sizeof(r), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+  CKRL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (sums) {
+    sums[0] = r.sum;
+    sums[1] = r.sumsq;
+  }
+  if (counts) {
+    counts[0] = r.n_units;
+    counts[1] = r.n_adv;
+    counts[2] = r.n_val;
+    counts[3] = r.n_pos;
+    counts[4] = r.groups_retained;
+    counts[5] = r.status;
+  }
+  if (r.status == CKRL_ERR_DEGENERATE_GROUP) return fail((int32_t)r.status, "all trajectories in the group have equal return");
+  if (r.status) return fail((int32_t)r.status, "device-side error");
   return CKRL_OK;
 }
 

@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
   for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
     const int64_t r = a.idx[i];
     const int64_t P = (int64_t)C * M;
-    copy_bytes((char*)a.dp.logits + i * P * V * lb, (const char*)a.sp.logits + r * P * V * lb, P * V * lb);
+    if (a.sp.logits)
+      copy_bytes((char*)a.dp.logits + i * P * V * lb, (const char*)a.sp.logits + r * P * V * lb, P * V * lb);
     const int t = threadIdx.x;
     for (int k = t; k < P; k += blockDim.x) {
       if (a.src.tokens) {
