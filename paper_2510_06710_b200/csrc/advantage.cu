@@ -17,7 +17,7 @@ namespace ckrl {
 // (fixed order: thread t sums partials t, t+nthr, ...; then a fixed tree).
 __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, int M) {
   __shared__ bool is_last;
-  __shared__ AsmPartial wpart[kAsmWarpsPerCta];
+  __shared__ AsmPartial wpart[32];  // any block size up to 1024
   AsmPartial* parts = reinterpret_cast<AsmPartial*>(ws + L.asm_partials);
   uint32_t* tickets = reinterpret_cast<uint32_t*>(ws + L.tickets);
   if (threadIdx.x == 0) {
@@ -72,11 +72,13 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
 // phases wait for completion. The serial schedule's CTAs are small enough to co-reside
 // with the loss kernel's CTAs.
 template <bool SERIAL>
-__global__ void __launch_bounds__(128, 6)  // <= 85 regs: co-resides with a loss CTA
+// 2 warps per CTA (<= 80 regs): a CTA co-resides with a loss CTA (19 warps x 96 regs), so
+// the loss kernel's persistent CTAs all start at once under programmatic dependent launch.
+__global__ void __launch_bounds__(32 * kAsmWarpsPerCta, 12)
 ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lambda,
                     uint8_t* counted, float* adv, float* ret, char* ws, WsLayout L) {
   asm volatile("griddepcontrol.launch_dependents;");
-  __shared__ GaeSums wsum[4];
+  __shared__ GaeSums wsum[kAsmWarpsPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
   GaeSums g{0.0, 0.0, 0.0, 0.0};
@@ -92,7 +94,7 @@ ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lamb
       g.counted_slots += __shfl_down_sync(0xffffffffu, g.counted_slots, off);
     }
   } else {
-    const int e = blockIdx.x * 4 + warp;
+    const int e = blockIdx.x * kAsmWarpsPerCta + warp;
     if (e < ro.num_envs)
       g = action_level ? env_gae(ActionAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda)
                        : env_gae(ChunkAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda);
@@ -101,7 +103,7 @@ ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lamb
   __syncthreads();
   AsmPartial p{0.0, 0.0, 0.0, 0.0};
   if (threadIdx.x == 0)
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < kAsmWarpsPerCta; ++w) {
       p.n += wsum[w].n;
       p.s1 += wsum[w].s1;
       p.s2 += wsum[w].s2;
@@ -420,12 +422,13 @@ cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double
                                 cudaStream_t s, int /*reserved_sms*/) {
   const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
   if (serial_gae_enabled() && n_items <= kSerialItems) {
-    const int grid = (ro.num_envs + 127) / 128;
-    ppo_assemble_kernel<true><<<grid > 0 ? grid : 1, 128, 0, s>>>(
+    const int nt = 32 * kAsmWarpsPerCta;
+    const int grid = (ro.num_envs + nt - 1) / nt;
+    ppo_assemble_kernel<true><<<grid > 0 ? grid : 1, nt, 0, s>>>(
         ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
   } else {
-    const int grid = (ro.num_envs + 3) / 4;
-    ppo_assemble_kernel<false><<<grid > 0 ? grid : 1, 128, 0, s>>>(
+    const int grid = (ro.num_envs + kAsmWarpsPerCta - 1) / kAsmWarpsPerCta;
+    ppo_assemble_kernel<false><<<grid > 0 ? grid : 1, 32 * kAsmWarpsPerCta, 0, s>>>(
         ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
   }
   return cudaGetLastError();

@@ -12,7 +12,7 @@ namespace ckrl {
 constexpr int kWarp = 32;
 constexpr int kMaxRanks = 64;
 constexpr int kLossThreads = 256;     // 8 warps per CTA in the tile kernel
-constexpr int kAsmWarpsPerCta = 4;    // one warp per env in the assembly kernel
+constexpr int kAsmWarpsPerCta = 2;    // one warp per env in the assembly kernel
 constexpr int kMaxLossCtas = 148 * 8; // persistent grid upper bound (partials slots)
 constexpr int kGrpoMaxEligible = 8192;
 

@@ -54,6 +54,8 @@ struct LossArgs {
   // kernel starts (programmatic dependent launch)
   int pdl;
   int reserved_sms;
+  int nbuf;      // TMA kernel: row-partial buffers (multiple of 4, <= kMaxRowBufs)
+  int rows_cap;  // TMA kernel: rows per buffer (rec_per_tile * C * M)
 };
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,

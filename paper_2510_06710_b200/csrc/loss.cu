@@ -857,7 +857,8 @@ __device__ __forceinline__ double log_f32_exact_exp(float s) {
   return (double)e * kLN2 + (double)logf(mant);
 }
 
-constexpr int kRowBufs = 4;     // row-partial + metadata buffers (row warps <-> unit warps)
+constexpr int kRowBufs = 4;        // buffer warps; row buffers come in multiples of this
+constexpr int kMaxRowBufs = 32;    // row-partial + metadata buffers (row warps <-> unit warps)
 constexpr int kTileRowsMax = 128;  // rows (tokens) per tile
 
 // Per-tile small inputs staged in shared memory by the metadata warp, so consumer warps
@@ -876,25 +877,26 @@ struct MetaSmem {
   uint8_t* act;   // per slot: bit1 unit active (counted / trajectory slot with weight)
   uint8_t* need;  // per slot: the row phase evaluates this slot's rows
 };
-__host__ __device__ constexpr size_t meta_bytes() {
-  return (size_t)kTileRowsMax * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1 + 1);
+__host__ __device__ constexpr size_t meta_bytes(int cap) {
+  return (size_t)cap * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1 + 1);
 }
-__device__ __forceinline__ MetaSmem carve_meta(unsigned char* p) {
+__device__ __forceinline__ MetaSmem carve_meta(unsigned char* p, int cap) {
   MetaSmem m;
   m.eadv = reinterpret_cast<double*>(p);
-  m.tok = reinterpret_cast<int32_t*>(m.eadv + kTileRowsMax);
-  m.old = reinterpret_cast<float*>(m.tok + kTileRowsMax);
-  m.w = m.old + kTileRowsMax;
-  m.adv = m.w + kTileRowsMax;
-  m.ret = m.adv + kTileRowsMax;
-  m.nv = m.ret + kTileRowsMax;
-  m.esz = reinterpret_cast<int32_t*>(m.nv + kTileRowsMax);
-  m.act = reinterpret_cast<uint8_t*>(m.esz + kTileRowsMax);
-  m.need = m.act + kTileRowsMax;
+  m.tok = reinterpret_cast<int32_t*>(m.eadv + cap);
+  m.old = reinterpret_cast<float*>(m.tok + cap);
+  m.w = m.old + cap;
+  m.adv = m.w + cap;
+  m.ret = m.adv + cap;
+  m.nv = m.ret + cap;
+  m.esz = reinterpret_cast<int32_t*>(m.nv + cap);
+  m.act = reinterpret_cast<uint8_t*>(m.esz + cap);
+  m.need = m.act + cap;
   return m;
 }
-__host__ __device__ constexpr size_t rowbuf_bytes() {
-  return rowsmem_bytes(kTileRowsMax) + meta_bytes();
+// One row buffer: per-row partials + the tile's metadata, for `cap` rows (cap % 8 == 0).
+__host__ __device__ constexpr size_t rowbuf_bytes(int cap) {
+  return rowsmem_bytes(cap) + meta_bytes(cap);
 }
 
 // Row metadata (what the row warps read): token ids and per-slot "evaluate" flags. In the
@@ -1191,11 +1193,12 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
 
 
 constexpr int kBufWarps = kRowBufs;  // buffer warp m owns row buffer m (tiles i = m mod 4)
-template <int ROWW>
-constexpr int tma_threads() { return 32 * (1 + ROWW + kBufWarps); }  // producer, row, buffer warps
+template <int ROWW, int BW = kBufWarps>
+constexpr int tma_threads() { return 32 * (1 + ROWW + BW); }  // producer, row, buffer warps
 
-__device__ __forceinline__ void bufwarps_sync() {  // named barrier over the 4 buffer warps
-  asm volatile("bar.sync 2, %0;" ::"n"(32 * kBufWarps) : "memory");
+template <int BW = kBufWarps>
+__device__ __forceinline__ void bufwarps_sync() {  // named barrier over the buffer warps
+  asm volatile("bar.sync 2, %0;" ::"n"(32 * BW) : "memory");
 }
 
 // Fused PPO step, phase A (buffer warps only): GAE + counted masks for this CTA's envs,
@@ -1292,23 +1295,25 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
 //                   barrier, while the producer and row warps already stream logits.
 // Synchronisation is mbarrier-only: full[s]/empty[s] (producer <-> row warps),
 // metafull[b] (buffer warp -> row warps), rowfull[b] (row warps -> buffer warp).
-template <int MODE, typename LT, int ROWW, int RIF, bool FUSED>
-__global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossArgs a, int nstage,
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW>
+__global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(LossArgs a, int nstage,
                                                                           uint32_t tile_bytes) {
-  constexpr int kThreads = tma_threads<ROWW>();
+  constexpr int kThreads = tma_threads<ROWW, BW>();
+  static_assert(!FUSED || BW == kBufWarps, "the fused step runs with 4 buffer warps");
   constexpr int kPasses = (kTileRowsMax + ROWW * 4 - 1) / (ROWW * 4);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ LossConsts s_k, s_kf;
   __shared__ double s_red[kThreads / 32][RAW_COUNT];
   __shared__ bool s_last;
-  __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4], metafull_bar[kRowBufs],
-      rowfull_bar[kRowBufs];
+  __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4], metafull_bar[kMaxRowBufs],
+      rowfull_bar[kMaxRowBufs];
 
   constexpr int V = 256;
   constexpr int kCW = ROWW;  // row warps
   const int M = a.M, P = a.C * M;
   unsigned char* stage_base = smem_raw;
   unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
+  const int nbuf = a.nbuf, cap = a.rows_cap;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
@@ -1317,7 +1322,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kCW);
     }
-    for (int b = 0; b < kRowBufs; ++b) {
+    for (int b = 0; b < a.nbuf; ++b) {
       mbar_init(&metafull_bar[b], 1);
       mbar_init(&rowfull_bar[b], kCW);
     }
@@ -1359,14 +1364,14 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
       const int s = it % nstage;
-      const int b = it % kRowBufs;
-      unsigned char* bb = buf_base + b * rowbuf_bytes();
-      const RowSmem sm = carve_rows(bb, kTileRowsMax);
-      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
+      const int b = it % nbuf;
+      unsigned char* bb = buf_base + b * rowbuf_bytes(cap);
+      const RowSmem sm = carve_rows(bb, cap);
+      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(cap), cap);
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
-      mbar_wait(&metafull_bar[b], (it / kRowBufs) & 1);  // buffer b holds tile it's row metadata
+      mbar_wait(&metafull_bar[b], (it / nbuf) & 1);  // buffer b holds tile it's row metadata
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(11 + 3 * it);
       mbar_wait(&full_bar[s], (it / nstage) & 1);
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
@@ -1418,46 +1423,60 @@ __global__ void __launch_bounds__(tma_threads<ROWW>(), 1) tma_tile_kernel(LossAr
     }
   } else {
     // ---------------- buffer warps ----------------
-    const int b = warp - 1 - kCW;
-    unsigned char* bb = buf_base + b * rowbuf_bytes();
-    const RowSmem sm = carve_rows(bb, kTileRowsMax);
-    const MetaSmem mt = carve_meta(bb + rowsmem_bytes(kTileRowsMax));
-    const int64_t stride = (int64_t)kBufWarps * gridDim.x;
-    int64_t tile = blockIdx.x + (int64_t)b * gridDim.x;
-    int it = b;
-    int64_t r0 = 0;
-    int nrec = 0;
-    if (tile < a.n_tiles) {  // rows of the first tile can start right away
-      nrec = tile_recs(tile, r0);
-      row_meta<MODE, FUSED>(a, r0, nrec, lane, mt, a.pdl != 0);
+    // Warp m owns tiles it = m, m+4, ... and their buffers it % nbuf; with nbuf > 4 the
+    // row warps run up to nbuf tiles ahead of the unit phases (e.g. while the overlapped
+    // step's assembly kernel is still running), and the backlog drains 4 tiles at a time.
+    const int m = warp - 1 - kCW;
+    const int64_t stride = (int64_t)BW * gridDim.x;
+    auto buf_of = [&](int itx, RowSmem& sm, MetaSmem& mt) {
+      unsigned char* bb = buf_base + (itx % nbuf) * rowbuf_bytes(cap);
+      sm = carve_rows(bb, cap);
+      mt = carve_meta(bb + rowsmem_bytes(cap), cap);
+    };
+    RowSmem sm;
+    MetaSmem mt;
+    // rows of the first nbuf tiles can start right away
+    for (int itx = m; itx < nbuf; itx += BW) {
+      const int64_t tl = blockIdx.x + (int64_t)itx * gridDim.x;
+      if (tl >= a.n_tiles) break;
+      int64_t rr0;
+      const int nr = tile_recs(tl, rr0);
+      buf_of(itx, sm, mt);
+      row_meta<MODE, FUSED>(a, rr0, nr, lane, mt, a.pdl != 0);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&metafull_bar[b]);
-      if (lane == 0 && b == 0) tl_mark(24);
+      if (lane == 0) mbar_arrive(&metafull_bar[itx]);
+      if (lane == 0 && itx == 0) tl_mark(24);
     }
     if (FUSED) {
-      fused_phase_a(a, b, lane, &s_kf);
+      fused_phase_a(a, m, lane, &s_kf);
     } else {
       // overlapped step: the assembly kernel's outputs (stats record, counted, advantages)
       // are consumed only from here on (no-op when not launched as a PDL dependent)
       if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (b == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
-      bufwarps_sync();
+      if (m == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
+      bufwarps_sync<BW>();
     }
     const LossConsts k = FUSED ? s_kf : s_k;
-    for (; tile < a.n_tiles; tile += stride, it += kBufWarps) {
+    int it = m;
+    for (int64_t tile = blockIdx.x + (int64_t)m * gridDim.x; tile < a.n_tiles; tile += stride, it += BW) {
+      int64_t r0;
+      const int nrec = tile_recs(tile, r0);
+      const int b = it % nbuf;
+      buf_of(it, sm, mt);
       UnitRegs ur;
       unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);  // in flight while rows finish
-      mbar_wait(&rowfull_bar[b], (it / kRowBufs) & 1);
-      if (lane == 0 && it == b) tl_mark(20 + b);
+      mbar_wait(&rowfull_bar[b], (it / nbuf) & 1);
+      if (lane == 0 && it == m) tl_mark(20 + m);
       unit_meta_store<MODE>(a, nrec, lane, ur, mt);
       __syncwarp();
       unit_phase_smem<MODE>(a, k, acc, sm, mt, r0, nrec, lane);
       __syncwarp();
-      if (lane == 0 && it == b) tl_mark(4 + b);  // first unit phase of each buffer warp
-      const int64_t ntile = tile + stride;
+      if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
+      const int64_t ntile = tile + (int64_t)nbuf * gridDim.x;  // next user of buffer b
       if (ntile < a.n_tiles) {
-        nrec = tile_recs(ntile, r0);
-        row_meta<MODE, FUSED>(a, r0, nrec, lane, mt, a.pdl != 0);
+        int64_t nr0;
+        const int nn = tile_recs(ntile, nr0);
+        row_meta<MODE, FUSED>(a, nr0, nn, lane, mt, a.pdl != 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
@@ -1512,7 +1531,17 @@ constexpr size_t kStageTarget = 56 * 1024;
 
 // TMA pipeline plan: whole records per tile (~56 KB), 2-4 stages. Returns false when a
 // single record does not fit twice (then the direct kernel runs).
-static bool tma_plan(const LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, uint32_t& tile_bytes) {
+static int max_row_bufs() {  // CKRL_NBUF caps the row-buffer count (A/B experiments)
+  static int n = -1;
+  if (n < 0) {
+    const char* env = getenv("CKRL_NBUF");
+    n = env ? atoi(env) : kMaxRowBufs;
+    if (n > kMaxRowBufs) n = kMaxRowBufs;
+  }
+  return n;
+}
+
+static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, uint32_t& tile_bytes) {
   const size_t rec = (size_t)a.C * a.M * 256 * dbytes;
   rec_per_tile = (int)(kStageTarget / rec);
   if (rec_per_tile < 1) rec_per_tile = 1;
@@ -1520,19 +1549,29 @@ static bool tma_plan(const LossArgs& a, int dbytes, int& rec_per_tile, int& nsta
   if (a.C * a.M > max_rows) return false;
   if (rec_per_tile * a.C * a.M > max_rows) rec_per_tile = max_rows / (a.C * a.M);
   tile_bytes = (uint32_t)(rec_per_tile * rec);
-  const size_t rows = (size_t)rec_per_tile * a.C * a.M;
-  const size_t fixed = kRowBufs * rowbuf_bytes() + 1024;
-  (void)rows;
-  nstage = fixed < kSmemBudget ? (int)((kSmemBudget - fixed) / tile_bytes) : 0;
-  if (nstage > 4) nstage = 4;
-  return nstage >= 2;
+  const int cap = (rec_per_tile * a.C * a.M + 7) & ~7;
+  const size_t buf = rowbuf_bytes(cap);
+  // up to 3 stages in flight, then as many row buffers (multiples of 4) as fit
+  for (nstage = 3; nstage >= 2; --nstage) {
+    const size_t used = (size_t)nstage * tile_bytes + 1024;
+    if (used >= kSmemBudget) continue;
+    int nb = (int)((kSmemBudget - used) / buf) & ~3;
+    if (nb > max_row_bufs()) nb = max_row_bufs();
+    if (nb >= kRowBufs) {
+      a.nbuf = nb;
+      a.rows_cap = cap;
+      return true;
+    }
+  }
+  return false;
 }
 
-template <int MODE, typename LT, int ROWW, int RIF, bool FUSED>
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW = kBufWarps>
 static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
-  auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED>;
+  auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED, BW>;
+  if (a.nbuf % BW) a.nbuf -= a.nbuf % BW;
   a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
-  const size_t smem = (size_t)nstage * tile_bytes + kRowBufs * rowbuf_bytes();
+  const size_t smem = (size_t)nstage * tile_bytes + (size_t)a.nbuf * rowbuf_bytes(a.rows_cap);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t grid = device_sms();
@@ -1542,7 +1581,7 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
   if (!FUSED && a.pdl) {  // programmatic dependent of the assembly kernel
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(tma_threads<ROWW>());
+    cfg.blockDim = dim3(tma_threads<ROWW, BW>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1553,13 +1592,13 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
     return cudaLaunchKernelEx(&cfg, kern, a, nstage, tile_bytes);
   }
   if (!FUSED) {
-    kern<<<(unsigned)grid, tma_threads<ROWW>(), smem, s>>>(a, nstage, tile_bytes);
+    kern<<<(unsigned)grid, tma_threads<ROWW, BW>(), smem, s>>>(a, nstage, tile_bytes);
     return cudaGetLastError();
   }
   // The fused step has a grid-wide barrier: co-residency of every CTA is required, so the
   // launch is cooperative (one CTA per SM by construction).
   void* args[] = {&a, &nstage, &tile_bytes};
-  return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(tma_threads<ROWW>()),
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(tma_threads<ROWW, BW>()),
                                      args, smem, s);
 }
 
@@ -1569,12 +1608,14 @@ template <int MODE, typename LT, bool FUSED>
 static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
   if (g_tma_variant < 0) {
     const char* env = getenv("CKRL_TMA_VARIANT");
-    g_tma_variant = env ? atoi(env) : 0;
+    g_tma_variant = env ? atoi(env) : 4;
   }
   switch (g_tma_variant) {
     // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
     case 3: return launch_tma_v<MODE, LT, 8, 2, FUSED>(a, s, grid_out, nstage, tile_bytes);
-    default: return launch_tma_v<MODE, LT, 16, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
+    case 0: return launch_tma_v<MODE, LT, 16, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
+    // default: 14 row warps (a 56-row tile is 14 x 4 rows) -> 19 warps, 96 registers, no spills
+    default: return launch_tma_v<MODE, LT, 14, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
   }
 }
 
