@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    p.add_argument("--grad", action="store_true",
+                   help="extend the step with the softmax-backward seam (ckrl_logits_grad -> dlogits)")
     return p.parse_args()
 
 
@@ -229,7 +231,8 @@ def workload(args, cfg, world):
             "action_dim": cfg.tokens_per_action, "bins": cfg.vocab,
             "granularity": {"advantage": lv[a], "logprob": lv[l], "value": lv[v]},
             "global_envs": cfg.num_envs * world, "parallelism": f"env-sharded x{world}",
-            "logits_dtype": args.dtype}
+            "logits_dtype": args.dtype,
+            **({"step_includes": "assemble + loss + logits_grad (dlogits)"} if getattr(args, "grad", False) else {})}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -296,13 +299,29 @@ def main():
     if cfg.algo == "ppo":
         step = optim.PpoStep(reps[0][0], GaeParams(0.99, 0.95), spec,
                              PpoParams(0.2, 0.5, 0.01, True), comm=comm)
-        run = lambda i: step(reps[i % R][0], reps[i % R][1])  # noqa: E731
+        run0 = lambda i: step(reps[i % R][0], reps[i % R][1])  # noqa: E731
         launches_per_step = 2
     else:
         opts = GrpoAssemblyOptions(spec)
         step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
-        run = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
+        run0 = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
         launches_per_step = 3
+    run = run0
+    if args.grad:  # + dlogits for the model backward (policy_net.cpp:431-456)
+        from paper_2510_06710_b200 import policy as ckpolicy
+        dlogits = torch.empty_like(reps[0][1].logits)
+        gstatus = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def grad(i):
+            ro, pol = reps[i % R][0], reps[i % R][1]
+            ckpolicy.logits_grad(pol.logits, ro.tokens, step.outputs.coeff_logprob,
+                                 step.outputs.coeff_entropy, out=dlogits, status=gstatus,
+                                 stream=torch.cuda.current_stream(), check=False)
+
+        def run(i):
+            run0(i)
+            grad(i)
+        launches_per_step += 1
     if world > 1:
         launches_per_step += 1  # finalize after the loss-scalar all-reduce
 
@@ -392,6 +411,25 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f).get(f"{args.config}_{args.dtype}")
 
+    grad_line = None
+    if args.grad:
+        gev = []
+        for i in range(min(K, 50)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            grad(i)
+            e1.record(stream)
+            gev.append((e0, e1))
+        torch.cuda.synchronize()
+        gms = sum(e0.elapsed_time(e1) for e0, e1 in gev) / len(gev)
+        rows = env_steps(cfg) * cfg.tokens_per_action
+        gbytes = rows * (2 * cfg.vocab * dbytes + 1 + 8)
+        gach = gbytes / (gms * 1e-3) / 1e9
+        grad_line = {"kernel": "logits_grad_256 (dlogits, softmax-backward seam)", "kernel_ms": gms,
+                     "algorithmic_bytes_per_launch": gbytes, "achieved": gach, "unit": "GB/s",
+                     "frac": gach / peaks()[0], "out_dtype": args.dtype,
+                     "status": int(gstatus.item())}
+
     # --- e2e through the public API with host (pinned) buffers
     e2e = None
     if not args.profile:
@@ -421,6 +459,7 @@ def main():
                      "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
                      "step_frac": (kbytes / (ms * 1e-3) / 1e9) / peak},
         "cpu_baseline": cpu,
+        **({"logits_grad": grad_line} if grad_line else {}),
         "e2e": e2e,
         "gpu_launches": K * launches_per_step,
         "clocks": clk.summary(),

@@ -287,6 +287,27 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t chunk_len, int32_t tokens_p
                          float* token_entropy, double* action_logprob, double* chunk_logprob,
                          ckrl_stream_t stream);
 
+/* ---- (f1) softmax-backward seam --------------------------------------------------------- */
+
+/* The per-position logits gradient PolicyNet::accumulate_chunk_gradient forms before its
+ * outer_add / trunk backward (policy/policy_net.cpp:431-456):
+ *   dlogits[k][v] = coeff_lp[k] * ([v == tok_k] - p_kv) + coeff_ent[k] * (-p_kv * (ls_kv + H_k)),
+ * ls = log_softmax(logits[k]), p = exp(ls), H_k = -sum_v p_kv ls_kv, for `rows` positions of
+ * `vocab` bins. coeff_lp / coeff_ent are the loss outputs (ckrl_loss_outputs; coeff_ent may be
+ * NULL = all zero). Positions with both coefficients zero are skipped by the reference; their
+ * row is written as zeros. A non-finite coefficient is the reference's NonFinite (:437-438):
+ * the row is zeroed and *status_device (optional, caller-zeroed int32) is set to
+ * CKRL_ERR_NON_FINITE; read it with ckrl_read_status. dlogits may alias logits when both
+ * dtypes match (in place). Asynchronous on `stream`. */
+int32_t ckrl_logits_grad(int64_t rows, int32_t vocab, int32_t logits_dtype, const void* logits,
+                         int32_t token_dtype, const void* tokens, const float* coeff_lp,
+                         const float* coeff_ent, int32_t out_dtype, void* dlogits,
+                         int32_t* status_device, ckrl_stream_t stream);
+
+/* Synchronises `stream`, reads a device status word written by an asynchronous entry point
+ * and returns it as the call's status (0 when clear). */
+int32_t ckrl_read_status(const int32_t* status_device, ckrl_stream_t stream);
+
 /* ---- (d) losses ----------------------------------------------------------------------- */
 
 /* ppo_loss (optim/losses.cpp:62-232) over every record (full batch), fused with the token

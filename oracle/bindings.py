@@ -54,7 +54,8 @@ class Oracle:
         self.lib = C.CDLL(path)
         for name in ("orc_compute_gae", "orc_assemble_ppo", "orc_normalize_advantages",
                      "orc_ppo_loss", "orc_grpo_group_advantage", "orc_success_rate_filter",
-                     "orc_assemble_grpo", "orc_grpo_loss", "orc_validate_granularity"):
+                     "orc_assemble_grpo", "orc_grpo_loss", "orc_validate_granularity",
+                     "orc_logits_grad"):
             getattr(self.lib, name).restype = C.c_int
 
     # --- rollout marshalling -------------------------------------------------
@@ -112,6 +113,17 @@ class Oracle:
         lp, ent = np.zeros(rows), np.zeros(rows)
         self.lib.orc_token_stats(C.c_int64(rows), V, _p(lg), _p(tk), _p(lp), _p(ent))
         return lp, ent
+
+    def logits_grad(self, logits, tokens, coeff_lp, coeff_ent):
+        """dlogits per position (policy/policy_net.cpp:431-456); returns (status, [rows][V])."""
+        lg = _c64(logits)
+        V = lg.shape[-1]
+        rows = lg.size // V
+        tk = np.ascontiguousarray(tokens, dtype=np.int32).reshape(-1)
+        kl, ke = _c64(np.reshape(coeff_lp, -1)), _c64(np.reshape(coeff_ent, -1))
+        out = np.zeros((rows, V))
+        st = self.lib.orc_logits_grad(C.c_int64(rows), V, _p(lg), _p(tk), _p(kl), _p(ke), _p(out))
+        return st, out
 
     def assemble_ppo(self, d, spec, gamma, lam):
         a, l, v = spec
@@ -239,6 +251,7 @@ def _ref_lib():
         lib = C.CDLL(REF_SO)
         lib.refx_create.restype = C.c_void_p
         lib.refx_last_error.restype = C.c_char_p
+        lib.refx_bpol_offset.restype = C.c_longlong
         for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo_subset",
                   "refx_grpo_subset", "refx_ppo", "refx_grpo",
                   "refx_replay_ppo_grad", "refx_replay_grpo_grad"):
@@ -344,6 +357,9 @@ class RefScenario:
                                        C.c_double(upper), int(length_normalized), min_group_size,
                                        C.c_double(clip), C.c_longlong(ix.size), _p(ix), _p(diag))
         return st, diag
+
+    def bpol_offset(self) -> int:
+        return int(self.lib.refx_bpol_offset(C.c_void_p(self.h)))
 
     def replay_ppo_grad(self, val_level, counted, coeff_lp, coeff_ent, coeff_val):
         g = np.zeros(self.n_params)

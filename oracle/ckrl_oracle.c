@@ -82,6 +82,39 @@ void orc_token_stats(int64_t rows, int V, const double* logits, const int32_t* t
   free(ls);
 }
 
+/* policy/policy_net.cpp:431-456 (accumulate_chunk_gradient, the per-position logits
+ * gradient before outer_add / the trunk backward): positions with klp == 0 && kent == 0
+ * are skipped (zero row here), non-finite coefficients throw NonFinite (:437-438). */
+int orc_logits_grad(int64_t rows, int V, const double* logits, const int32_t* tokens,
+                    const double* coeff_lp, const double* coeff_ent, double* dlogits) {
+  double* ls = (double*)malloc(sizeof(double) * (size_t)V);
+  int st = ST_OK;
+  for (int64_t k = 0; k < rows; ++k) {
+    double* d = dlogits + k * V;
+    const double klp = coeff_lp[k], kent = coeff_ent[k];
+    if (klp == 0.0 && kent == 0.0) {
+      for (int v = 0; v < V; ++v) d[v] = 0.0;
+      continue;
+    }
+    if (!isfinite(klp) || !isfinite(kent)) {
+      st = ST_NON_FINITE;
+      break;
+    }
+    orc_log_softmax(V, logits + k * V, ls);
+    double H = 0.0;
+    if (kent != 0.0)
+      for (int v = 0; v < V; ++v) H -= exp(ls[v]) * ls[v];
+    for (int v = 0; v < V; ++v) {
+      double pv = exp(ls[v]);
+      double dv = klp * ((v == tokens[k] ? 1.0 : 0.0) - pv);
+      if (kent != 0.0) dv += kent * (-pv * (ls[v] + H));
+      d[v] = dv;
+    }
+  }
+  free(ls);
+  return st;
+}
+
 /* ---------------------------------------------------------------- PPO assembly */
 
 typedef struct {

@@ -200,6 +200,15 @@ void* refx_create(const refx_cfg* cfg, int* status) {
 
 void refx_destroy(void* h) { delete static_cast<Scenario*>(h); }
 
+// Offset of the policy-head bias b_pol in the flat parameter vector (policy_net.cpp:107-152
+// order: w_in, b_in, pos_bias, emb, trunk, w_pol, b_pol, ...). Its gradient slice is the sum
+// over evaluated positions of the per-position logits gradient (outer_add, :451-452).
+long long refx_bpol_offset(void* h) {
+  const policy::PolicyDescriptor& d = static_cast<Scenario*>(h)->current.descriptor();
+  const long long H = d.hidden, D = d.obs_dim, L = d.trunk_layers, V = d.vocab, P = d.positions();
+  return H * D + H + P * H + P * V * H + L * (H * H + H) + V * H;
+}
+
 void refx_dims(void* h, long long* dims) {
   auto* s = static_cast<Scenario*>(h);
   dims[0] = s->E;

@@ -141,6 +141,9 @@ SIGNATURES = {
                                    P(GrpoOptions), P(GrpoParams), P(GrpoBatchC),
                                    P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
     "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
+    "ckrl_logits_grad": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp,
+                                     C.c_int32, vp, vp, vp]),
+    "ckrl_read_status": (C.c_int32, [vp, vp]),
     "ckrl_debug_timeline": (C.c_int32, [vp, C.c_int32]),
     "ckrl_select_records": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
                                         C.c_int64, vp, P(Rollout), P(PpoBatchC), P(PolicyOutputs), vp,

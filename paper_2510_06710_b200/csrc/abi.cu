@@ -354,6 +354,41 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, in
   return CKRL_OK;
 }
 
+int32_t ckrl_logits_grad(int64_t rows, int32_t V, int32_t logits_dtype, const void* logits,
+                         int32_t token_dtype, const void* tokens, const float* coeff_lp,
+                         const float* coeff_ent, int32_t out_dtype, void* dlogits,
+                         int32_t* status_device, ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(rows >= 0 && V >= 1, CKRL_ERR_LENGTH_MISMATCH, "bad logits_grad dimensions");
+  if (rows == 0) return CKRL_OK;
+  CKRL_REQUIRE(logits && tokens && coeff_lp && dlogits, CKRL_ERR_INVALID_ARGUMENT,
+               "logits / tokens / coeff_lp / dlogits required");
+  CKRL_REQUIRE((logits_dtype == CKRL_DTYPE_F32 || logits_dtype == CKRL_DTYPE_BF16) &&
+                   (out_dtype == CKRL_DTYPE_F32 || out_dtype == CKRL_DTYPE_BF16) &&
+                   (token_dtype == CKRL_DTYPE_U8 || token_dtype == CKRL_DTYPE_I32),
+               CKRL_ERR_INVALID_ARGUMENT, "unsupported dtype");
+  CKRL_REQUIRE(token_dtype == CKRL_DTYPE_I32 || V <= 256, CKRL_ERR_INVALID_ARGUMENT,
+               "u8 tokens need vocab <= 256");
+  CKRL_REQUIRE(dlogits != logits || out_dtype == logits_dtype, CKRL_ERR_INVALID_ARGUMENT,
+               "in-place logits_grad needs matching dtypes");
+  CKRL_CUDA(launch_logits_grad(logits, logits_dtype == CKRL_DTYPE_BF16, tokens, token_dtype == CKRL_DTYPE_I32,
+                               coeff_lp, coeff_ent, rows, V, dlogits, out_dtype == CKRL_DTYPE_BF16,
+                               status_device, (cudaStream_t)stream));
+  return CKRL_OK;
+}
+
+int32_t ckrl_read_status(const int32_t* status_device, ckrl_stream_t stream) {
+  CKRL_REQUIRE(status_device, CKRL_ERR_INVALID_ARGUMENT, "null status");
+  int32_t host = 0;
+  CKRL_CUDA(cudaMemcpyAsync(&host, status_device, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+  CKRL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (host == CKRL_ERR_NON_FINITE) return fail(host, "non-finite gradient coefficient");
+  if (host) return fail(host, "device-side error");
+  return CKRL_OK;
+}
+
 static bool fused_enabled() {
   static int on = -1;
   if (on < 0) {

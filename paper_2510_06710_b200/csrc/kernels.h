@@ -70,6 +70,9 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t launch_logits_grad(const void* logits, int logits_bf16, const void* tokens, int tok_i32,
+                               const float* coeff_lp, const float* coeff_ent, int64_t rows, int V,
+                               void* out, int out_bf16, int32_t* status, cudaStream_t s);
 cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t read_timeline(uint64_t* out, int n);

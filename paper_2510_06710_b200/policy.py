@@ -1,6 +1,7 @@
 """The fused action-token kernel as a standalone operator: PolicyNet::evaluate_chunk
 (policy/policy_net.cpp:333-357) + aggregate_logprob (core/granularity.cpp:83-113) over
-current-policy logits rows."""
+current-policy logits rows; and the softmax-backward seam, the per-position logits gradient of
+PolicyNet::accumulate_chunk_gradient (policy/policy_net.cpp:431-456)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -31,3 +32,31 @@ def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, stream=None):
                                            _ptr(tokens), _ptr(lp), _ptr(ent), _ptr(act), _ptr(chk),
                                            stream_ptr(stream)))
     return {"token_logprob": lp, "token_entropy": ent, "action_logprob": act, "chunk_logprob": chk}
+
+
+def logits_grad(logits: torch.Tensor, tokens: torch.Tensor, coeff_logprob: torch.Tensor,
+                coeff_entropy=None, out=None, out_dtype=None, status=None, stream=None,
+                check: bool = True) -> torch.Tensor:
+    """dlogits[..., v] = coeff_lp * ([v == tok] - p_v) + coeff_ent * (-p_v * (ls_v + H)) per
+    position (policy/policy_net.cpp:431-456). logits [..., V] (f32/bf16), tokens / coefficients
+    [...] (the loss outputs). `out` may be `logits` itself (in place). With check=True the call
+    synchronises and raises NonFinite like the reference (:437-438); otherwise pass a zeroed
+    int32 `status` tensor and read it later with `_lib.read_status`."""
+    V = logits.shape[-1]
+    rows = logits.numel() // V
+    if out is None:
+        out = torch.empty(logits.shape, dtype=out_dtype or logits.dtype, device=logits.device)
+    ld = _lib.DTYPE_BF16 if logits.dtype == torch.bfloat16 else _lib.DTYPE_F32
+    od = _lib.DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.DTYPE_F32
+    td = _lib.DTYPE_U8 if tokens.dtype == torch.uint8 else _lib.DTYPE_I32
+    tokens = tokens.contiguous() if tokens.dtype in (torch.uint8, torch.int32) else tokens.to(torch.int32).contiguous()
+    klp = coeff_logprob.contiguous().float()
+    kent = coeff_entropy.contiguous().float() if coeff_entropy is not None else None
+    if status is None and check:
+        status = torch.zeros(1, dtype=torch.int32, device=logits.device)
+    _lib.check(_lib.lib().ckrl_logits_grad(rows, V, ld, _ptr(logits.contiguous()), td, _ptr(tokens),
+                                           _ptr(klp), _ptr(kent), od, _ptr(out), _ptr(status),
+                                           stream_ptr(stream)))
+    if check:
+        _lib.check(_lib.lib().ckrl_read_status(_ptr(status), stream_ptr(stream)))
+    return out

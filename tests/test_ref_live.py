@@ -37,6 +37,15 @@ def test_ppo_bitexact_and_gradient_replay(oracle, mode, seed):
         np.testing.assert_array_equal(diag, r["diag"])
         g = sc.replay_ppo_grad(spec[2], counted, clp, cent, cval)
         np.testing.assert_array_equal(g, r["grad"])
+        # logits-gradient seam (row f1): the oracle's per-position dlogits, summed in the
+        # reference's record / position order, are the b_pol slice of grad_out bit-for-bit
+        st, dl = oracle.logits_grad(d["logits"], d["tokens"], clp, cent)
+        assert st == 0
+        bsum = np.zeros(sc.V)
+        for row in dl:
+            bsum += row
+        o = sc.bpol_offset()
+        np.testing.assert_array_equal(bsum, g[o:o + sc.V])
 
 
 @pytest.mark.parametrize("seed", [3, 4])
@@ -56,7 +65,14 @@ def test_grpo_bitexact_and_gradient_replay(oracle, seed, ln):
         assert st == r["status"]
         if st == 0:
             np.testing.assert_array_equal(diag, r["diag"])
-            np.testing.assert_array_equal(sc.replay_grpo_grad(spec, coeff, length_normalized=ln), r["grad"])
+            g = sc.replay_grpo_grad(spec, coeff, length_normalized=ln)
+            np.testing.assert_array_equal(g, r["grad"])
+            # logits-gradient seam: entropy-free coefficients; the replay walks groups, not
+            # records, so the b_pol sums agree to rounding
+            st, dl = oracle.logits_grad(d["logits"], d["tokens"], coeff, np.zeros_like(coeff))
+            assert st == 0
+            o = sc.bpol_offset()
+            np.testing.assert_allclose(dl.sum(axis=0), g[o:o + sc.V], rtol=1e-12, atol=1e-15)
 
 
 def test_reference_rejects_what_the_abi_rejects():
