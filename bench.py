@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "adam"])
+    p.add_argument("--adam-params", type=int, default=1 << 28, help="adam: parameters per GPU")
     p.add_argument("--stages", default="1,2,4", help="cfg5: pipeline depths k to time")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-graph", action="store_true")
@@ -249,6 +250,9 @@ def main():
         return
     if args.config == "cfg5":
         bench_pipeline(args, rank, world, local)
+        return
+    if args.config == "adam":
+        bench_adam(args, rank, world, local)
         return
 
     import numpy as np
@@ -470,6 +474,51 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- row f4: Adam
+def bench_adam(args, rank, world, local):
+    """Adam::step with global-norm clipping (ckrl_adam_step) on f32 state: the norm pass reads
+    g, the update reads p, g, m, v and writes p, g (clipping active), m, v -> 36 B / param.
+    Inputs (4 x 1 GiB at the default 2^28 params) exceed L2 by 32x."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2510_06710_b200 as ck
+    from paper_2510_06710_b200 import optim
+    ck.lib()
+    n = args.adam_params
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    params = torch.randn(n, device=dev, generator=g)
+    grad = torch.randn(n, device=dev, generator=g)
+    adam = optim.Adam(n, 1e-4, max_grad_norm=1.0, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        adam.step_async(params, grad)
+    torch.cuda.synchronize()
+    K = max(1, min(args.steps, 50))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(K):
+            adam.step_async(params, grad)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    nbytes = 36 * n
+    peak, peak_kind = peaks()
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": "Adam step (row f4): parameters/s", "value": world * n / (ms * 1e-3), "unit": "params/s",
+        "n_gpus": world, "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"adam: {n} f32 params per GPU, clip active",
+                                         "l2": "16 GiB of state per step > 126 MB L2"},
+        "roofline": {"bound": "hbm", "achieved": nbytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": nbytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_launch": nbytes,
+                     "peak_kind": peak_kind, "kernel": "adam_norm + adam_update"},
+        "gpu_launches": 2 * K, "clocks": clk.summary(), "last_norm": float(adam.norm.item())}), flush=True)
 
 
 # ----------------------------------------------------------------------------- cfg5 pipeline

@@ -63,7 +63,10 @@ typedef enum {
 
 /* core/granularity.hpp:8 enum class Level { Chunk, Action, Token } */
 enum { CKRL_LEVEL_CHUNK = 0, CKRL_LEVEL_ACTION = 1, CKRL_LEVEL_TOKEN = 2 };
-enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3 };
+enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3, CKRL_DTYPE_F64 = 4 };
+
+/* NCCL communicator of a multi-rank job (ckrl_comm_create, below). */
+typedef struct ckrl_comm ckrl_comm;
 enum { CKRL_FLAG_TERMINATED = 1, CKRL_FLAG_TRUNCATED = 2, CKRL_FLAG_VALID = 4 };
 
 /* Diagnostics slots written to device memory (optim/losses.hpp:31-39 LossDiagnostics). */
@@ -308,6 +311,32 @@ int32_t ckrl_logits_grad(int64_t rows, int32_t vocab, int32_t logits_dtype, cons
  * and returns it as the call's status (0 when clear). */
 int32_t ckrl_read_status(const int32_t* status_device, ckrl_stream_t stream);
 
+/* ---- (f4) optimizer step --------------------------------------------------------------- */
+
+/* optim::Adam (optim/adam.hpp:10-27, adam.cpp:15-41). */
+typedef struct ckrl_adam_params {
+  double learning_rate;
+  double max_grad_norm; /* <= 0: no clipping */
+  double beta1;         /* reference default 0.9 */
+  double beta2;         /* 0.999 */
+  double eps;           /* 1e-8 */
+} ckrl_adam_params;
+
+/* Scratch for ckrl_adam_step (zero it once after allocating; its counter self-resets). */
+size_t ckrl_adam_workspace_bytes(void);
+
+/* Adam::step on `n` parameters (dtype CKRL_DTYPE_F32 or a double-precision step with
+ * dtype = 4, CKRL_DTYPE_F64): ||grad|| (fp64 accumulate; all-reduced over `comm` when the
+ * parameters are sharded across ranks), NonFinite if it is not finite (nothing is modified,
+ * *status_device set; read it with ckrl_read_status), grad clipped in place to max_grad_norm,
+ * then m / v / params updated with bias corrections for step `t` (>= 1, the count after this
+ * step: the reference's ++t_). *norm_device receives the pre-clip norm. Asynchronous on
+ * `stream`; two launches (the update a programmatic dependent of the norm). */
+int32_t ckrl_adam_step(int32_t dtype, int64_t n, void* params, void* grad, void* exp_avg,
+                       void* exp_avg_sq, const ckrl_adam_params* p, int64_t t, double* norm_device,
+                       int32_t* status_device, void* workspace, size_t workspace_bytes,
+                       ckrl_comm* comm, ckrl_stream_t stream);
+
 /* ---- (d) losses ----------------------------------------------------------------------- */
 
 /* ppo_loss (optim/losses.cpp:62-232) over every record (full batch), fused with the token
@@ -331,7 +360,6 @@ int32_t ckrl_grpo_loss(const ckrl_rollout* rollout, const ckrl_grpo_batch* batch
 
 /* Whole step (the measured hot path): assemble -> [stats allgather over `comm`] -> fused
  * loss. comm may be NULL (single rank). */
-typedef struct ckrl_comm ckrl_comm;
 int32_t ckrl_ppo_step(const ckrl_rollout* rollout, const ckrl_policy_outputs* policy,
                       const ckrl_gae_params* gae, const ckrl_granularity* spec,
                       const ckrl_ppo_params* params, ckrl_ppo_batch* batch,

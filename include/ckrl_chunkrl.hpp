@@ -161,6 +161,16 @@ void validate_granularity(const GranularitySpec& spec);
 
 namespace policy {
 enum class ValueHeadKind { Scalar, Vector };
+
+/// The per-position logits gradient PolicyNet::accumulate_chunk_gradient forms before its
+/// outer_add / trunk backward (policy/policy_net.cpp:431-456), on the device: logits rows
+/// [P][vocab] (e.g. forward_logits outputs), tokens [P], coefficients [P] (ppo_loss's
+/// LossCoefficients or GRPO's, entropy optional) -> dlogits [P][vocab]. Positions with both
+/// coefficients zero give zero rows; a non-finite coefficient throws NonFinite (:437-438).
+std::vector<double> chunk_logits_gradient(std::span<const double> logits, int vocab,
+                                          std::span<const int> tokens,
+                                          std::span<const double> coeff_logprob,
+                                          std::span<const double> coeff_entropy = {});
 }  // namespace policy
 
 /// PolicyNet::value (policy_net.hpp:82): 1 entry for the scalar head, C for the vector head.
@@ -345,6 +355,25 @@ struct LossCoefficients {
 };
 
 void normalize_advantages(advantage::PpoBatch& batch);
+
+/// optim::Adam (optim/adam.hpp:10-27) with its moments resident on the device (float64, the
+/// reference's precision). step() takes host spans like the reference — grad is clipped in
+/// place, the pre-clip norm is returned, NonFinite leaves everything untouched;
+/// step_device() runs on device-resident params / grad (n doubles each) with no copies.
+class Adam {
+ public:
+  Adam(std::size_t num_params, double learning_rate, double max_grad_norm = 0.0, double beta1 = 0.9,
+       double beta2 = 0.999, double eps = 1e-8);
+  ~Adam();
+  Adam(const Adam&) = delete;
+  Adam& operator=(const Adam&) = delete;
+  double step(std::span<double> params, std::span<double> grad);
+  double step_device(double* params, double* grad);
+
+ private:
+  struct State;
+  State* s_;
+};
 
 LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& batch,
                          std::span<const std::size_t> record_indices, const PpoParams& params,

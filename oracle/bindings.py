@@ -55,7 +55,7 @@ class Oracle:
         for name in ("orc_compute_gae", "orc_assemble_ppo", "orc_normalize_advantages",
                      "orc_ppo_loss", "orc_grpo_group_advantage", "orc_success_rate_filter",
                      "orc_assemble_grpo", "orc_grpo_loss", "orc_validate_granularity",
-                     "orc_logits_grad"):
+                     "orc_logits_grad", "orc_adam_step"):
             getattr(self.lib, name).restype = C.c_int
 
     # --- rollout marshalling -------------------------------------------------
@@ -124,6 +124,14 @@ class Oracle:
         out = np.zeros((rows, V))
         st = self.lib.orc_logits_grad(C.c_int64(rows), V, _p(lg), _p(tk), _p(kl), _p(ke), _p(out))
         return st, out
+
+    def adam_step(self, params, grad, m, v, t, lr, max_grad_norm=0.0, beta1=0.9, beta2=0.999, eps=1e-8):
+        """Adam::step (optim/adam.cpp:15-41) in place on float64 arrays; returns (status, norm)."""
+        norm = C.c_double(0.0)
+        st = self.lib.orc_adam_step(C.c_int64(params.size), _p(params), _p(grad), _p(m), _p(v),
+                                    C.c_double(lr), C.c_double(max_grad_norm), C.c_double(beta1),
+                                    C.c_double(beta2), C.c_double(eps), C.c_int64(t), C.byref(norm))
+        return st, norm.value
 
     def assemble_ppo(self, d, spec, gamma, lam):
         a, l, v = spec
@@ -252,6 +260,7 @@ def _ref_lib():
         lib.refx_create.restype = C.c_void_p
         lib.refx_last_error.restype = C.c_char_p
         lib.refx_bpol_offset.restype = C.c_longlong
+        lib.refx_adam.restype = C.c_int
         for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo_subset",
                   "refx_grpo_subset", "refx_ppo", "refx_grpo",
                   "refx_replay_ppo_grad", "refx_replay_grpo_grad"):
@@ -260,6 +269,19 @@ def _ref_lib():
             getattr(lib, n).restype = C.c_double
         _REF_LIB = lib
     return _REF_LIB
+
+
+def ref_adam(params, grads, lr, max_grad_norm=0.0, beta1=0.9, beta2=0.999, eps=1e-8):
+    """The reference's optim::Adam over len(grads) steps (grads [steps][n], clipped in place);
+    returns (status, params, grads, norms)."""
+    lib = _ref_lib()
+    p = _c64(params).copy()
+    g = _c64(grads).copy()
+    steps, n = g.shape
+    norms = np.zeros(steps)
+    st = lib.refx_adam(C.c_longlong(n), steps, _p(p), _p(g), C.c_double(lr), C.c_double(max_grad_norm),
+                       C.c_double(beta1), C.c_double(beta2), C.c_double(eps), _p(norms))
+    return st, p, g, norms
 
 
 class RefScenario:

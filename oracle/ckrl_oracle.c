@@ -115,6 +115,33 @@ int orc_logits_grad(int64_t rows, int V, const double* logits, const int32_t* to
   return st;
 }
 
+/* optim/adam.cpp:15-41 (Adam::step). `t` is the step count after this step (the reference's
+ * ++t_); m, v are the moment buffers. Returns NonFinite without modifying anything when the
+ * gradient norm is not finite. */
+int orc_adam_step(int64_t n, double* params, double* grad, double* m, double* v, double lr,
+                  double max_grad_norm, double beta1, double beta2, double eps, int64_t t,
+                  double* norm_out) {
+  double norm_sq = 0.0;
+  for (int64_t i = 0; i < n; ++i) norm_sq += grad[i] * grad[i];
+  double norm = sqrt(norm_sq);
+  *norm_out = norm;
+  if (!isfinite(norm)) return ST_NON_FINITE;
+  if (max_grad_norm > 0.0 && norm > max_grad_norm) {
+    double scale = max_grad_norm / norm;
+    for (int64_t i = 0; i < n; ++i) grad[i] *= scale;
+  }
+  double bc1 = 1.0 - pow(beta1, (double)t);
+  double bc2 = 1.0 - pow(beta2, (double)t);
+  for (int64_t i = 0; i < n; ++i) {
+    m[i] = beta1 * m[i] + (1.0 - beta1) * grad[i];
+    v[i] = beta2 * v[i] + (1.0 - beta2) * grad[i] * grad[i];
+    double mhat = m[i] / bc1;
+    double vhat = v[i] / bc2;
+    params[i] -= lr * mhat / (sqrt(vhat) + eps);
+  }
+  return ST_OK;
+}
+
 /* ---------------------------------------------------------------- PPO assembly */
 
 typedef struct {

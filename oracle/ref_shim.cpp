@@ -28,6 +28,7 @@
 #include "chunkrl/advantage/assembler.hpp"
 #include "chunkrl/core/errors.hpp"
 #include "chunkrl/core/rng.hpp"
+#include "chunkrl/optim/adam.hpp"
 #include "chunkrl/optim/losses.hpp"
 #include "chunkrl/optim/update.hpp"
 #include "chunkrl/placement/rollout.hpp"
@@ -195,6 +196,23 @@ void* refx_create(const refx_cfg* cfg, int* status) {
     g_err = ex.what();
     *status = status_of(ex);
     return nullptr;
+  }
+}
+
+// The reference's own optim::Adam (optim/adam.cpp) for `steps` steps; grads[s*n + i] is the
+// gradient of step s (clipped in place, as the reference does). Returns the status of the
+// first failing step; norms[s] the pre-clip norm of each step.
+int refx_adam(long long n, int steps, double* params, double* grads, double lr, double max_grad_norm,
+              double beta1, double beta2, double eps, double* norms) {
+  try {
+    optim::Adam adam(static_cast<std::size_t>(n), lr, max_grad_norm, beta1, beta2, eps);
+    for (int s = 0; s < steps; ++s)
+      norms[s] = adam.step(std::span<double>(params, static_cast<std::size_t>(n)),
+                           std::span<double>(grads + static_cast<std::size_t>(s) * n, static_cast<std::size_t>(n)));
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
   }
 }
 

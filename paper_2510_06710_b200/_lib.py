@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CKRL_LIB") or os.path.join(HERE, "libckrl.so")
 
 LEVEL_CHUNK, LEVEL_ACTION, LEVEL_TOKEN = 0, 1, 2
-DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32 = 0, 1, 2, 3
+DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32, DTYPE_F64 = 0, 1, 2, 3, 4
 FLAG_TERMINATED, FLAG_TRUNCATED, FLAG_VALID = 1, 2, 4
 DIAG_COUNT = 8
 DIAG_NAMES = ("loss", "surrogate", "value_loss", "entropy", "clip_frac", "approx_kl", "units",
@@ -144,6 +144,9 @@ SIGNATURES = {
     "ckrl_logits_grad": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp,
                                      C.c_int32, vp, vp, vp]),
     "ckrl_read_status": (C.c_int32, [vp, vp]),
+    "ckrl_adam_workspace_bytes": (C.c_size_t, []),
+    "ckrl_adam_step": (C.c_int32, [C.c_int32, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp,
+                                   C.c_size_t, vp, vp]),
     "ckrl_debug_timeline": (C.c_int32, [vp, C.c_int32]),
     "ckrl_select_records": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
                                         C.c_int64, vp, P(Rollout), P(PpoBatchC), P(PolicyOutputs), vp,

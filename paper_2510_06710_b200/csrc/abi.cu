@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cmath>
+
 using namespace ckrl;
 
 namespace {
@@ -386,6 +388,37 @@ int32_t ckrl_read_status(const int32_t* status_device, ckrl_stream_t stream) {
   CKRL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   if (host == CKRL_ERR_NON_FINITE) return fail(host, "non-finite gradient coefficient");
   if (host) return fail(host, "device-side error");
+  return CKRL_OK;
+}
+
+size_t ckrl_adam_workspace_bytes(void) { return adam_workspace_bytes(); }
+
+int32_t ckrl_adam_step(int32_t dtype, int64_t n, void* params, void* grad, void* exp_avg,
+                       void* exp_avg_sq, const ckrl_adam_params* p, int64_t t, double* norm_device,
+                       int32_t* status_device, void* workspace, size_t workspace_bytes,
+                       ckrl_comm* comm, ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(p && workspace, CKRL_ERR_INVALID_ARGUMENT, "params / workspace required");
+  CKRL_REQUIRE(workspace_bytes >= adam_workspace_bytes(), CKRL_ERR_INVALID_ARGUMENT, "workspace too small");
+  CKRL_REQUIRE(dtype == CKRL_DTYPE_F32 || dtype == CKRL_DTYPE_F64, CKRL_ERR_INVALID_ARGUMENT,
+               "Adam state dtype must be f32 or f64");
+  CKRL_REQUIRE(n >= 0 && t >= 1, CKRL_ERR_INVALID_ARGUMENT, "n >= 0 and step t >= 1 required");
+  CKRL_REQUIRE(n == 0 || (params && grad && exp_avg && exp_avg_sq), CKRL_ERR_INVALID_ARGUMENT,
+               "params / grad / moments required");
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int f64 = dtype == CKRL_DTYPE_F64;
+  // adam.cpp:29-30: bias corrections with the host's pow, as the reference computes them
+  const double bc1 = 1.0 - std::pow(p->beta1, (double)t), bc2 = 1.0 - std::pow(p->beta2, (double)t);
+  CKRL_CUDA(launch_adam_norm(f64, grad, n, ws, s));
+  const bool shard = comm && comm->world > 1;
+  if (shard)
+    CKRL_NCCL(nccl().AllReduce(adam_norm_sq_slot(ws), adam_norm_sq_slot(ws), 1, ncclFloat64, ncclSum,
+                               comm->nc, s));
+  CKRL_CUDA(launch_adam_update(f64, params, grad, exp_avg, exp_avg_sq, n, p->learning_rate, p->max_grad_norm,
+                               p->beta1, p->beta2, p->eps, bc1, bc2, ws, norm_device, status_device,
+                               shard ? 0 : 1, s));
   return CKRL_OK;
 }
 

@@ -70,6 +70,12 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
+size_t adam_workspace_bytes();
+double* adam_norm_sq_slot(char* ws);
+cudaError_t launch_adam_norm(int f64, const void* g, int64_t n, char* ws, cudaStream_t s);
+cudaError_t launch_adam_update(int f64, void* p, void* g, void* m, void* v, int64_t n, double lr,
+                               double max_norm, double b1, double b2, double eps, double bc1, double bc2,
+                               char* ws, double* norm_out, int32_t* status, int pdl, cudaStream_t s);
 cudaError_t launch_logits_grad(const void* logits, int logits_bf16, const void* tokens, int tok_i32,
                                const float* coeff_lp, const float* coeff_ent, int64_t rows, int V,
                                void* out, int out_bf16, int32_t* status, cudaStream_t s);

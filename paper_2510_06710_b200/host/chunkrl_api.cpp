@@ -893,4 +893,87 @@ LossDiagnostics grpo_loss(const CurrentPolicy& net, const advantage::GrpoBatch& 
 
 }  // namespace optim
 
+namespace policy {
+
+std::vector<double> chunk_logits_gradient(std::span<const double> logits, int vocab,
+                                          std::span<const int> tokens,
+                                          std::span<const double> coeff_logprob,
+                                          std::span<const double> coeff_entropy) {
+  const std::size_t P = tokens.size();
+  if (vocab < 1 || logits.size() != P * static_cast<std::size_t>(vocab) || coeff_logprob.size() != P ||
+      (!coeff_entropy.empty() && coeff_entropy.size() != P))
+    throw LengthMismatch("coefficient length must be C*M");
+  if (P == 0) return {};
+  std::vector<float> lg(logits.begin(), logits.end());
+  std::vector<int32_t> tk(tokens.begin(), tokens.end());
+  std::vector<float> kl(coeff_logprob.begin(), coeff_logprob.end());
+  std::vector<float> ke(coeff_entropy.begin(), coeff_entropy.end());
+  DevBuf<float> d_lg, d_kl, d_ke, d_out(lg.size());
+  DevBuf<int32_t> d_tk, d_st(1);
+  d_lg.upload(lg);
+  d_tk.upload(tk);
+  d_kl.upload(kl);
+  if (!ke.empty()) d_ke.upload(ke);
+  d_st.zero();
+  throw_if_error(ckrl_logits_grad(static_cast<int64_t>(P), vocab, CKRL_DTYPE_F32, d_lg.get(), CKRL_DTYPE_I32,
+                                  d_tk.get(), d_kl.get(), ke.empty() ? nullptr : d_ke.get(), CKRL_DTYPE_F32,
+                                  d_out.get(), d_st.get(), nullptr));
+  throw_if_error(ckrl_read_status(d_st.get(), nullptr));
+  std::vector<float> out = d_out.download();
+  return std::vector<double>(out.begin(), out.end());
+}
+
+}  // namespace policy
+
+namespace optim {
+
+struct Adam::State {
+  std::size_t n = 0;
+  ckrl_adam_params p{};
+  std::int64_t t = 0;
+  DevBuf<double> m, v, norm, params, grad;
+  DevBuf<int32_t> status;
+  DevBuf<unsigned char> ws;
+};
+
+Adam::Adam(std::size_t num_params, double learning_rate, double max_grad_norm, double beta1, double beta2,
+           double eps)
+    : s_(new State) {
+  s_->n = num_params;
+  s_->p = ckrl_adam_params{learning_rate, max_grad_norm, beta1, beta2, eps};
+  s_->m.alloc(num_params);
+  s_->v.alloc(num_params);
+  s_->m.zero();
+  s_->v.zero();
+  s_->norm.alloc(1);
+  s_->status.alloc(1);
+  s_->ws.alloc(ckrl_adam_workspace_bytes());
+  s_->ws.zero();
+}
+
+Adam::~Adam() { delete s_; }
+
+double Adam::step_device(double* params, double* grad) {
+  s_->status.zero();
+  throw_if_error(ckrl_adam_step(CKRL_DTYPE_F64, static_cast<int64_t>(s_->n), params, grad, s_->m.get(),
+                                s_->v.get(), &s_->p, s_->t + 1, s_->norm.get(), s_->status.get(), s_->ws.get(),
+                                s_->ws.size(), nullptr, nullptr));
+  throw_if_error(ckrl_read_status(s_->status.get(), nullptr));  // NonFinite: t_ unchanged (adam.cpp:21-28)
+  ++s_->t;
+  return s_->norm.download()[0];
+}
+
+double Adam::step(std::span<double> params, std::span<double> grad) {
+  if (params.size() != s_->n || grad.size() != s_->n) throw LengthMismatch("Adam buffer size mismatch");
+  s_->params.upload(params.data(), params.size());
+  s_->grad.upload(grad.data(), grad.size());
+  const double norm = step_device(s_->params.get(), s_->grad.get());
+  std::vector<double> p = s_->params.download(), g = s_->grad.download();
+  std::copy(p.begin(), p.end(), params.begin());
+  std::copy(g.begin(), g.end(), grad.begin());
+  return norm;
+}
+
+}  // namespace optim
+
 }  // namespace ckrl::chunkrl

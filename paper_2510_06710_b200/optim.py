@@ -187,3 +187,56 @@ class GrpoStep:
 
     def diagnostics(self, stream=None) -> dict:
         return read_diagnostics(self.diag, stream)
+
+
+class AdamParamsC(C.Structure):
+    _fields_ = [("learning_rate", C.c_double), ("max_grad_norm", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double)]
+
+
+class Adam:
+    """optim::Adam (optim/adam.hpp:10-27): plain Adam with optional global gradient-norm
+    clipping, on device tensors. step(params, grad) clips grad in place when
+    max_grad_norm > 0, updates params, and returns the pre-clip gradient norm (a host float,
+    like the reference; raises NonFinite without modifying anything when it is not finite).
+    step_async leaves the norm / status on the device (no host sync). State dtype follows the
+    parameters: float32, or float64 for the reference's precision. With `comm` (parameters
+    sharded across ranks) ||g||^2 is all-reduced over NCCL."""
+
+    def __init__(self, num_params: int, learning_rate: float, max_grad_norm: float = 0.0,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, device="cuda",
+                 dtype=torch.float32, comm=None):
+        self.m = torch.zeros(num_params, dtype=dtype, device=device)
+        self.v = torch.zeros(num_params, dtype=dtype, device=device)
+        self.t = 0
+        self.params = AdamParamsC(learning_rate, max_grad_norm, beta1, beta2, eps)
+        nb = _lib.lib().ckrl_adam_workspace_bytes()
+        self.ws = torch.zeros(int(nb), dtype=torch.uint8, device=device)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.comm = comm
+
+    def step_async(self, params: torch.Tensor, grad: torch.Tensor, stream=None) -> None:
+        n = self.m.numel()
+        if params.numel() != n or grad.numel() != n:
+            from .errors import LengthMismatch
+            raise LengthMismatch("Adam buffer size mismatch")
+        if params.dtype != self.m.dtype or grad.dtype != self.m.dtype:
+            raise TypeError("params / grad dtype must match the optimizer state")
+        dt = _lib.DTYPE_F64 if self.m.dtype == torch.float64 else _lib.DTYPE_F32
+        _lib.check(_lib.lib().ckrl_adam_step(
+            dt, n, C.c_void_p(params.data_ptr()), C.c_void_p(grad.data_ptr()),
+            C.c_void_p(self.m.data_ptr()), C.c_void_p(self.v.data_ptr()), C.byref(self.params),
+            self.t + 1, C.c_void_p(self.norm.data_ptr()), C.c_void_p(self.status.data_ptr()),
+            C.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+            self.comm.handle if self.comm is not None else None, stream_ptr(stream)))
+        self.t += 1
+
+    def step(self, params: torch.Tensor, grad: torch.Tensor, stream=None) -> float:
+        self.status.zero_()
+        self.step_async(params, grad, stream)
+        st = _lib.lib().ckrl_read_status(C.c_void_p(self.status.data_ptr()), stream_ptr(stream))
+        if st:
+            self.t -= 1  # the reference throws before ++t_ (adam.cpp:21-28)
+            _lib.check(st)
+        return float(self.norm.item())

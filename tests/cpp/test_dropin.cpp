@@ -660,6 +660,60 @@ TEST_CASE("GRPO loss: two-member group, equal weights") {
   CHECK(d.units == 2);
 }
 
+TEST_CASE("logits gradient seam matches the reference's per-position formula") {
+  // policy_net.cpp:444-456 restated in double on the host for a 3-position chunk of 5 bins
+  const int V = 5;
+  const std::vector<double> lg = {0.1, -1.2, 2.0, 0.3, 0.0, 1.5, 1.5, -0.5, 0.2, 3.0, -2.0, 0.0, 0.7, 0.1, -0.4};
+  const std::vector<int> tok = {2, 4, 0};
+  const std::vector<double> klp = {0.25, 0.0, -1.5}, kent = {0.01, 0.0, 0.02};
+  std::vector<double> got = policy::chunk_logits_gradient(lg, V, tok, klp, kent);
+  CHECK(got.size() == lg.size());
+  for (int k = 0; k < 3; ++k) {
+    double mx = lg[k * V];
+    for (int v = 0; v < V; ++v) mx = std::max(mx, lg[k * V + v]);
+    double s = 0.0;
+    for (int v = 0; v < V; ++v) s += std::exp(lg[k * V + v] - mx);
+    const double lse = mx + std::log(s);
+    double H = 0.0;
+    for (int v = 0; v < V; ++v) H -= std::exp(lg[k * V + v] - lse) * (lg[k * V + v] - lse);
+    for (int v = 0; v < V; ++v) {
+      const double ls = lg[k * V + v] - lse, p = std::exp(ls);
+      double want = klp[k] * ((v == tok[k] ? 1.0 : 0.0) - p) + kent[k] * (-p * (ls + H));
+      if (klp[k] == 0.0 && kent[k] == 0.0) want = 0.0;
+      CHECK(std::fabs(got[k * V + v] - want) <= 1e-6 * std::max(1.0, std::fabs(want)));
+    }
+  }
+  std::vector<double> bad = klp;
+  bad[2] = std::nan("");
+  CHECK_THROWS_AS(policy::chunk_logits_gradient(lg, V, tok, bad, kent), NonFinite);
+  CHECK_THROWS_AS(policy::chunk_logits_gradient(lg, V, tok, std::vector<double>{1.0}, kent), LengthMismatch);
+}
+
+TEST_CASE("Adam on the quadratic probe drives parameters toward zero") {
+  // tests/test_optim.cpp:464-475
+  std::vector<double> theta{1.0, -2.0, 3.0};
+  Adam adam(3, 0.1);
+  for (int i = 0; i < 200; ++i) {
+    std::vector<double> grad = theta;
+    adam.step(theta, grad);
+  }
+  for (double v : theta) CHECK(std::abs(v) < 0.05);
+}
+
+TEST_CASE("Adam gradient norm clipping") {
+  // tests/test_optim.cpp:477-484
+  std::vector<double> theta{0.0, 0.0};
+  Adam adam(2, 0.1, 1.0);
+  std::vector<double> grad{30.0, 40.0};
+  double norm = adam.step(theta, grad);
+  CHECK_APPROX(norm, 50.0, 1e-12);
+  CHECK_APPROX(std::sqrt(grad[0] * grad[0] + grad[1] * grad[1]), 1.0, 1e-9);
+  std::vector<double> bad{std::nan(""), 1.0};
+  CHECK_THROWS_AS(adam.step(theta, bad), NonFinite);
+  std::vector<double> short_grad{1.0};
+  CHECK_THROWS_AS(adam.step(theta, short_grad), LengthMismatch);
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
     for (const auto& c : cases()) std::printf("%s\n", c.name);

@@ -79,3 +79,30 @@ def test_reference_rejects_what_the_abi_rejects():
     sc = RefScenario()
     assert sc.ppo((1, 0, 1))["status"] == 1   # UnsupportedCombination (action adv, chunk lp)
     assert sc.ppo((0, 2, 1))["status"] == 12  # ConfigError (value level != advantage level)
+
+
+@pytest.mark.parametrize("max_norm", [0.0, 1.0, 1e3])
+def test_adam_oracle_bitexact_vs_reference(oracle, max_norm):
+    """Row f4: the oracle's Adam::step restatement equals the reference's optim::Adam bit-for-bit
+    over several steps (norms, clipped grads, parameters)."""
+    from oracle.bindings import ref_adam
+    rng = np.random.default_rng(7)
+    n, steps = 257, 6
+    p0 = rng.normal(size=n)
+    grads = rng.normal(size=(steps, n)) * 3.0
+    st, p_ref, g_ref, norms_ref = ref_adam(p0, grads, 0.01, max_norm)
+    assert st == 0
+    p, m, v = p0.copy(), np.zeros(n), np.zeros(n)
+    for s in range(steps):
+        g = grads[s].copy()
+        st, norm = oracle.adam_step(p, g, m, v, s + 1, 0.01, max_norm)
+        assert st == 0 and norm == norms_ref[s]
+        np.testing.assert_array_equal(g, g_ref[s])
+    np.testing.assert_array_equal(p, p_ref)
+    # non-finite norm: NonFinite, nothing modified
+    bad = grads[:1].copy()
+    bad[0, 3] = np.inf
+    assert ref_adam(p0, bad, 0.01, max_norm)[0] == 6
+    p2, g2 = p0.copy(), bad[0].copy()
+    assert oracle.adam_step(p2, g2, np.zeros(n), np.zeros(n), 1, 0.01, max_norm)[0] == 6
+    np.testing.assert_array_equal(p2, p0)
