@@ -449,6 +449,27 @@ int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* spec, const double* params,
                           ckrl_pipeline_outputs* out, void* workspace, size_t workspace_bytes,
                           ckrl_stream_t stream);
 
+/* ---- (f3) wire and on-disk formats (host) ------------------------------------------------ */
+
+/* dump_slab (core/types.cpp:9-28) of an SoA slab in HOST memory: the reference's
+ * trajectories.txt text ("# env_id episode_uid step tokens[M] reward terminated truncated
+ * valid" then one line per atomic slot; uid = env << 32 | episode_id, -1 frozen; reward as
+ * %.17g of the f64 reward, e.g. ckrl_pipeline_outputs.reward_f64). Writes at most `capacity`
+ * bytes (NUL-terminated when it fits) and the full text length to *length (capacity 0 /
+ * out NULL: size query). */
+int32_t ckrl_dump_slab(int32_t num_envs, int32_t num_chunks, int32_t chunk_len,
+                       int32_t tokens_per_action, int32_t token_dtype, const void* tokens,
+                       const double* reward, const uint8_t* flags, const int32_t* episode_id,
+                       char* out, size_t capacity, size_t* length);
+
+/* save_checkpoint / load_checkpoint (policy/checkpoint.cpp:37-83): the CKRL v1 file of a
+ * policy descriptor + its flat f64 parameters (host memory). Load with params NULL queries
+ * the descriptor and count; errors are the reference's chunkrl::Error cases (bad magic,
+ * version, count mismatch, truncation) as CKRL_ERR_GENERIC with the reference's message. */
+int32_t ckrl_save_checkpoint(const ckrl_policy_desc* desc, const double* params, const char* path);
+int32_t ckrl_load_checkpoint(const char* path, ckrl_policy_desc* desc, double* params,
+                             int64_t capacity, int64_t* count);
+
 /* ---- multi-GPU (NCCL over NVLink): stats + loss scalars only -------------------------- */
 int32_t ckrl_comm_unique_id(void* out_id /* 128 bytes */);
 int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out);

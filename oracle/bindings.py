@@ -261,6 +261,12 @@ def _ref_lib():
         lib.refx_last_error.restype = C.c_char_p
         lib.refx_bpol_offset.restype = C.c_longlong
         lib.refx_adam.restype = C.c_int
+        for n in ("refx_dump_slab", "refx_save_checkpoint", "refx_load_checkpoint"):
+            getattr(lib, n).restype = C.c_int
+        lib.refx_dump_slab.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        lib.refx_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
+        lib.refx_load_checkpoint.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                                             C.POINTER(C.c_longlong)]
         for n in ("refx_export", "refx_export_episodes", "refx_export_params", "refx_ppo_subset",
                   "refx_grpo_subset", "refx_ppo", "refx_grpo",
                   "refx_replay_ppo_grad", "refx_replay_grpo_grad"):
@@ -282,6 +288,19 @@ def ref_adam(params, grads, lr, max_grad_norm=0.0, beta1=0.9, beta2=0.999, eps=1
     st = lib.refx_adam(C.c_longlong(n), steps, _p(p), _p(g), C.c_double(lr), C.c_double(max_grad_norm),
                        C.c_double(beta1), C.c_double(beta2), C.c_double(eps), _p(norms))
     return st, p, g, norms
+
+
+def ref_load_checkpoint(path: str):
+    """The reference's load_checkpoint: (status, descriptor 7-tuple, params)."""
+    lib = _ref_lib()
+    desc = (C.c_int * 7)()
+    cnt = C.c_longlong(0)
+    st = lib.refx_load_checkpoint(path.encode(), desc, None, 0, C.byref(cnt))
+    if st:
+        return st, None, None
+    p = np.zeros(cnt.value)
+    st = lib.refx_load_checkpoint(path.encode(), desc, _p(p), cnt, C.byref(cnt))
+    return st, tuple(desc), p
 
 
 class RefScenario:
@@ -379,6 +398,18 @@ class RefScenario:
                                        C.c_double(upper), int(length_normalized), min_group_size,
                                        C.c_double(clip), C.c_longlong(ix.size), _p(ix), _p(diag))
         return st, diag
+
+    def dump_slab(self) -> str:
+        """The reference's own dump_slab text (core/types.cpp:9-28) of this rollout."""
+        n = C.c_size_t(0)
+        self.lib.refx_dump_slab(C.c_void_p(self.h), None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        self.lib.refx_dump_slab(C.c_void_p(self.h), buf, n.value, C.byref(n))
+        return buf.raw[:n.value].decode()
+
+    def save_checkpoint(self, path: str) -> None:
+        if self.lib.refx_save_checkpoint(C.c_void_p(self.h), path.encode()):
+            raise RuntimeError(self.lib.refx_last_error().decode())
 
     def bpol_offset(self) -> int:
         return int(self.lib.refx_bpol_offset(C.c_void_p(self.h)))

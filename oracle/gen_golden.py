@@ -123,5 +123,21 @@ def main():
         print(f"{path}: {os.path.getsize(path) / 1024:.1f} KiB")
 
 
+def dump_fixture():
+    """dump_toyreach.npz: a reference rollout's SoA slab + the reference's own dump_slab text
+    (core/types.cpp:9-28), for tests/test_formats.py / test_gpu_pipeline.py on the GPU box."""
+    sc = RefScenario(num_envs=4, num_chunks=5, chunk_length=3, max_episode_steps=5, reward_shaping=1,
+                     env_seed=21, sample_seed=22, net_seed=23)
+    d = sc.export(with_logits=False)
+    text = sc.dump_slab()
+    path = os.path.join(OUT, "dump_toyreach.npz")
+    np.savez_compressed(path, tokens=d["tokens"], reward=d["reward"], flags=d["flags"],
+                        episode_id=d["episode_id"], text=np.frombuffer(text.encode(), np.uint8))
+    print("wrote", path, len(text), "bytes of dump text")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "dump":
+        dump_fixture()
+        sys.exit(0)
     main()

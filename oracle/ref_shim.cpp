@@ -29,6 +29,7 @@
 #include "chunkrl/core/errors.hpp"
 #include "chunkrl/core/rng.hpp"
 #include "chunkrl/optim/adam.hpp"
+#include "chunkrl/policy/checkpoint.hpp"
 #include "chunkrl/optim/losses.hpp"
 #include "chunkrl/optim/update.hpp"
 #include "chunkrl/placement/rollout.hpp"
@@ -209,6 +210,40 @@ int refx_adam(long long n, int steps, double* params, double* grads, double lr, 
     for (int s = 0; s < steps; ++s)
       norms[s] = adam.step(std::span<double>(params, static_cast<std::size_t>(n)),
                            std::span<double>(grads + static_cast<std::size_t>(s) * n, static_cast<std::size_t>(n)));
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
+  }
+}
+
+// The reference's own dump_slab (core/types.cpp:9-28) of the scenario's slab; *len gets the
+// full length, at most cap bytes are copied.
+int refx_dump_slab(void* h, char* out, size_t cap, size_t* len) {
+  const std::string text = dump_slab(static_cast<Scenario*>(h)->slab);
+  *len = text.size();
+  if (out && cap) std::memcpy(out, text.data(), std::min(cap, text.size()));
+  return 0;
+}
+
+// save_checkpoint / load_checkpoint (policy/checkpoint.cpp:37-83) of the rollout snapshot.
+int refx_save_checkpoint(void* h, const char* path) {
+  try {
+    policy::save_checkpoint(static_cast<Scenario*>(h)->snapshot, path);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
+  }
+}
+int refx_load_checkpoint(const char* path, int* desc7, double* params, long long cap, long long* count) {
+  try {
+    policy::PolicyNet net = policy::load_checkpoint(path);
+    const policy::PolicyDescriptor& d = net.descriptor();
+    const int f[7] = {d.obs_dim, d.hidden, d.trunk_layers, d.value_hidden, d.vocab, d.C, d.M};
+    std::memcpy(desc7, f, sizeof f);
+    *count = static_cast<long long>(net.num_params());
+    if (params && *count <= cap) std::memcpy(params, net.params().data(), sizeof(double) * net.num_params());
     return 0;
   } catch (const std::exception& ex) {
     g_err = ex.what();

@@ -422,6 +422,44 @@ int32_t ckrl_adam_step(int32_t dtype, int64_t n, void* params, void* grad, void*
   return CKRL_OK;
 }
 
+int32_t ckrl_dump_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
+                       const double* reward, const uint8_t* flags, const int32_t* episode_id, char* out,
+                       size_t capacity, size_t* length) {
+  CKRL_REQUIRE(E >= 0 && Tc >= 0 && C >= 1 && M >= 1, CKRL_ERR_LENGTH_MISMATCH, "bad slab dimensions");
+  CKRL_REQUIRE(length, CKRL_ERR_INVALID_ARGUMENT, "length output required");
+  CKRL_REQUIRE((int64_t)E * Tc == 0 || (tokens && reward && flags && episode_id), CKRL_ERR_INVALID_ARGUMENT,
+               "slab arrays required");
+  CKRL_REQUIRE(token_dtype == CKRL_DTYPE_U8 || token_dtype == CKRL_DTYPE_I32, CKRL_ERR_INVALID_ARGUMENT,
+               "token dtype must be u8 or i32");
+  std::string text;
+  format_slab(E, Tc, C, M, token_dtype, tokens, reward, flags, episode_id, text);
+  *length = text.size();
+  if (out && capacity) {
+    const size_t n = text.size() < capacity ? text.size() : capacity;
+    std::memcpy(out, text.data(), n);
+    if (n < capacity) out[n] = '\0';
+  }
+  return CKRL_OK;
+}
+
+int32_t ckrl_save_checkpoint(const ckrl_policy_desc* d, const double* params, const char* path) {
+  CKRL_REQUIRE(d && path, CKRL_ERR_INVALID_ARGUMENT, "descriptor / path required");
+  const int64_t n = policy_num_params(*d);
+  CKRL_REQUIRE(n >= 0, CKRL_ERR_CONFIG, "bad policy descriptor");
+  CKRL_REQUIRE(n == 0 || params, CKRL_ERR_INVALID_ARGUMENT, "parameters required");
+  std::string err;
+  const int32_t st = write_checkpoint(*d, params, n, path, err);
+  return st ? fail(st, err) : CKRL_OK;
+}
+
+int32_t ckrl_load_checkpoint(const char* path, ckrl_policy_desc* d, double* params, int64_t capacity,
+                             int64_t* count) {
+  CKRL_REQUIRE(path && d && count, CKRL_ERR_INVALID_ARGUMENT, "path / descriptor / count required");
+  std::string err;
+  const int32_t st = read_checkpoint(path, d, params, capacity, count, err);
+  return st ? fail(st, err) : CKRL_OK;
+}
+
 static bool fused_enabled() {
   static int on = -1;
   if (on < 0) {

@@ -1,6 +1,8 @@
 // Launchers shared between the kernel translation units and the C-ABI layer.
 #pragma once
 
+#include <string>
+
 #include "common.cuh"
 
 namespace ckrl {
@@ -70,6 +72,12 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
+int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
+                    const double* reward, const uint8_t* flags, const int32_t* episode_id, std::string& out);
+int32_t write_checkpoint(const ckrl_policy_desc& d, const double* params, int64_t count, const char* path,
+                         std::string& err);
+int32_t read_checkpoint(const char* path, ckrl_policy_desc* d, double* params, int64_t capacity,
+                        int64_t* count_out, std::string& err);
 size_t adam_workspace_bytes();
 double* adam_norm_sq_slot(char* ws);
 cudaError_t launch_adam_norm(int f64, const void* g, int64_t n, char* ws, cudaStream_t s);

@@ -140,6 +140,16 @@ def test_pipeline_logits_output(ref_cache):
 
 
 @pytest.mark.parametrize("name", sorted(SCENARIOS))
+def test_pipeline_dump_is_the_references_trajectories_text(name, ref_cache):
+    """Row f3: the CUDA rollout's slab, written in the reference's trajectories.txt format
+    (ckrl_dump_slab), is byte-identical to the reference's own dump_slab of its rollout."""
+    from paper_2510_06710_b200 import formats
+    sc, _, p, ids = ref_cache(name)
+    _, g = run_pipeline(name, 2 if specs_of(SCENARIOS[name])[0]["num_envs"] % 2 == 0 else 1, p, ids)
+    assert formats.dump_slab(g["tokens"], g["reward_f64"], g["flags"], g["episode_id"]) == sc.dump_slab()
+
+
+@pytest.mark.parametrize("name", sorted(SCENARIOS))
 def test_pipeline_scheduling_invariance(name, ref_cache):
     _, _, p, ids = ref_cache(name)
     E = specs_of(SCENARIOS[name])[0]["num_envs"]
