@@ -382,6 +382,9 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
  * [4..7] first unit phase of each buffer warp, [8] last row tile, [9] all roles done,
  * [10] reduction done. Synchronises the device. */
 int32_t ckrl_debug_timeline(uint64_t* out, int32_t n);
+/* Profiling aid: per-CTA %globaltimer stamps of the last TMA loss launch, [3][1184]: start,
+ * roles done, exit. Synchronises the device. */
+int32_t ckrl_debug_cta_times(uint64_t* out, int32_t n);
 
 /* ---- (e) rollout pipeline on CUDA streams / events (cfg5) ----------------------------- */
 

@@ -144,6 +144,7 @@ SIGNATURES = {
     "ckrl_logits_grad": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp,
                                      C.c_int32, vp, vp, vp]),
     "ckrl_read_status": (C.c_int32, [vp, vp]),
+    "ckrl_debug_cta_times": (C.c_int32, [vp, C.c_int32]),
     "ckrl_adam_workspace_bytes": (C.c_size_t, []),
     "ckrl_dump_slab": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
                                    C.c_char_p, C.c_size_t, P(C.c_size_t)]),

@@ -873,6 +873,12 @@ int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* sp, const double* params,
   return CKRL_OK;
 }
 
+int32_t ckrl_debug_cta_times(uint64_t* out, int32_t n) {
+  CKRL_CUDA(cudaDeviceSynchronize());
+  CKRL_CUDA(debug_cta_times(out, n));
+  return CKRL_OK;
+}
+
 int32_t ckrl_debug_timeline(uint64_t* out, int32_t n) {
   CKRL_REQUIRE(out && n > 0, CKRL_ERR_INVALID_ARGUMENT, "bad timeline buffer");
   CKRL_CUDA(cudaDeviceSynchronize());

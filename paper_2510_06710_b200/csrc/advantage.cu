@@ -420,6 +420,15 @@ static bool serial_gae_enabled() {  // thread-per-env schedule (measured slower;
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
                                 double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
                                 cudaStream_t s, int /*reserved_sms*/) {
+  // The overlapped step's loss kernel (one ~217 KB-smem CTA per SM) starts while this runs:
+  // an SM whose L1/shared split was configured for this kernel's small footprint cannot take
+  // the loss CTA until it drains and reconfigures, so ask for the maximum carveout here too.
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(ppo_assemble_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ppo_assemble_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve = true;
+  }
   const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
   if (serial_gae_enabled() && n_items <= kSerialItems) {
     const int nt = 32 * kAsmWarpsPerCta;

@@ -72,6 +72,7 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t debug_cta_times(uint64_t* out, int n);
 int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
                     const double* reward, const uint8_t* flags, const int32_t* episode_id, std::string& out);
 int32_t write_checkpoint(const ckrl_policy_desc& d, const double* params, int64_t count, const char* path,

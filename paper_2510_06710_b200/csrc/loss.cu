@@ -20,11 +20,18 @@
 
 namespace ckrl {
 
-// Optional on-device timeline of CTA 0 (SM cycles), read with ckrl_debug_timeline().
+// Optional on-device timeline of CTA 0 (%globaltimer, ns), read with ckrl_debug_timeline().
 __device__ uint64_t g_timeline[32];
-__device__ __forceinline__ void tl_mark(int slot) {
-  if (blockIdx.x == 0) g_timeline[slot] = clock64();
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
+__device__ __forceinline__ void tl_mark(int slot) {
+  if (blockIdx.x == 0) g_timeline[slot] = gtimer();
+}
+// Per-CTA start / roles-done / exit stamps of the last TMA loss launch (ckrl_debug_cta_times).
+__device__ uint64_t g_cta_times[3][1184];
 
 constexpr float kL2E = 1.4426950408889634f;
 constexpr double kLN2 = 0.6931471805599453;
@@ -544,15 +551,19 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
     double x = 0.0;
     for (int w = 0; w < nwarps; ++w) x += s_red[w][tid];
     parts[blockIdx.x * RAW_COUNT + tid] = x;
-    __threadfence();
   }
   __syncthreads();
   if (tid == 0) tl_mark(26);
-  if (tid == 0) *s_last = atomicAdd(&tickets[TICKET_LOSS], 1u) == gridDim.x - 1;
+  if (tid == 0) {
+    // one acq_rel ticket instead of fence + atomic + fence: the release publishes this CTA's
+    // partials (ordered before it by the barrier), the acquire makes every earlier CTA's visible
+    uint32_t t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(&tickets[TICKET_LOSS]) : "memory");
+    *s_last = t == gridDim.x - 1;
+  }
   __syncthreads();
   if (tid == 0) tl_mark(27);
   if (!*s_last) return;
-  __threadfence();
   // Last CTA: every thread sums a fixed strided subset of the partials (loads in
   // parallel), then a fixed-shape tree over warps -> deterministic for a given grid.
   {
@@ -902,50 +913,75 @@ __host__ __device__ constexpr size_t rowbuf_bytes(int cap) {
 // Row metadata (what the row warps read): token ids and per-slot "evaluate" flags. In the
 // fused step the assembly outputs do not exist yet, so every valid slot is evaluated
 // (counted slots are a subset); otherwise the assembled activity decides.
+struct RowRegs {
+  int32_t tok[4];
+  int32_t g[4];   // GRPO: env group id (non-PDL path)
+  float w[4];     // GRPO: slot weight
+  uint8_t fl[4];  // raw slot flags / counted / membership byte
+};
 template <int MODE, bool FUSED>
-__device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec, int lane,
-                                         const MetaSmem& m, bool from_flags) {
+__device__ __forceinline__ void row_meta_load(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                              RowRegs& R, bool from_flags) {
   const int C = a.C, P = C * a.M;
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P, s0 = r0 * C;
-  int32_t tok[4];
-  uint8_t nd[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
-    if (i < rows) tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
+    if (i < rows) R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
+    R.fl[q] = 1;
+    if (i < slots && !a.all_rows && MODE != MODE_STATS) {
+      if (FUSED || from_flags) {
+        R.fl[q] = a.ro.flags[s0 + i];
+      } else if (MODE == MODE_PPO) {
+        R.fl[q] = a.counted[s0 + i];
+      } else {
+        R.g[q] = a.env_group[(int)(s0 + i) / C / a.Tc];
+        R.fl[q] = a.slot_member[s0 + i];
+        R.w[q] = a.slot_weight[s0 + i];
+      }
+    }
+  }
+}
+template <int MODE, bool FUSED>
+__device__ __forceinline__ void row_meta_store(const LossArgs& a, int nrec, int lane, const RowRegs& R,
+                                               const MetaSmem& m, bool from_flags) {
+  const int C = a.C, P = C * a.M;
+  const int rows = nrec * P, slots = nrec * C;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = lane + 32 * q;
+    if (i < rows) m.tok[i] = R.tok[q];
     if (i < slots) {
       bool n = true;
       if (!a.all_rows && MODE != MODE_STATS) {
-        if (FUSED || from_flags) {  // assembly outputs not available yet: every valid slot
-          n = (a.ro.flags[s0 + i] & CKRL_FLAG_VALID) != 0;
-        } else if (MODE == MODE_PPO) {
-          n = a.counted[s0 + i] != 0;
-        } else {
-          const int e = (int)((s0 + i) / C / a.Tc);
-          const int32_t g = a.env_group[e];
-          const uint8_t mem = a.slot_member[s0 + i];
-          const float w = a.slot_weight[s0 + i];
-          n = (g >= 0) & (mem != 0) & (w != 0.0f);
-        }
+        if (FUSED || from_flags)
+          n = (R.fl[q] & CKRL_FLAG_VALID) != 0;
+        else if (MODE == MODE_PPO)
+          n = R.fl[q] != 0;
+        else
+          n = (R.g[q] >= 0) & (R.fl[q] != 0) & (R.w[q] != 0.0f);
       }
-      nd[q] = n ? 1 : 0;
+      m.need[i] = n ? 1 : 0;
     }
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = lane + 32 * q;
-    if (i < rows) m.tok[i] = tok[q];
-    if (i < slots) m.need[i] = nd[q];
-  }
+}
+template <int MODE, bool FUSED>
+__device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                         const MetaSmem& m, bool from_flags) {
+  RowRegs R;
+  row_meta_load<MODE, FUSED>(a, r0, nrec, lane, R, from_flags);
+  row_meta_store<MODE, FUSED>(a, nrec, lane, R, m, from_flags);
 }
 
-// Unit metadata (read only by the buffer warp that owns the tile), register image.
+// Register images of a tile's metadata hold the RAW loaded values: nothing derived from a
+// load is computed before the matching *_store, so a *_load only issues loads and their
+// latency hides behind whatever runs in between (the current tile's unit phase).
 struct UnitRegs {
   float old[4], w[4], adv[4], ret[4], nv[4];
-  int32_t esz[4];
+  int32_t esz[4], g[4];
   double eadv[4];
-  uint8_t act[4];
+  uint8_t act[4];  // raw: counted (PPO) / slot membership (GRPO)
 };
 
 // Loads that may read what other CTAs wrote earlier in the same (fused) launch go
@@ -962,18 +998,11 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
     if (i < rows) R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
     if (i < slots) {
       if (MODE == MODE_PPO) {
-        R.act[q] = __ldcg(a.counted + s0 + i) != 0 ? 2 : 0;
-        R.w[q] = 0.0f;
+        R.act[q] = __ldcg(a.counted + s0 + i);
       } else if (MODE == MODE_GRPO) {
-        const int e = (int)((s0 + i) / C / a.Tc);
-        const int32_t g = a.env_group[e];
-        const uint8_t mem = a.slot_member[s0 + i];
-        const float w = a.slot_weight[s0 + i];
-        const bool on = (g >= 0) & (mem != 0) & (w != 0.0f);
-        R.act[q] = on ? 2 : 0;
-        R.w[q] = w;
-      } else {
-        R.act[q] = 0;
+        R.g[q] = a.env_group[(int)(s0 + i) / C / a.Tc];
+        R.act[q] = a.slot_member[s0 + i];
+        R.w[q] = a.slot_weight[s0 + i];
       }
     }
     if (MODE == MODE_PPO) {
@@ -990,7 +1019,7 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
       }
     }
     if (MODE == MODE_GRPO && i < nrec) {
-      const int e = (int)((r0 + i) / a.Tc);
+      const int e = (int)(r0 + i) / a.Tc;
       R.esz[q] = a.env_group_size[e];
       R.eadv[q] = a.env_adv[e];
     }
@@ -1007,8 +1036,16 @@ __device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int
     const int i = lane + 32 * q;
     if (i < rows) m.old[i] = R.old[q];
     if (i < slots) {
-      m.act[i] = R.act[q];
-      m.w[i] = R.w[q];
+      if (MODE == MODE_PPO) {
+        m.act[i] = R.act[q] != 0 ? 2 : 0;
+        m.w[i] = 0.0f;
+      } else if (MODE == MODE_GRPO) {
+        m.act[i] = ((R.g[q] >= 0) & (R.act[q] != 0) & (R.w[q] != 0.0f)) ? 2 : 0;
+        m.w[i] = R.w[q];
+      } else {
+        m.act[i] = 0;
+        m.w[i] = 0.0f;
+      }
     }
     if (MODE == MODE_PPO && i < slots) {  // covers both unit kinds (nrec <= slots)
       m.adv[i] = R.adv[q];
@@ -1024,10 +1061,19 @@ __device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int
 
 // Warp-level unit phase over one tile, all inputs from shared memory (see unit_phase for
 // the semantics; identical arithmetic).
+// Where the unit phase writes its per-position / per-unit outputs: the caller's global arrays,
+// or (bulk path) shared-memory staging rebased so that index k0 + row lands on staging[row].
+struct Outs {
+  float *tok_lp, *tok_ent, *coeff_lp, *coeff_ent, *coeff_val;
+};
+__device__ __forceinline__ Outs outs_of(const LossArgs& a) {
+  return Outs{a.tok_lp, a.tok_ent, a.coeff_lp, a.coeff_ent, a.coeff_val};
+}
+
 template <int MODE>
 __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossConsts& k, Acc& acc,
                                                 const RowSmem& sm, const MetaSmem& m, int64_t r0,
-                                                int nrec, int lane) {
+                                                int nrec, int lane, const Outs& o) {
   const int C = a.C, M = a.M, P = C * M;
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P;
@@ -1036,17 +1082,17 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   for (int row = lane; row < rows; row += 32) {
     const int64_t kk = k0 + row;
     const int sl = row / M, r = row / P;
-    const float sf = sm.s[row];
-    const double ls = log_f32_exact_exp(sf);
+    // row warps left log2(sum) in s and sum(e*y)/sum(e) in t2 (TMA row phase)
+    const double ls = (double)sm.s[row] * kLN2;
     const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
-    const float ent = (float)ls - 0.6931471805599453f * (sm.t2[row] / sf);
+    const float ent = (float)ls - 0.6931471805599453f * sm.t2[row];
     sm.lp[row] = lp;
-    if (a.tok_lp) a.tok_lp[kk] = (float)lp;
-    if (a.tok_ent) a.tok_ent[kk] = ent;
+    if (o.tok_lp) o.tok_lp[kk] = (float)lp;
+    if (o.tok_ent) o.tok_ent[kk] = ent;
     const bool on = (m.act[sl] & 2) != 0;
     if (MODE == MODE_PPO) {
       if (on) acc.ent += ent;
-      if (a.coeff_ent) a.coeff_ent[kk] = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
+      if (o.coeff_ent) o.coeff_ent[kk] = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
     }
     if (MODE != MODE_STATS && a.lp_level == CKRL_LEVEL_TOKEN) {
       float coeff = 0.0f;
@@ -1068,7 +1114,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         acc.kl += su.kl;
         coeff = (float)(-scale * su.dlogprob);
       }
-      if (a.coeff_lp) a.coeff_lp[kk] = coeff;
+      if (o.coeff_lp) o.coeff_lp[kk] = coeff;
     }
   }
   __syncwarp();
@@ -1120,8 +1166,8 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
           acc.kl += su.kl;
           coeff = (float)(-scale * su.dlogprob);
         }
-        if (a.coeff_lp)
-          for (int j = 0; j < M; ++j) a.coeff_lp[(r0 * C + sl) * M + j] = coeff;
+        if (o.coeff_lp)
+          for (int j = 0; j < M; ++j) o.coeff_lp[(r0 * C + sl) * M + j] = coeff;
       }
       if (act_val) {
         float cv = 0.0f;
@@ -1130,7 +1176,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
           acc.valsq += err * err;
           cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
         }
-        if (a.coeff_val) a.coeff_val[r0 * C + sl] = cv;
+        if (o.coeff_val) o.coeff_val[r0 * C + sl] = cv;
       }
     }
 
@@ -1175,9 +1221,9 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
           }
           coeff = (float)(-scale * su.dlogprob);
         }
-        if (a.coeff_lp)
+        if (o.coeff_lp)
           for (int t = lane; t < P; t += 32)
-            a.coeff_lp[rec * P + t] = (m.act[r * C + t / M] & 2) ? coeff : 0.0f;
+            o.coeff_lp[rec * P + t] = (m.act[r * C + t / M] & 2) ? coeff : 0.0f;
       }
       if (chunk_val && lane == 0) {
         float cv = 0.0f;
@@ -1186,7 +1232,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
           acc.valsq += err * err;
           cv = (float)(a.vcoef * 2.0 * err * k.inv_val);
         }
-        if (a.coeff_val) a.coeff_val[rec] = cv;
+        if (o.coeff_val) o.coeff_val[rec] = cv;
       }
     }
 }
@@ -1318,6 +1364,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
 
   if (tid == 0) {
     tl_mark(0);
+    if (blockIdx.x < 1184) g_cta_times[0][blockIdx.x] = gtimer();
     for (int s = 0; s < nstage; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kCW);
@@ -1407,8 +1454,10 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
               xt = sizeof(LT) == 4 ? (float)reinterpret_cast<const float*>(rp[q])[tok]
                                    : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
             }
-            sm.s[row] = need ? s_[q] : 1.0f;
-            sm.t2[row] = need ? t_[q] : 0.0f;
+            // the row's two transcendental finishing ops stay on the row warps (2 MUFU ops per
+            // 256): the unit phase then needs no MUFU, which the row warps keep saturated
+            sm.s[row] = need ? __log2f(s_[q]) : 0.0f;               // log2 of the shifted sum
+            sm.t2[row] = need ? t_[q] * __frcp_rn(s_[q]) : 0.0f;    // sum e*y / sum e
             sm.c[row] = c_[q];
             sm.xt[row] = xt;
           }
@@ -1457,37 +1506,66 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       bufwarps_sync<BW>();
     }
     const LossConsts k = FUSED ? s_kf : s_k;
+    // Software pipeline: this warp's next tile's unit metadata and the row metadata of the
+    // next user of this buffer are issued (raw, into registers) before the current unit
+    // phase, so their memory latency hides behind it.
     int it = m;
-    for (int64_t tile = blockIdx.x + (int64_t)m * gridDim.x; tile < a.n_tiles; tile += stride, it += BW) {
-      int64_t r0;
-      const int nrec = tile_recs(tile, r0);
+    int64_t tile = blockIdx.x + (int64_t)m * gridDim.x;
+    int64_t r0 = 0;
+    int nrec = 0;
+    UnitRegs ur;
+    if (tile < a.n_tiles) {
+      nrec = tile_recs(tile, r0);
+      unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);
+    }
+    for (; tile < a.n_tiles; tile += stride, it += BW) {
       const int b = it % nbuf;
       buf_of(it, sm, mt);
-      UnitRegs ur;
-      unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);  // in flight while rows finish
       mbar_wait(&rowfull_bar[b], (it / nbuf) & 1);
+      const bool probe = lane == 0 && m == 0;
       if (lane == 0 && it == m) tl_mark(20 + m);
+      if (probe && it == BW) tl_mark(3);
       unit_meta_store<MODE>(a, nrec, lane, ur, mt);
       __syncwarp();
-      unit_phase_smem<MODE>(a, k, acc, sm, mt, r0, nrec, lane);
+      if (probe && it == 0) tl_mark(1);
+      if (probe && it == BW) tl_mark(28);
+      const int64_t cr0 = r0;
+      const int cn = nrec;
+      const int64_t ntile = tile + stride;
+      if (ntile < a.n_tiles) {
+        nrec = tile_recs(ntile, r0);
+        unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);
+      }
+      const int64_t rtile = tile + (int64_t)nbuf * gridDim.x;  // next user of buffer b
+      RowRegs rr;
+      int64_t rr0 = 0;
+      int rn = 0;
+      if (rtile < a.n_tiles) {
+        rn = tile_recs(rtile, rr0);
+        row_meta_load<MODE, FUSED>(a, rr0, rn, lane, rr, a.pdl != 0);
+      }
+      if (probe && it == 0) tl_mark(2);
+      if (probe && it == BW) tl_mark(29);
+      unit_phase_smem<MODE>(a, k, acc, sm, mt, cr0, cn, lane, outs_of(a));
       __syncwarp();
       if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
-      const int64_t ntile = tile + (int64_t)nbuf * gridDim.x;  // next user of buffer b
-      if (ntile < a.n_tiles) {
-        int64_t nr0;
-        const int nn = tile_recs(ntile, nr0);
-        row_meta<MODE, FUSED>(a, nr0, nn, lane, mt, a.pdl != 0);
+      if (probe && it == BW) tl_mark(30);
+      if (rtile < a.n_tiles) {
+        row_meta_store<MODE, FUSED>(a, rn, lane, rr, mt, a.pdl != 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
     }
+
   }
   if (warp == 1 && lane == 0) tl_mark(8);  // row warp 0 done with its last tile
   __syncthreads();
   if (tid == 0) tl_mark(9);
+  if (tid == 0 && blockIdx.x < 1184) g_cta_times[1][blockIdx.x] = gtimer();
   if (MODE == MODE_STATS) return;
   reduce_and_finish(a, FUSED ? s_kf : s_k, acc, tid, kThreads, s_red, &s_last);
   if (tid == 0) tl_mark(10);
+  if (tid == 0 && blockIdx.x < 1184) g_cta_times[2][blockIdx.x] = gtimer();
 }
 
 __global__ void finalize_kernel(LossArgs a) {
@@ -1671,6 +1749,10 @@ cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out) {
 
 cudaError_t read_timeline(uint64_t* out, int n) {
   return cudaMemcpyFromSymbol(out, g_timeline, sizeof(uint64_t) * (n < 32 ? n : 32));
+}
+
+cudaError_t debug_cta_times(uint64_t* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(uint64_t) * (n < 3 * 1184 ? n : 3 * 1184));
 }
 
 cudaError_t launch_finalize(LossArgs& a, cudaStream_t s) {

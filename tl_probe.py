@@ -15,6 +15,12 @@ torch.cuda.synchronize()
 buf = (C.c_uint64 * 32)()
 _lib.check(_lib.lib().ckrl_debug_timeline(buf, 32))
 t0 = buf[0]
-names = {0:'start',1:'gaeA',2:'gridbar',3:'consts',4:'unit0',8:'rowlast',9:'alldone',10:'reduced',11:'r0meta',12:'r0full',13:'r0done',14:'r1meta',15:'r1full',16:'r1done',17:'r2meta',18:'r2full',19:'r2done',20:'b0rowfull',24:'b0meta0',25:'red_sync',26:'red_fence',27:'red_ticket'}
-print(name, ' '.join(f"{names[i]}={(buf[i]-t0)/1965:.2f}" for i in sorted(names) if buf[i] >= t0 and buf[i]-t0 < 10**9))
-print('  waits(us): row0 metafull=%.2f full=%.2f | buf0 rowfull=%.2f unit+meta=%.2f' % tuple(buf[i]/1965 for i in (28,29,30,31)))
+names = {0:'start',1:'u0store',2:'u0issue',3:'u1rowfull',28:'u1store',29:'u1issue',30:'u1done',1:'gaeA',2:'gridbar',3:'consts',4:'unit0',8:'rowlast',9:'alldone',10:'reduced',11:'r0meta',12:'r0full',13:'r0done',14:'r1meta',15:'r1full',16:'r1done',17:'r2meta',18:'r2full',19:'r2done',20:'b0rowfull',24:'b0meta0',25:'red_sync',26:'red_fence',27:'red_ticket'}
+print(name, ' '.join(f"{names[i]}={(buf[i]-t0)/1000:.2f}" for i in sorted(names) if buf[i] >= t0 and buf[i]-t0 < 10**9))
+
+
+# kernel-level view: CUDA events around one step (assembly + loss), for comparison with the marks
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record(); st(ro, pol); e1.record(); torch.cuda.synchronize()
+_lib.check(_lib.lib().ckrl_debug_timeline(buf, 32))
+print('  step event us=%.2f  cta0 start->reduced us=%.2f' % (e0.elapsed_time(e1) * 1e3, (buf[10] - buf[0]) / 1000))
