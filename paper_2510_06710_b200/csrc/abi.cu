@@ -557,8 +557,12 @@ static int32_t grpo_loss_impl(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
                               const ckrl_policy_outputs* po, const ckrl_granularity* spec,
                               const ckrl_grpo_params* p, ckrl_loss_outputs* out, double* diag,
                               void* ws, int world, const StatsRecord* recs, int finalize,
-                              cudaStream_t s) {
+                              cudaStream_t s, int pdl = 0) {
   LossArgs a = base_args(ro, po, (char*)ws, world);
+  if (pdl) {  // programmatic dependent of the GRPO assembly (grpo_weights_kernel)
+    a.pdl = 1;
+    a.ro = *ro;
+  }
   a.mode = MODE_GRPO;
   a.adv_level = spec->advantage_level;
   a.lp_level = spec->logprob_level;
@@ -696,7 +700,8 @@ int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
   CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, w, L, s));
   if (world == 1)
     return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
-                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s);
+                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s,
+                          overlap_sms() > 0 && po->logits_dtype >= 0);
   if ((st = gather_stats(comm, w, L, s))) return st;
   if ((st = grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, world,
                            reinterpret_cast<const StatsRecord*>(w + L.stats_all), 0, s)))

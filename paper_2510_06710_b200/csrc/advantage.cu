@@ -368,6 +368,9 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
 // index is a warp prefix count of matching slots.
 __global__ void grpo_weights_kernel(ckrl_rollout ro, int length_normalized, ckrl_grpo_batch gb,
                                     const char* ws, WsLayout L) {
+  // the GRPO step's loss kernel may start streaming logits now (programmatic dependent
+  // launch); it reads the group data only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= ro.num_envs) return;
