@@ -56,11 +56,20 @@ __global__ void __launch_bounds__(kAdamThreads) adam_norm_kernel(const T* __rest
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
+  // last CTA: thread t sums partials t, t + 256, ... (loads in parallel), then the same
+  // fixed-shape tree -> deterministic for a given grid
   double t = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partials + b);
-  *norm_sq = t;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(partials + b);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double u = 0.0;
+  for (int w = 0; w < kAdamThreads / 32; ++w) u += wsum[w];
+  *norm_sq = u;
   *ticket = 0;  // self-reset for the next launch
 }
 

@@ -1078,10 +1078,13 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P;
   const bool chunk_adv = a.adv_level == CKRL_LEVEL_CHUNK;
+  // small-integer quotients (rows < 2^10, M, P, C <= 2^13) by float reciprocal: exact
+  const float inv_m = 1.0f / (float)M, inv_p = 1.0f / (float)P;
+  auto qdiv = [](int x, float inv) { return (int)(((float)x + 0.5f) * inv); };
 
   for (int row = lane; row < rows; row += 32) {
     const int64_t kk = k0 + row;
-    const int sl = row / M, r = row / P;
+    const int sl = qdiv(row, inv_m), r = qdiv(row, inv_p);
     // row warps left log2(sum) in s and sum(e*y)/sum(e) in t2 (TMA row phase)
     const double ls = (double)sm.s[row] * kLN2;
     const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
@@ -1188,7 +1191,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
       double lpn = 0.0, lpo = 0.0, wsum = 0.0;
       int any = 0;
       for (int t = lane; t < P; t += 32) {
-        const int sl = r * C + t / M;
+        const int sl = r * C + qdiv(t, inv_m);
         if (m.act[sl] & 2) {
           lpn += sm.lp[r * P + t];
           lpo += (double)m.old[r * P + t];
@@ -1223,7 +1226,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         }
         if (o.coeff_lp)
           for (int t = lane; t < P; t += 32)
-            o.coeff_lp[rec * P + t] = (m.act[r * C + t / M] & 2) ? coeff : 0.0f;
+            o.coeff_lp[rec * P + t] = (m.act[r * C + qdiv(t, inv_m)] & 2) ? coeff : 0.0f;
       }
       if (chunk_val && lane == 0) {
         float cv = 0.0f;
@@ -1409,18 +1412,21 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     const int cwarp = warp - 1;
     const int sub = lane >> 3, l8 = lane & 7;
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it) {
-      const int s = it % nstage;
-      const int b = it % nbuf;
+    // ring positions and phase bits kept incrementally (no integer division per tile)
+    int s = 0, b = 0;
+    uint32_t sph = 0, bph = 0;
+    const float inv_m = 1.0f / (float)M;  // slot of row r: (r + 0.5) / M, exact for rows < 2^10
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it,
+                 s = (s + 1 == nstage) ? (sph ^= 1u, 0) : s + 1, b = (b + 1 == nbuf) ? (bph ^= 1u, 0) : b + 1) {
       unsigned char* bb = buf_base + b * rowbuf_bytes(cap);
       const RowSmem sm = carve_rows(bb, cap);
       const MetaSmem mt = carve_meta(bb + rowsmem_bytes(cap), cap);
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
-      mbar_wait(&metafull_bar[b], (it / nbuf) & 1);  // buffer b holds tile it's row metadata
+      mbar_wait(&metafull_bar[b], bph);  // buffer b holds tile it's row metadata
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(11 + 3 * it);
-      mbar_wait(&full_bar[s], (it / nstage) & 1);
+      mbar_wait(&full_bar[s], sph);
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
 #pragma unroll
@@ -1447,7 +1453,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
           for (int q = 0; q < RIF; ++q) {
             const int row = rowq[q];
             if (!live[q] || row >= rows) continue;
-            const bool need = mt.need[row / M] != 0;
+            const bool need = mt.need[(int)(((float)row + 0.5f) * inv_m)] != 0;
             float xt = 0.0f;
             if (need) {
               const int tok = mt.tok[row];
@@ -1457,7 +1463,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
             // the row's two transcendental finishing ops stay on the row warps (2 MUFU ops per
             // 256): the unit phase then needs no MUFU, which the row warps keep saturated
             sm.s[row] = need ? __log2f(s_[q]) : 0.0f;               // log2 of the shifted sum
-            sm.t2[row] = need ? t_[q] * __frcp_rn(s_[q]) : 0.0f;    // sum e*y / sum e
+            sm.t2[row] = need ? __fdividef(t_[q], s_[q]) : 0.0f;   // sum e*y / sum e
             sm.c[row] = c_[q];
             sm.xt[row] = xt;
           }
