@@ -33,3 +33,35 @@ for name in sys.argv[1:] or ["cfg3"]:
         q = lambda x: "min %.1f p50 %.1f p90 %.1f max %.1f" % (x.min(), np.median(x), np.percentile(x, 90), x.max())
         print(f"{name} {mode}: start [{q(s)}] done [{q(dn)}] exit [{q(ex)}] us")
         print("   slowest CTAs:", np.argsort(-dn)[:8].tolist(), "done-start spread", q(dn - s))
+
+# overlapped step: where and when the assembly CTAs ran vs the loss CTAs' start
+if os.environ.get("ASM_PROBE", "0") == "1" and hasattr(_lib.lib(), "ckrl_debug_asm_times"):
+    asm = (C.c_uint64 * (3 * 1184))()
+    smid = (C.c_uint32 * 1184)()
+    g = torch.cuda.CUDAGraph()  # replayed like bench.py (no host submission gaps)
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        st(ro, pol)
+    torch.cuda.current_stream().wait_stream(s_)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        st(ro, pol)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().ckrl_debug_asm_times(asm, 3 * 1184, smid))
+    _lib.check(_lib.lib().ckrl_debug_cta_times(buf, 3 * 1184))
+    A = np.array(asm, dtype=np.int64).reshape(3, 1184)
+    T = np.array(buf, dtype=np.int64).reshape(3, 1184)[:, :148]
+    nA = int((A[0] > 0).sum())
+    a0 = A[0][:nA].min()
+    dn = (T[1] - a0) / 1e3
+    ex = (T[2] - a0) / 1e3
+    print(f"loss done max {dn.max():.1f} exit max {ex.max():.1f} us (rel. first assembly start)")
+    print(f"assembly: {nA} CTAs, start [{(A[0][:nA]-a0).min()/1e3:.1f}..{(A[0][:nA]-a0).max()/1e3:.1f}] end [{(A[1][:nA]-a0).min()/1e3:.1f}..{(A[1][:nA]-a0).max()/1e3:.1f}] us")
+    ls = (T[0] - a0) / 1e3
+    asm_sms = set(A[2][:nA].tolist())
+    on = np.array([int(smid[i]) in asm_sms for i in range(148)])
+    print("(graph replay)")
+    print(f"loss CTA start (rel. first assembly start): on assembly SMs p50 {np.median(ls[on]):.1f} max {ls[on].max():.1f} (n={on.sum()}); others p50 {np.median(ls[~on]) if (~on).any() else -1:.1f} max {ls[~on].max() if (~on).any() else -1:.1f}")
