@@ -463,9 +463,9 @@ class RefScenario:
         return s, diag
 
     def bench_grpo(self, spec, threads, iters, align, eps_std=1e-8, length_normalized=True,
-                   clip=0.2):
+                   clip=0.2, apply_filter=True):
         diag = np.zeros(7)
         s = self.lib.refx_bench_grpo(C.c_void_p(self.h), spec[0], spec[1], C.c_double(eps_std),
                                      int(length_normalized), C.c_double(clip), threads, iters,
-                                     align, _p(diag))
+                                     align, _p(diag), int(apply_filter))
         return s, diag

@@ -639,8 +639,10 @@ TrajectorySlab sub_slab(const TrajectorySlab& slab, int e0, int e1) {
   s.tokens_per_action = slab.tokens_per_action;
   s.records.assign(slab.records.begin() + e0, slab.records.begin() + e1);
   for (const auto& ep : slab.episodes)
-    if (ep.env_id >= e0 && ep.env_id < e1)
+    if (ep.env_id >= e0 && ep.env_id < e1) {
       s.episodes.push_back(ep);
+      s.episodes.back().env_id -= e0;  // records are re-indexed from 0 in the shard
+    }
   return s;
 }
 } // namespace
@@ -717,7 +719,7 @@ double refx_bench_ppo(void* h, int adv_level, int lp_level, int val_level, doubl
 }
 
 double refx_bench_grpo(void* h, int adv_level, int lp_level, double eps_std, int length_normalized,
-                       double clip_eps, int threads, int iters, int align, double* diag) {
+                       double clip_eps, int threads, int iters, int align, double* diag, int apply_filter) {
   auto* s = static_cast<Scenario*>(h);
   try {
     threads = std::max(1, std::min(threads, s->E));
@@ -731,6 +733,7 @@ double refx_bench_grpo(void* h, int adv_level, int lp_level, double eps_std, int
     o.spec = GranularitySpec{level_of(adv_level), level_of(lp_level), level_of(adv_level)};
     o.eps_std = eps_std;
     o.length_normalized = length_normalized != 0;
+    o.apply_filter = apply_filter != 0;
     optim::GrpoParams gp;
     gp.clip_eps = clip_eps;
     const int P = static_cast<int>(shards.size());
