@@ -397,6 +397,7 @@ def main():
             advantage.assemble_ppo_batch(ro, PpoAssemblyOptions(GaeParams(0.99, 0.95), spec),
                                          out=step.batch)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # device busy while the host enqueues e0 / launch / e1
             e0.record(stream)
             optim.ppo_loss(ro, pol, step.batch, PpoParams(0.2, 0.5, 0.01, True), step.outputs,
                            diag=step.diag)
@@ -405,6 +406,7 @@ def main():
             from paper_2510_06710_b200 import advantage
             advantage.assemble_grpo_batch(ro, ept, GrpoAssemblyOptions(spec), out=step.batch)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # device busy while the host enqueues e0 / launch / e1
             e0.record(stream)
             optim.grpo_loss(ro, pol, step.batch, GrpoParams(0.2), step.outputs, diag=step.diag)
             e1.record(stream)
@@ -426,6 +428,7 @@ def main():
         gev = []
         for i in range(min(K, 50)):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)
             e0.record(stream)
             grad(i)
             e1.record(stream)
