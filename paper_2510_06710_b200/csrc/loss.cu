@@ -931,8 +931,10 @@ __device__ __forceinline__ void row_meta_load(const LossArgs& a, int64_t r0, int
     if (i < rows) R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
     R.fl[q] = 1;
     if (i < slots && !a.all_rows && MODE != MODE_STATS) {
-      if (FUSED || from_flags) {
+      if (FUSED) {
         R.fl[q] = a.ro.flags[s0 + i];
+      } else if (from_flags) {  // overlapped step: every row (the loss masks by counted), no load
+        R.fl[q] = CKRL_FLAG_VALID;
       } else if (MODE == MODE_PPO) {
         R.fl[q] = a.counted[s0 + i];
       } else {
@@ -974,10 +976,18 @@ __device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec
   row_meta_store<MODE, FUSED>(a, nrec, lane, R, m, from_flags);
 }
 
+// PPO tiles whose advantage, return and new-value units (value level == advantage level for
+// GAE assembly) fit one warp three times over.
+__device__ __forceinline__ bool small_units(const LossArgs& a, int nrec) {
+  const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : nrec * a.C;
+  return a.adv_level == a.val_level && 3 * U <= 32;
+}
+
 // Register images of a tile's metadata hold the RAW loaded values: nothing derived from a
 // load is computed before the matching *_store, so a *_load only issues loads and their
 // latency hides behind whatever runs in between (the current tile's unit phase).
 struct UnitRegs {
+  float mix;  // PPO small-unit path: this lane's advantage / return / new value (unit_meta_load)
   float old[4], w[4], adv[4], ret[4], nv[4];
   int32_t esz[4], g[4];
   double eadv[4];
@@ -1005,7 +1015,19 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
         R.w[q] = a.slot_weight[s0 + i];
       }
     }
-    if (MODE == MODE_PPO) {
+    if (MODE == MODE_PPO && small_units(a, nrec)) {
+      // one warp-wide load for all three per-unit arrays: lanes [0,U) advantages, [U,2U)
+      // returns, [2U,3U) new values (each global load instruction a buffer warp issues waits
+      // in the MIO queue behind the row warps' shared loads)
+      if (q == 0) {
+        const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;  // == advantage units
+        const int64_t ub = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
+        const float* p = lane < U ? a.adv + ub + lane
+                                  : lane < 2 * U ? a.ret + ub + (lane - U)
+                                                 : (a.new_values ? a.new_values + ub + (lane - 2 * U) : nullptr);
+        R.mix = (lane < 3 * U && p) ? __ldcg(p) : 0.0f;
+      }
+    } else if (MODE == MODE_PPO) {
       const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
       const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
       if (i < adv_units) {
@@ -1047,7 +1069,14 @@ __device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int
         m.w[i] = 0.0f;
       }
     }
-    if (MODE == MODE_PPO && i < slots) {  // covers both unit kinds (nrec <= slots)
+    if (MODE == MODE_PPO && small_units(a, nrec)) {
+      if (q == 0) {
+        const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+        if (lane < U) m.adv[lane] = R.mix;
+        else if (lane < 2 * U) m.ret[lane - U] = R.mix;
+        else if (lane < 3 * U) m.nv[lane - 2 * U] = R.mix;
+      }
+    } else if (MODE == MODE_PPO && i < slots) {  // covers both unit kinds (nrec <= slots)
       m.adv[i] = R.adv[q];
       m.ret[i] = R.ret[q];
       m.nv[i] = R.nv[q];

@@ -15,7 +15,7 @@ torch.cuda.synchronize()
 buf = (C.c_uint64 * 32)()
 _lib.check(_lib.lib().ckrl_debug_timeline(buf, 32))
 t0 = buf[0]
-names = {0:'start',1:'u0store',2:'u0issue',3:'u1rowfull',28:'u1store',29:'u1issue',30:'u1done',1:'gaeA',2:'gridbar',3:'consts',4:'unit0',8:'rowlast',9:'alldone',10:'reduced',11:'r0meta',12:'r0full',13:'r0done',14:'r1meta',15:'r1full',16:'r1done',17:'r2meta',18:'r2full',19:'r2done',20:'b0rowfull',24:'b0meta0',25:'red_sync',26:'red_fence',27:'red_ticket'}
+names = {0:'start',1:'u0store',2:'u0issue',3:'u1rowfull',28:'u1store',29:'u1issue',30:'u1done',31:'u1tokpass',1:'gaeA',2:'gridbar',3:'consts',4:'unit0',8:'rowlast',9:'alldone',10:'reduced',11:'r0meta',12:'r0full',13:'r0done',14:'r1meta',15:'r1full',16:'r1done',17:'r2meta',18:'r2full',19:'r2done',20:'b0rowfull',24:'b0meta0',25:'red_sync',26:'red_fence',27:'red_ticket'}
 print(name, ' '.join(f"{names[i]}={(buf[i]-t0)/1000:.2f}" for i in sorted(names) if buf[i] >= t0 and buf[i]-t0 < 10**9))
 
 
