@@ -197,7 +197,7 @@ def test_ppo_synthetic_vs_oracle(cfg_name, envs, oracle):
     assert torch.equal(first, step.diag)
 
 
-@pytest.mark.parametrize("cfg_name,envs", [("cfg2", None), ("cfg4", 64)])
+@pytest.mark.parametrize("cfg_name,envs", [("cfg2", None), ("cfg4", 64), ("cfg4", None)])
 def test_grpo_synthetic_vs_oracle(cfg_name, envs, oracle):
     from paper_2510_06710_b200 import synth
     cfg, d, logits, tokens = synth_case(cfg_name, envs)
