@@ -218,7 +218,12 @@ def test_grpo_synthetic_vs_oracle(cfg_name, envs, oracle):
     np.testing.assert_array_equal(step.batch.slot_member.cpu().numpy(), asm["slot_member"])
     st, want, coeff = oracle.grpo_loss(r, l, asm, r["logits"], 0.2)
     assert got[6] == want[6]
-    assert_close(got[:6], want[:6], TOL, "diag")
+    # The GRPO loss is a signed sum whose terms cancel (group-relative advantages sum to ~0),
+    # so its error scales with the terms' L1 mass, not with the result: at the full cfg4 size
+    # |sum| is ~1e-3 of sum|terms|. Bound: 1e-5 x max(|ref|, sum of |per-position coefficient|).
+    l1 = float(np.abs(coeff).sum())
+    assert_close(got[:2], want[:2], TOL, "loss / surrogate", floor=l1)
+    assert_close(got[2:6], want[2:6], TOL, "diag")
     assert_close(step.outputs.coeff_logprob.cpu().numpy(), coeff, 1e-4, "coeff")
 
 
