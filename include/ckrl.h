@@ -164,6 +164,9 @@ typedef struct {
   float* coeff_value;    /* value level shape, dLoss/dV */
   float* token_logprob;  /* [E][Tc][C][M]  new log-probs (evaluate_chunk) */
   float* token_entropy;  /* [E][Tc][C][M]  new entropies */
+  void* dlogits;         /* [E][Tc][C][M][V] optional, logits dtype: the softmax-backward seam
+                            (accumulate_chunk_gradient's dlogits, policy_net.cpp:431-456) fused
+                            into the loss launch (V = 256; ckrl_logits_grad otherwise) */
 } ckrl_loss_outputs;
 
 /* ---- host-only helpers (no device work) ---------------------------------------------- */

@@ -77,7 +77,7 @@ class GrpoBatchC(C.Structure):
 
 class LossOutputs(C.Structure):
     _fields_ = [("coeff_logprob", vp), ("coeff_entropy", vp), ("coeff_value", vp),
-                ("token_logprob", vp), ("token_entropy", vp)]
+                ("token_logprob", vp), ("token_entropy", vp), ("dlogits", vp)]
 
 
 class EnvConfig(C.Structure):

@@ -226,11 +226,12 @@ class LossOutputs:
     coeff_value: Optional[torch.Tensor] = None
     token_logprob: Optional[torch.Tensor] = None
     token_entropy: Optional[torch.Tensor] = None
+    dlogits: Optional[torch.Tensor] = None  # fused softmax-backward seam, logits' shape and dtype
 
     def c(self) -> _lib.LossOutputs:
         return _lib.LossOutputs(*[_ptr(t) for t in (
             self.coeff_logprob, self.coeff_entropy, self.coeff_value, self.token_logprob,
-            self.token_entropy)])
+            self.token_entropy, self.dlogits)])
 
     @classmethod
     def allocate(cls, rollout: RolloutBuffer, value_level: Level, tokens: bool = False):

@@ -119,6 +119,7 @@ void set_outputs(LossArgs& a, const ckrl_loss_outputs* o) {
   a.coeff_val = o->coeff_value;
   a.tok_lp = o->token_logprob;
   a.tok_ent = o->token_entropy;
+  a.dlogits = o->dlogits;
   a.all_rows = (o->token_logprob || o->token_entropy) ? 1 : 0;
 }
 
@@ -631,7 +632,7 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
   cudaStream_t s = (cudaStream_t)stream;
   WsLayout L = ws_layout(ro->num_envs, world);
   char* w = (char*)ws;
-  if (world == 1 && fused_enabled()) {
+  if (world == 1 && fused_enabled() && !(out && out->dlogits)) {
     // one persistent launch: GAE assembly overlapped with the logits stream
     LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
                           reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1);

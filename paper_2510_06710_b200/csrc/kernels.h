@@ -58,6 +58,7 @@ struct LossArgs {
   int reserved_sms;
   int nbuf;      // TMA kernel: row-partial buffers (multiple of 4, <= kMaxRowBufs)
   int rows_cap;  // TMA kernel: rows per buffer (rec_per_tile * C * M)
+  void* dlogits; // optional fused softmax-backward output [positions][V] (logits dtype)
 };
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,

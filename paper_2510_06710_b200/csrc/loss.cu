@@ -716,6 +716,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1102,7 +1110,8 @@ __device__ __forceinline__ Outs outs_of(const LossArgs& a) {
 template <int MODE>
 __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossConsts& k, Acc& acc,
                                                 const RowSmem& sm, const MetaSmem& m, int64_t r0,
-                                                int nrec, int lane, const Outs& o) {
+                                                int nrec, int lane, const Outs& o,
+                                                float* gklp = nullptr, float* gkent = nullptr) {
   const int C = a.C, M = a.M, P = C * M;
   const int rows = nrec * P, slots = nrec * C;
   const int64_t k0 = r0 * P;
@@ -1124,8 +1133,11 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
     const bool on = (m.act[sl] & 2) != 0;
     if (MODE == MODE_PPO) {
       if (on) acc.ent += ent;
-      if (o.coeff_ent) o.coeff_ent[kk] = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
+      const float cent = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
+      if (o.coeff_ent) o.coeff_ent[kk] = cent;
+      if (gkent) gkent[row] = cent;
     }
+    if (MODE == MODE_GRPO && gkent) gkent[row] = 0.0f;
     if (MODE != MODE_STATS && a.lp_level == CKRL_LEVEL_TOKEN) {
       float coeff = 0.0f;
       if (on) {
@@ -1147,6 +1159,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         coeff = (float)(-scale * su.dlogprob);
       }
       if (o.coeff_lp) o.coeff_lp[kk] = coeff;
+      if (gklp) gklp[row] = coeff;
     }
   }
   __syncwarp();
@@ -1200,6 +1213,8 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         }
         if (o.coeff_lp)
           for (int j = 0; j < M; ++j) o.coeff_lp[(r0 * C + sl) * M + j] = coeff;
+        if (gklp)
+          for (int j = 0; j < M; ++j) gklp[sl * M + j] = coeff;
       }
       if (act_val) {
         float cv = 0.0f;
@@ -1256,6 +1271,9 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
         if (o.coeff_lp)
           for (int t = lane; t < P; t += 32)
             o.coeff_lp[rec * P + t] = (m.act[r * C + qdiv(t, inv_m)] & 2) ? coeff : 0.0f;
+        if (gklp)
+          for (int t = lane; t < P; t += 32)
+            gklp[r * P + t] = (m.act[r * C + qdiv(t, inv_m)] & 2) ? coeff : 0.0f;
       }
       if (chunk_val && lane == 0) {
         float cv = 0.0f;
@@ -1269,6 +1287,91 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
     }
 }
 
+
+// ---------------------------------------------------------------------------------
+// Fused softmax-backward seam (row f1, GRAD kernels): once a tile's unit phase has produced
+// its per-position coefficients, the row warps that computed its rows re-read them (from L2:
+// the ring lag is kept to 4 tiles and the first read is issued evict_last) and write
+//   dlogits_v = klp * ([v == tok] - p_v) - kent * p_v * (ls_v + H)
+// (policy_net.cpp:444-456) from the row statistics already in shared memory (shift c,
+// log2 of the shifted sum, sum e*y / sum e) — the logits are read from HBM once, not twice.
+// ---------------------------------------------------------------------------------
+struct GradSmem {  // per row buffer: token id and the two coefficients of each row
+  int32_t* tok;
+  float* klp;
+  float* kent;
+};
+__device__ __forceinline__ GradSmem carve_grad(unsigned char* base, int cap) {
+  GradSmem g;
+  g.tok = reinterpret_cast<int32_t*>(base);
+  g.klp = reinterpret_cast<float*>(g.tok + cap);
+  g.kent = g.klp + cap;
+  return g;
+}
+template <typename LT>
+__device__ __forceinline__ void grad_row(const LossArgs& a, const RowSmem& sm, const GradSmem& gs, int row,
+                                         int64_t kk, int l8) {
+  constexpr int V = 256;
+  const float klp = gs.klp[row], kent = gs.kent[row];
+  float d[32];
+  if (klp == 0.0f && kent == 0.0f) {  // the reference skips the position: zero row
+#pragma unroll
+    for (int k = 0; k < 32; ++k) d[k] = 0.0f;
+  } else {
+    float x[32];
+    if (sizeof(LT) == 4) {
+      const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(a.logits) + kk * V);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 v = ldg_stream(p + l8 + 8 * i);
+        x[4 * i] = v.x;
+        x[4 * i + 1] = v.y;
+        x[4 * i + 2] = v.z;
+        x[4 * i + 3] = v.w;
+      }
+    } else {
+      const uint4* p = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.logits) + kk * V);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 v = ldg_stream_u4(p + l8 + 8 * i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          x[8 * i + 2 * j] = __uint_as_float(w[j] << 16);
+          x[8 * i + 2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+        }
+      }
+    }
+    const float c = sm.c[row], l2s = sm.s[row];
+    const float H = 0.6931471805599453f * (l2s - sm.t2[row]);  // entropy (nats)
+    const int tok = gs.tok[row];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const float z = fmaf(x[k], kL2E, -c) - l2s;  // log2 p
+      const float pv = ex2(z);
+      const float ls = z * 0.6931471805599453f;
+      const int col = sizeof(LT) == 4 ? 4 * (l8 + 8 * (k >> 2)) + (k & 3) : 8 * (l8 + 8 * (k >> 3)) + (k & 7);
+      d[k] = klp * ((col == tok ? 1.0f : 0.0f) - pv) - kent * (pv * (ls + H));
+    }
+  }
+  if (sizeof(LT) == 4) {
+    float4* q = reinterpret_cast<float4*>(static_cast<float*>(a.dlogits) + kk * V);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) __stcs(q + l8 + 8 * i, make_float4(d[4 * i], d[4 * i + 1], d[4 * i + 2], d[4 * i + 3]));
+  } else {
+    uint4* q = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.dlogits) + kk * V);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(d[8 * i + 2 * j], d[8 * i + 2 * j + 1]);
+        w[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      __stcs(q + l8 + 8 * i, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+  }
+}
 
 constexpr int kBufWarps = kRowBufs;  // buffer warp m owns row buffer m (tiles i = m mod 4)
 template <int ROWW, int BW = kBufWarps>
@@ -1373,7 +1476,7 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
 //                   barrier, while the producer and row warps already stream logits.
 // Synchronisation is mbarrier-only: full[s]/empty[s] (producer <-> row warps),
 // metafull[b] (buffer warp -> row warps), rowfull[b] (row warps -> buffer warp).
-template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW>
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW, bool GRAD = false>
 __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(LossArgs a, int nstage,
                                                                           uint32_t tile_bytes) {
   constexpr int kThreads = tma_threads<ROWW, BW>();
@@ -1392,6 +1495,8 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
   unsigned char* stage_base = smem_raw;
   unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
   const int nbuf = a.nbuf, cap = a.rows_cap;
+  unsigned char* grad_base = buf_base + (size_t)nbuf * rowbuf_bytes(cap);  // GRAD: GradSmem per buffer
+  auto grad_of = [&](int bi) { return carve_grad(grad_base + (size_t)bi * cap * 12, cap); };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
@@ -1418,6 +1523,8 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      uint64_t l2_keep = 0;
+      if (GRAD) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2_keep));
       const char* src = reinterpret_cast<const char*>(a.logits);
       const size_t rec_bytes = (size_t)P * V * sizeof(LT);
       int it = 0;
@@ -1432,7 +1539,10 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         unsigned char* d = stage_base + (size_t)s * tile_bytes;
         for (uint32_t off = 0; off < bytes; off += 32768u) {
           const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-          bulk_g2s(d + off, g + off, n, &full_bar[s]);
+          if (GRAD)  // keep the tile in L2 for the gradient pass's re-read
+            bulk_g2s_keep(d + off, g + off, n, &full_bar[s], l2_keep);
+          else
+            bulk_g2s(d + off, g + off, n, &full_bar[s]);
         }
       }
     }
@@ -1445,6 +1555,17 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     int s = 0, b = 0;
     uint32_t sph = 0, bph = 0;
     const float inv_m = 1.0f / (float)M;  // slot of row r: (r + 0.5) / M, exact for rows < 2^10
+    // GRAD: dlogits of an earlier tile whose coefficients the unit phase left in buffer b
+    auto grad_pass = [&](int64_t gtile, const RowSmem& gsm, const GradSmem& gs) {
+      int64_t gr0;
+      const int grows = tile_recs(gtile, gr0) * P;
+      for (int p = 0; p < kPasses; ++p) {
+        const int rg0 = (p * kCW + cwarp) * 4;
+        if (rg0 >= grows) break;  // warp-uniform
+        const int row = rg0 + sub;
+        if (row < grows) grad_row<LT>(a, gsm, gs, row, gr0 * P + row, l8);
+      }
+    };
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it,
                  s = (s + 1 == nstage) ? (sph ^= 1u, 0) : s + 1, b = (b + 1 == nbuf) ? (bph ^= 1u, 0) : b + 1) {
       unsigned char* bb = buf_base + b * rowbuf_bytes(cap);
@@ -1455,6 +1576,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       const int rows = nrec * P;
       mbar_wait(&metafull_bar[b], bph);  // buffer b holds tile it's row metadata
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(11 + 3 * it);
+      if (GRAD && it >= nbuf) grad_pass(tile - (int64_t)nbuf * gridDim.x, sm, grad_of(b));
       mbar_wait(&full_bar[s], sph);
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
@@ -1483,6 +1605,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
             const int row = rowq[q];
             if (!live[q] || row >= rows) continue;
             const bool need = mt.need[(int)(((float)row + 0.5f) * inv_m)] != 0;
+            if (GRAD) grad_of(b).tok[row] = mt.tok[row];
             float xt = 0.0f;
             if (need) {
               const int tok = mt.tok[row];
@@ -1503,6 +1626,14 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         mbar_arrive(&empty_bar[s]);    // stage s fully read by this warp
         mbar_arrive(&rowfull_bar[b]);  // my rows' results are in buffer b
         if (cwarp == 0 && it < 3) tl_mark(13 + 3 * it);
+      }
+    }
+    if (GRAD) {  // the last nbuf tiles' gradient passes (their buffers are not reused)
+      for (int li = it > nbuf ? it - nbuf : 0; li < it; ++li) {  // local tile index
+        const int bi = li % nbuf;
+        unsigned char* bb = buf_base + bi * rowbuf_bytes(cap);
+        mbar_wait(&metafull_bar[bi], (uint32_t)((li / nbuf + 1) & 1));  // its unit phase is done
+        grad_pass(blockIdx.x + (int64_t)li * gridDim.x, carve_rows(bb, cap), grad_of(bi));
       }
     }
   } else {
@@ -1581,12 +1712,20 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       }
       if (probe && it == 0) tl_mark(2);
       if (probe && it == BW) tl_mark(29);
-      unit_phase_smem<MODE>(a, k, acc, sm, mt, cr0, cn, lane, outs_of(a));
+      if constexpr (GRAD) {
+        const GradSmem gs = grad_of(b);
+        unit_phase_smem<MODE>(a, k, acc, sm, mt, cr0, cn, lane, outs_of(a), gs.klp, gs.kent);
+      } else {
+        unit_phase_smem<MODE>(a, k, acc, sm, mt, cr0, cn, lane, outs_of(a));
+      }
       __syncwarp();
       if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
       if (probe && it == BW) tl_mark(30);
       if (rtile < a.n_tiles) {
         row_meta_store<MODE, FUSED>(a, rn, lane, rr, mt, a.pdl != 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&metafull_bar[b]);
+      } else if (GRAD) {  // no next user: the arrival only releases the tile's gradient pass
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
@@ -1663,13 +1802,16 @@ static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, ui
   if (rec_per_tile * a.C * a.M > max_rows) rec_per_tile = max_rows / (a.C * a.M);
   tile_bytes = (uint32_t)(rec_per_tile * rec);
   const int cap = (rec_per_tile * a.C * a.M + 7) & ~7;
-  const size_t buf = rowbuf_bytes(cap);
-  // up to 3 stages in flight, then as many row buffers (multiples of 4) as fit
+  const bool grad = a.dlogits != nullptr;
+  const size_t buf = rowbuf_bytes(cap) + (grad ? (size_t)cap * 12 : 0);  // + GradSmem
+  // up to 3 stages in flight, then as many row buffers (multiples of 4) as fit; the fused
+  // gradient keeps the ring at 4 so a tile's re-read (4 tiles later) still hits L2
   for (nstage = 3; nstage >= 2; --nstage) {
     const size_t used = (size_t)nstage * tile_bytes + 1024;
     if (used >= kSmemBudget) continue;
     int nb = (int)((kSmemBudget - used) / buf) & ~3;
     if (nb > max_row_bufs()) nb = max_row_bufs();
+    if (grad && nb > kRowBufs) nb = kRowBufs;
     if (nb >= kRowBufs) {
       a.nbuf = nb;
       a.rows_cap = cap;
@@ -1679,12 +1821,13 @@ static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, ui
   return false;
 }
 
-template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW = kBufWarps>
+template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW = kBufWarps, bool GRAD = false>
 static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
-  auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED, BW>;
+  auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED, BW, GRAD>;
   if (a.nbuf % BW) a.nbuf -= a.nbuf % BW;
   a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
-  const size_t smem = (size_t)nstage * tile_bytes + (size_t)a.nbuf * rowbuf_bytes(a.rows_cap);
+  const size_t smem = (size_t)nstage * tile_bytes + (size_t)a.nbuf * rowbuf_bytes(a.rows_cap) +
+                      (GRAD ? (size_t)a.nbuf * a.rows_cap * 12 : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t grid = device_sms();
@@ -1723,6 +1866,9 @@ static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int ns
     const char* env = getenv("CKRL_TMA_VARIANT");
     g_tma_variant = env ? atoi(env) : 4;
   }
+  if constexpr (!FUSED && MODE != MODE_STATS)
+    if (a.dlogits)  // fused softmax-backward seam (row f1)
+      return launch_tma_v<MODE, LT, 14, 1, FUSED, kBufWarps, true>(a, s, grid_out, nstage, tile_bytes);
   switch (g_tma_variant) {
     // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
     case 3: return launch_tma_v<MODE, LT, 8, 2, FUSED>(a, s, grid_out, nstage, tile_bytes);
@@ -1745,15 +1891,21 @@ static cudaError_t launch_mode(LossArgs& a, cudaStream_t s, int* g) {
   int rpt, nstage;
   uint32_t tile_bytes;
   const uintptr_t align = reinterpret_cast<uintptr_t>(a.logits) & 15;
-  if (fast && !g_force_direct && align == 0 && tma_plan(a, dbytes, rpt, nstage, tile_bytes)) {
+  const uintptr_t galign = reinterpret_cast<uintptr_t>(a.dlogits) & 15;
+  if (fast && !g_force_direct && align == 0 && galign == 0 && tma_plan(a, dbytes, rpt, nstage, tile_bytes)) {
     a.rec_per_tile = rpt;
     return a.logits_bf16 ? launch_tma<MODE, __nv_bfloat16, false>(a, s, g, nstage, tile_bytes)
                          : launch_tma<MODE, float, false>(a, s, g, nstage, tile_bytes);
   }
-  if (a.logits_bf16)
-    return fast ? launch_direct<MODE, __nv_bfloat16, true>(a, s, g)
-                : launch_direct<MODE, __nv_bfloat16, false>(a, s, g);
-  return fast ? launch_direct<MODE, float, true>(a, s, g) : launch_direct<MODE, float, false>(a, s, g);
+  cudaError_t e = a.logits_bf16 ? (fast ? launch_direct<MODE, __nv_bfloat16, true>(a, s, g)
+                                        : launch_direct<MODE, __nv_bfloat16, false>(a, s, g))
+                                : (fast ? launch_direct<MODE, float, true>(a, s, g)
+                                        : launch_direct<MODE, float, false>(a, s, g));
+  if (e != cudaSuccess || !a.dlogits || MODE == MODE_STATS) return e;
+  // no fused path for this shape: the standalone seam kernel over the loss's coefficients
+  if (!a.coeff_lp) return cudaErrorInvalidValue;
+  return launch_logits_grad(a.logits, a.logits_bf16, a.tokens, a.tok_i32, a.coeff_lp, a.coeff_ent,
+                            a.n_rec * a.C * a.M, a.V, a.dlogits, a.logits_bf16, nullptr, s);
 }
 
 // The fused single-GPU PPO step (assembly + loss in one persistent launch). Returns

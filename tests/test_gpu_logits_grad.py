@@ -139,3 +139,55 @@ def test_logits_grad_non_finite_coefficient_is_nonfinite():
     out = policy.logits_grad(logits, tokens, torch.zeros(64, device="cuda"))
     assert torch.count_nonzero(out) == 0
     assert policy.logits_grad(logits[:0], tokens[:0], klp[:0]).numel() == 0
+
+
+@pytest.mark.parametrize("cfg_name,envs,dtype", [("cfg3", 32, torch.float32), ("cfg1", 16, torch.float32),
+                                                 ("cfg3", 16, torch.bfloat16)])
+def test_fused_dlogits_in_the_ppo_step(cfg_name, envs, dtype, oracle):
+    """The seam fused into the loss launch (LossOutputs.dlogits): same rows as the oracle on
+    the step's own coefficients."""
+    cfg = synth.SynthConfig(**{**synth.CONFIGS[cfg_name].__dict__, "num_envs": envs})
+    d = synth.episodes_numpy(cfg)
+    logits, tokens, old = synth.token_tensors(cfg, dtype=dtype)
+    d["tokens"], d["old_logprob"] = tokens.cpu().numpy(), old.cpu().numpy()
+    a, l, v = synth.SPECS[cfg_name]
+    ro = RolloutBuffer.from_arrays(d, d["boot_scalar"] if a == 0 else d["boot_vector0"], cfg.vocab)
+    nv = d["new_value_scalar"] if v == 0 else d["new_value_vector"]
+    pol = PolicyOutputs(logits, torch.tensor(nv, dtype=torch.float32, device="cuda"))
+    step = optim.PpoStep(ro, GaeParams(0.99, 0.95), GranularitySpec(Level(a), Level(l), Level(v)),
+                         PpoParams(0.2, 0.5, 0.01, True))
+    step.outputs.dlogits = torch.full_like(logits, float("nan"))
+    step._oc = step.outputs.c()
+    step(ro, pol)
+    torch.cuda.synchronize()
+    klp, kent = step.outputs.coeff_logprob, step.outputs.coeff_entropy
+    st, want = oracle.logits_grad(logits.double().cpu().numpy(), tokens.cpu().numpy(),
+                                  f32(klp.cpu().numpy()), f32(kent.cpu().numpy()))
+    assert st == 0
+    got = step.outputs.dlogits.float().cpu().numpy()
+    assert np.isfinite(got).all(), "every row written"
+    assert_rows_close(got, want, rel=TOL if dtype == torch.float32 else 1e-2, what=f"fused {cfg_name}")
+
+
+def test_fused_dlogits_in_the_grpo_step(oracle):
+    from paper_2510_06710_b200.core import EpisodeTable, GrpoAssemblyOptions, GrpoParams
+    cfg = synth.SynthConfig(**{**synth.CONFIGS["cfg4"].__dict__, "num_envs": 16, "num_chunks": 8,
+                               "max_episode_steps": 64})
+    d = synth.episodes_numpy(cfg)
+    logits, tokens, old = synth.token_tensors(cfg)
+    d["tokens"], d["old_logprob"] = tokens.cpu().numpy(), old.cpu().numpy()
+    a, l, v = synth.SPECS["cfg4"]
+    ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], cfg.vocab)
+    step = optim.GrpoStep(ro, GrpoAssemblyOptions(GranularitySpec(Level(a), Level(l), Level(v)), apply_filter=False),
+                          GrpoParams(0.2))
+    step.outputs.dlogits = torch.full_like(logits, float("nan"))
+    step._oc = step.outputs.c()
+    step(ro, EpisodeTable.from_arrays(d), PolicyOutputs(logits))
+    torch.cuda.synchronize()
+    klp = step.outputs.coeff_logprob
+    st, want = oracle.logits_grad(logits.double().cpu().numpy(), tokens.cpu().numpy(),
+                                  f32(klp.cpu().numpy()), np.zeros(klp.numel()))
+    assert st == 0
+    got = step.outputs.dlogits.cpu().numpy()
+    assert np.isfinite(got).all()
+    assert_rows_close(got, want, what="fused grpo")
