@@ -46,8 +46,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
-    p.add_argument("--grad", action="store_true",
-                   help="extend the step with the softmax-backward seam (ckrl_logits_grad -> dlogits)")
+    p.add_argument("--grad", nargs="?", const="fused", default=None, choices=["fused", "separate"],
+                   help="extend the step with the softmax-backward seam (dlogits): fused into the loss "
+                        "launch (default) or the standalone ckrl_logits_grad kernel after it")
     return p.parse_args()
 
 
@@ -238,7 +239,7 @@ def workload(args, cfg, world):
             "granularity": {"advantage": lv[a], "logprob": lv[l], "value": lv[v]},
             "global_envs": cfg.num_envs * world, "parallelism": f"env-sharded x{world}",
             "logits_dtype": args.dtype,
-            **({"step_includes": "assemble + loss + logits_grad (dlogits)"} if getattr(args, "grad", False) else {})}
+            **({"step_includes": f"assemble + loss + dlogits ({args.grad})"} if getattr(args, "grad", None) else {})}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -316,7 +317,10 @@ def main():
         run0 = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
         launches_per_step = 3
     run = run0
-    if args.grad:  # + dlogits for the model backward (policy_net.cpp:431-456)
+    if args.grad == "fused":  # dlogits written by the loss launch itself (LossOutputs.dlogits)
+        step.outputs.dlogits = torch.empty_like(reps[0][1].logits)
+        step._oc = step.outputs.c()
+    if args.grad == "separate":  # + dlogits for the model backward (policy_net.cpp:431-456)
         from paper_2510_06710_b200 import policy as ckpolicy
         dlogits = torch.empty_like(reps[0][1].logits)
         gstatus = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -415,6 +419,8 @@ def main():
     ktimes = sorted(e0.elapsed_time(e1) for e0, e1 in kms[3:])
     kernel_ms = ktimes[len(ktimes) // 2]  # median launch
     kbytes = loss_kernel_bytes(cfg, dbytes, (a, l, v), cfg.algo)
+    if args.grad == "fused":  # the same launch also writes V * s_out bytes of dlogits per position
+        kbytes += env_steps(cfg) * cfg.tokens_per_action * cfg.vocab * dbytes
     peak, peak_kind = peaks()
     achieved = kbytes / (kernel_ms * 1e-3) / 1e9
     traffic = None
@@ -424,7 +430,12 @@ def main():
             traffic = json.load(f).get(f"{args.config}_{args.dtype}")
 
     grad_line = None
-    if args.grad:
+    if args.grad == "fused":  # the roofline below is the fused launch (loss + dlogits)
+        grad_line = {"kernel": "tma_tile_kernel<GRAD> (loss + dlogits in one launch)", "mode": "fused",
+                     "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": kbytes,
+                     "achieved": kbytes / (kernel_ms * 1e-3) / 1e9, "unit": "GB/s",
+                     "frac": kbytes / (kernel_ms * 1e-3) / 1e9 / peaks()[0]}
+    if args.grad == "separate":
         gev = []
         for i in range(min(K, 50)):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -468,7 +479,8 @@ def main():
                    "cuda_graph": graph is not None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "tile_kernel (fused token + loss)", "kernel_ms": kernel_ms,
+                     "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),
+                     "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
                      "step_frac": (kbytes / (ms * 1e-3) / 1e9) / peak},
         "cpu_baseline": cpu,

@@ -11,7 +11,7 @@ for c in cfg1 cfg2 cfg3 cfg4; do
   timeout 300 python bench.py --config $c --dtype bf16 --steps 100 --warmup 5 --no-cpu-baseline >> $O 2>/dev/null
 done
 for c in cfg3 cfg4; do
-  timeout 300 python bench.py --config $c --grad --steps 60 --warmup 5 --no-cpu-baseline >> $O 2>/dev/null
+  timeout 300 python bench.py --config $c --grad fused --steps 60 --warmup 5 --no-cpu-baseline >> $O 2>/dev/null
 done
 timeout 300 python bench.py --config adam --steps 20 >> $O 2>/dev/null
 timeout 600 python bench.py --config cfg5 --steps 10 --warmup 3 >> $O 2>/dev/null
