@@ -14,6 +14,7 @@ struct Unit {
   int32_t uid;   // segment key (episode id); units of one segment are contiguous
   double r, v, boot;
   int counted_slots;
+  int first;     // chunk level: first valid slot of the record (its counted run starts here)
 };
 
 // ---------------------------------------------------------------------------------
@@ -274,6 +275,12 @@ __device__ __forceinline__ GaeSums serial_gae(const Acc& acc, int n_items, doubl
 }
 
 // ---- accessors ------------------------------------------------------------------
+// 8-slot records can be read with vector loads when the arrays are 16-byte aligned (the
+// record offset, 8 slots, keeps every array's records 16-byte aligned).
+__device__ __forceinline__ bool vec_ok(const ckrl_rollout& ro) {
+  return ((reinterpret_cast<uintptr_t>(ro.flags) & 7) | (reinterpret_cast<uintptr_t>(ro.episode_id) & 15) |
+          (reinterpret_cast<uintptr_t>(ro.reward) & 15) | (reinterpret_cast<uintptr_t>(ro.bootstrap) & 15)) == 0;
+}
 struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   const ckrl_rollout ro;
   int e;
@@ -299,20 +306,43 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
       uint8_t f[kC];
       int32_t id[kC];
       float rw[kC], bt[kC];
+      if (C == kC && vec_ok(ro)) {
+        // a record's 8 slots are contiguous in every array: 7 vector loads instead of 32
+        const uint2 fw = __ldg(reinterpret_cast<const uint2*>(ro.flags + s0));
+        const int4 i0 = __ldg(reinterpret_cast<const int4*>(ro.episode_id + s0));
+        const int4 i1 = __ldg(reinterpret_cast<const int4*>(ro.episode_id + s0) + 1);
+        const float4 r0 = __ldg(reinterpret_cast<const float4*>(ro.reward + s0));
+        const float4 r1 = __ldg(reinterpret_cast<const float4*>(ro.reward + s0) + 1);
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(ro.bootstrap + s0));
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(ro.bootstrap + s0) + 1);
 #pragma unroll
-      for (int j = 0; j < kC; ++j)
-        if (j < C) {
-          f[j] = ro.flags[s0 + j];
-          id[j] = ro.episode_id[s0 + j];
-          rw[j] = ro.reward[s0 + j];
-          bt[j] = ro.bootstrap[s0 + j];
+        for (int j = 0; j < 4; ++j) {
+          f[j] = (uint8_t)(fw.x >> (8 * j));
+          f[j + 4] = (uint8_t)(fw.y >> (8 * j));
         }
+        id[0] = i0.x; id[1] = i0.y; id[2] = i0.z; id[3] = i0.w;
+        id[4] = i1.x; id[5] = i1.y; id[6] = i1.z; id[7] = i1.w;
+        rw[0] = r0.x; rw[1] = r0.y; rw[2] = r0.z; rw[3] = r0.w;
+        rw[4] = r1.x; rw[5] = r1.y; rw[6] = r1.z; rw[7] = r1.w;
+        bt[0] = b0.x; bt[1] = b0.y; bt[2] = b0.z; bt[3] = b0.w;
+        bt[4] = b1.x; bt[5] = b1.y; bt[6] = b1.z; bt[7] = b1.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kC; ++j)
+          if (j < C) {
+            f[j] = ro.flags[s0 + j];
+            id[j] = ro.episode_id[s0 + j];
+            rw[j] = ro.reward[s0 + j];
+            bt[j] = ro.bootstrap[s0 + j];
+          }
+      }
       int first = -1;
 #pragma unroll
       for (int j = kC - 1; j >= 0; --j)
         if (j < C && (f[j] & CKRL_FLAG_VALID)) first = j;
       if (first < 0) return u;  // fully frozen chunk
       u.is_unit = true;
+      u.first = first;
 #pragma unroll
       for (int j = 0; j < kC; ++j)
         if (j == first) u.uid = id[j];
@@ -339,6 +369,7 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
       }
     if (first < 0) return u;
     u.is_unit = true;
+    u.first = first;
     u.uid = ro.episode_id[s0 + first];
     int last = first;
     for (int j = first; j < C; ++j) {
@@ -359,12 +390,15 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
     adv[rec] = (float)a;
     ret[rec] = (float)R;
     // counted = the leading episode's contiguous valid prefix from the first valid slot
-    int first = -1;
-    for (int j = 0; j < C; ++j) {
-      bool v = ro.flags[rec * C + j] & CKRL_FLAG_VALID;
-      if (first < 0 && v) first = j;
-      counted[rec * C + j] = (first >= 0 && j < first + u.counted_slots) ? 1 : 0;
+    if (C == 8 && (reinterpret_cast<uintptr_t>(counted) & 7) == 0) {
+      uint64_t w = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        w |= (uint64_t)(j >= u.first && j < u.first + u.counted_slots ? 1 : 0) << (8 * j);
+      *reinterpret_cast<uint64_t*>(counted + rec * 8) = w;
+      return;
     }
+    for (int j = 0; j < C; ++j) counted[rec * C + j] = (j >= u.first && j < u.first + u.counted_slots) ? 1 : 0;
   }
   __device__ void store_empty(int t) const {
     const int C = ro.chunk_len;
