@@ -564,16 +564,18 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   __syncthreads();
   if (tid == 0) tl_mark(27);
   if (!*s_last) return;
+  if (tid == 0) g_timeline[28] = gtimer();  // probe: last CTA after its ticket
   // Last CTA: every thread sums a fixed strided subset of the partials (loads in
   // parallel), then a fixed-shape tree over warps -> deterministic for a given grid.
   {
     double x[RAW_COUNT];
 #pragma unroll
     for (int i = 0; i < RAW_COUNT; ++i) x[i] = 0.0;
-    const volatile double* vp = parts;
+    // plain L2 loads (the acquire above ordered every CTA's released partials before them;
+    // volatile loads would serialise the 8 per thread)
     for (unsigned b = tid; b < gridDim.x; b += nthr_total)
 #pragma unroll
-      for (int i = 0; i < RAW_COUNT; ++i) x[i] += vp[b * RAW_COUNT + i];
+      for (int i = 0; i < RAW_COUNT; ++i) x[i] += __ldcg(parts + b * RAW_COUNT + i);
 #pragma unroll
     for (int i = 0; i < RAW_COUNT; ++i) {
       double y = x[i];
@@ -582,6 +584,7 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
       x[i] = y;
     }
     __syncthreads();
+    if (tid == 0) g_timeline[29] = gtimer();  // probe: partials loaded and warp-reduced
     if (lane == 0)
 #pragma unroll
       for (int i = 0; i < RAW_COUNT; ++i) s_red[warp][i] = x[i];
@@ -594,8 +597,10 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   }
   __syncthreads();
   if (tid == 0) {
+    g_timeline[30] = gtimer();  // probe: raw sums written
     tickets[TICKET_LOSS] = 0;
     if (a.finalize) finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
+    g_timeline[31] = gtimer();  // probe: finalised
   }
 }
 

@@ -33,6 +33,11 @@ for name in sys.argv[1:] or ["cfg3"]:
         q = lambda x: "min %.1f p50 %.1f p90 %.1f max %.1f" % (x.min(), np.median(x), np.percentile(x, 90), x.max())
         print(f"{name} {mode}: start [{q(s)}] done [{q(dn)}] exit [{q(ex)}] us")
         print("   slowest CTAs:", np.argsort(-dn)[:8].tolist(), "done-start spread", q(dn - s))
+        tl = (C.c_uint64 * 32)()
+        _lib.check(_lib.lib().ckrl_debug_timeline(tl, 32))
+        vals = tuple((int(tl[i]) - int(t[1].max())) / 1e3 for i in (28, 29, 30, 31)) + (
+            (int(t[2].max()) - int(t[1].max())) / 1e3,)
+        print("   last CTA (us after the latest done): ticket %.2f loaded %.2f written %.2f finalised %.2f; exit max %.2f" % vals)
 
 # overlapped step: where and when the assembly CTAs ran vs the loss CTAs' start
 if os.environ.get("ASM_PROBE", "0") == "1" and hasattr(_lib.lib(), "ckrl_debug_asm_times"):
