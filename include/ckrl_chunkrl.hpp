@@ -38,6 +38,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "ckrl.h"
@@ -144,6 +145,11 @@ struct TrajectorySlab {
   }
 };
 
+/// dump_slab (core/types.cpp:9-28): the trajectories.txt text of a slab (through
+/// ckrl_dump_slab). Episode uids must be the reference's env << 32 | k (vec_env.cpp:14-16);
+/// every env must hold the same number of records.
+std::string dump_slab(const TrajectorySlab& slab);
+
 // ---- core/granularity.hpp -------------------------------------------------------------------
 enum class Level { Chunk, Action, Token };
 const char* level_name(Level level);
@@ -161,6 +167,23 @@ void validate_granularity(const GranularitySpec& spec);
 
 namespace policy {
 enum class ValueHeadKind { Scalar, Vector };
+
+/// policy::PolicyDescriptor (policy_net.hpp:15-26).
+struct PolicyDescriptor {
+  int obs_dim = 1;
+  int hidden = 32;
+  int trunk_layers = 2;
+  int value_hidden = 32;
+  int vocab = 4;
+  int C = 4;
+  int M = 2;
+  bool operator==(const PolicyDescriptor&) const = default;
+};
+/// save_checkpoint / load_checkpoint (policy/checkpoint.cpp:37-83) over a descriptor and its
+/// flat f64 parameters (the layout of policy_net.cpp:107-152); the same CKRL v1 bytes, and the
+/// reference's Error cases.
+void save_checkpoint(const PolicyDescriptor& desc, std::span<const double> params, const std::string& path);
+std::pair<PolicyDescriptor, std::vector<double>> load_checkpoint(const std::string& path);
 
 /// The per-position logits gradient PolicyNet::accumulate_chunk_gradient forms before its
 /// outer_add / trunk backward (policy/policy_net.cpp:431-456), on the device: logits rows

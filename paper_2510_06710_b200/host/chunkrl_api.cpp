@@ -976,4 +976,59 @@ double Adam::step(std::span<double> params, std::span<double> grad) {
 
 }  // namespace optim
 
+std::string dump_slab(const TrajectorySlab& slab) {
+  const int E = slab.num_envs, C = slab.chunk_length, M = slab.tokens_per_action;
+  const int Tc = E > 0 ? static_cast<int>(slab.records[0].size()) : 0;
+  for (const auto& r : slab.records)
+    if (static_cast<int>(r.size()) != Tc) throw LengthMismatch("dump_slab: ragged records");
+  const std::size_t S = static_cast<std::size_t>(E) * Tc * C;
+  std::vector<int32_t> tok(S * M), ids(S);
+  std::vector<double> rw(S);
+  std::vector<uint8_t> fl(S);
+  for (int e = 0; e < E; ++e)
+    for (int t = 0; t < Tc; ++t) {
+      const StepRecord& rec = slab.records[static_cast<std::size_t>(e)][static_cast<std::size_t>(t)];
+      for (int j = 0; j < C; ++j) {
+        const std::size_t s = (static_cast<std::size_t>(e) * Tc + t) * C + j;
+        const std::size_t jj = static_cast<std::size_t>(j);
+        for (int m = 0; m < M; ++m) tok[s * M + m] = rec.chunk.actions[jj].tokens[static_cast<std::size_t>(m)];
+        rw[s] = rec.rewards[jj];
+        fl[s] = static_cast<uint8_t>((rec.terminated[jj] ? CKRL_FLAG_TERMINATED : 0) |
+                                     (rec.truncated[jj] ? CKRL_FLAG_TRUNCATED : 0) |
+                                     (rec.valid[jj] ? CKRL_FLAG_VALID : 0));
+        const std::int64_t uid = rec.episode_uid[jj];
+        ids[s] = uid < 0 ? -1 : static_cast<int32_t>(uid & 0xffffffff);
+      }
+    }
+  std::size_t n = 0;
+  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(), nullptr,
+                                0, &n));
+  std::string out(n, '\0');
+  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(),
+                                out.data(), n, &n));
+  return out;
+}
+
+namespace policy {
+
+void save_checkpoint(const PolicyDescriptor& d, std::span<const double> params, const std::string& path) {
+  const ckrl_policy_desc cd{d.obs_dim, d.hidden, d.trunk_layers, d.value_hidden, d.vocab, d.C, d.M};
+  if (ckrl_policy_num_params(&cd) != static_cast<int64_t>(params.size()))
+    throw LengthMismatch("checkpoint parameter count mismatch");
+  throw_if_error(ckrl_save_checkpoint(&cd, params.data(), path.c_str()));
+}
+
+std::pair<PolicyDescriptor, std::vector<double>> load_checkpoint(const std::string& path) {
+  ckrl_policy_desc cd{};
+  int64_t n = 0;
+  throw_if_error(ckrl_load_checkpoint(path.c_str(), &cd, nullptr, 0, &n));
+  std::vector<double> p(static_cast<std::size_t>(n));
+  throw_if_error(ckrl_load_checkpoint(path.c_str(), &cd, p.data(), n, &n));
+  return {PolicyDescriptor{cd.obs_dim, cd.hidden, cd.trunk_layers, cd.value_hidden, cd.vocab, cd.chunk_len,
+                           cd.tokens_per_action},
+          std::move(p)};
+}
+
+}  // namespace policy
+
 }  // namespace ckrl::chunkrl

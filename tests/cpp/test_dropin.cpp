@@ -714,6 +714,45 @@ TEST_CASE("Adam gradient norm clipping") {
   CHECK_THROWS_AS(adam.step(theta, short_grad), LengthMismatch);
 }
 
+TEST_CASE("dump_slab and the CKRL checkpoint keep the reference's formats") {
+  // core/types.cpp:9-28 on a 1-env, 2-record, C = 2 slab (uid = env << 32 | k)
+  TrajectorySlab slab;
+  slab.num_envs = 1;
+  slab.chunk_length = 2;
+  slab.tokens_per_action = 2;
+  slab.records.resize(1);
+  for (int t = 0; t < 2; ++t) {
+    StepRecord r;
+    r.chunk.actions.resize(2);
+    for (int j = 0; j < 2; ++j) r.chunk.actions[static_cast<std::size_t>(j)].tokens = {t + j, 3};
+    r.rewards = {0.1, t == 1 ? 1.1 : 0.0};
+    r.terminated = {false, t == 1};
+    r.truncated = {false, false};
+    r.valid = {true, true};
+    r.episode_uid = {0, 0};
+    slab.records[0].push_back(r);
+  }
+  const std::string want =
+      "# env_id episode_uid step tokens[2] reward terminated truncated valid\n"
+      "0 0 0 0 3 0.10000000000000001 0 0 1\n"
+      "0 0 1 1 3 0 0 0 1\n"
+      "0 0 2 1 3 0.10000000000000001 0 0 1\n"
+      "0 0 3 2 3 1.1000000000000001 1 0 1\n";
+  CHECK(dump_slab(slab) == want);
+  // checkpoint round trip; a count mismatch is the reference's Error
+  policy::PolicyDescriptor d{6, 4, 1, 3, 5, 2, 2};
+  const ckrl_policy_desc cd{6, 4, 1, 3, 5, 2, 2};
+  std::vector<double> p(static_cast<std::size_t>(ckrl_policy_num_params(&cd)));
+  for (std::size_t i = 0; i < p.size(); ++i) p[i] = 0.25 * static_cast<double>(i) - 3.0;
+  const std::string path = "/tmp/ckrl_dropin_test.ckrl";
+  policy::save_checkpoint(d, p, path);
+  auto [d2, p2] = policy::load_checkpoint(path);
+  CHECK(d2 == d);
+  CHECK(p2 == p);
+  CHECK_THROWS_AS(policy::save_checkpoint(d, std::vector<double>(3, 0.0), path), LengthMismatch);
+  CHECK_THROWS_AS(policy::load_checkpoint("/tmp/ckrl_dropin_missing.ckrl"), Error);
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
     for (const auto& c : cases()) std::printf("%s\n", c.name);
@@ -721,6 +760,7 @@ int main(int argc, char** argv) {
   }
   int failed_cases = 0;
   for (const auto& c : cases()) {
+    if (argc > 1 && std::strstr(c.name, argv[1]) == nullptr) continue;  // optional name filter
     const int before = g_failures;
     try {
       c.fn();

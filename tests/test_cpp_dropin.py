@@ -33,3 +33,13 @@ def test_cpp_dropin_cases():
     print(r.stdout)
     print(r.stderr)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_cpp_dropin_host_formats():
+    """CPU: the host-only cases (trajectories dump, CKRL checkpoint) run without a device."""
+    if not os.path.exists(os.path.join(ROOT, "paper_2510_06710_b200", "libckrl.so")):
+        pytest.skip("libckrl.so not built")
+    _build()
+    r = subprocess.run([BIN, "dump_slab"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "[ ok ] dump_slab" in r.stdout
