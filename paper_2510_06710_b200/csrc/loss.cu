@@ -789,75 +789,123 @@ __device__ __forceinline__ void row_fast_smem(const LT* row, int l8, float& s_ou
   c_out = c;
 }
 
+// Packed f32x2 arithmetic (FFMA2 / FADD2: two lanes of fp32 per issue slot, same rounding as
+// the scalar ops) and three-input max (FMNMX3); bf16 rows take their max on the packed words
+// (HMNMX2: max is exact, so the result equals the fp32 max of the widened values).
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 // R independent row groups per warp in flight (ILP across the shuffle / MUFU latencies).
+// Per lane and row: 32 logits as 16 (even, odd) pairs; the even / odd elements accumulate
+// into the low / high halves of the packed sums (two partial sums, added at the end).
 template <typename LT, int R>
 __device__ __forceinline__ void rows_fast_smem(const LT* const* rowp, int l8, float* s_out,
                                                float* t_out, float* c_out) {
-  float x[R][32];
+  uint64_t x[R][16];
+  float m[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if constexpr (sizeof(LT) == 4) {
       const float4* p = reinterpret_cast<const float4*>(rowp[r]);
+      float f[32];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float4 v = p[l8 + 8 * i];
-        x[r][4 * i + 0] = v.x;
-        x[r][4 * i + 1] = v.y;
-        x[r][4 * i + 2] = v.z;
-        x[r][4 * i + 3] = v.w;
+        const float4 v = p[l8 + 8 * i];
+        f[4 * i + 0] = v.x;
+        f[4 * i + 1] = v.y;
+        f[4 * i + 2] = v.z;
+        f[4 * i + 3] = v.w;
+        x[r][2 * i] = f2pack(v.x, v.y);
+        x[r][2 * i + 1] = f2pack(v.z, v.w);
       }
+      float mx[11];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) mx[i] = fmax3(f[i], f[i + 10], f[i + 20]);
+      mx[10] = fmaxf(f[30], f[31]);
+      const float a0 = fmax3(mx[0], mx[1], mx[2]), a1 = fmax3(mx[3], mx[4], mx[5]);
+      const float a2 = fmax3(mx[6], mx[7], mx[8]), a3 = fmaxf(mx[9], mx[10]);
+      m[r] = fmaxf(fmax3(a0, a1, a2), a3);
     } else {
       const uint4* p = reinterpret_cast<const uint4*>(rowp[r]);
+      uint32_t w[16];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        uint4 v = p[l8 + 8 * i];
-        x[r][8 * i + 0] = bf16_lo(v.x);
-        x[r][8 * i + 1] = bf16_hi(v.x);
-        x[r][8 * i + 2] = bf16_lo(v.y);
-        x[r][8 * i + 3] = bf16_hi(v.y);
-        x[r][8 * i + 4] = bf16_lo(v.z);
-        x[r][8 * i + 5] = bf16_hi(v.z);
-        x[r][8 * i + 6] = bf16_lo(v.w);
-        x[r][8 * i + 7] = bf16_hi(v.w);
+        const uint4 v = p[l8 + 8 * i];
+        w[4 * i + 0] = v.x;
+        w[4 * i + 1] = v.y;
+        w[4 * i + 2] = v.z;
+        w[4 * i + 3] = v.w;
       }
+      uint32_t mw[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mw[i] = bmax2(w[i], w[i + 8]);
+#pragma unroll
+      for (int k = 4; k >= 1; k >>= 1)
+#pragma unroll
+        for (int i = 0; i < k; ++i) mw[i] = bmax2(mw[i], mw[i + k]);
+      m[r] = fmaxf(bf16_lo(mw[0]), bf16_hi(mw[0]));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[r][i] = f2pack(bf16_lo(w[i]), bf16_hi(w[i]));
     }
-  }
-  float m[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    float mx[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) mx[i] = fmaxf(x[r][i], x[r][i + 16]);
-#pragma unroll
-    for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-      for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
-    m[r] = mx[0];
   }
 #pragma unroll
   for (int o = 1; o <= 4; o <<= 1)
 #pragma unroll
     for (int r = 0; r < R; ++r) m[r] = fmaxf(m[r], __shfl_xor_sync(0xffffffffu, m[r], o));
-  float sa[R][2], ta[R][2], c[R];
+  const uint64_t l2e = f2pack(kL2E, kL2E);
+  uint64_t sa[R], ta[R], nc[R];
+  float c[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     c[r] = m[r] * kL2E;
-    sa[r][0] = sa[r][1] = ta[r][0] = ta[r][1] = 0.f;
+    nc[r] = f2pack(-c[r], -c[r]);
+    sa[r] = ta[r] = 0ull;
   }
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < 16; ++i)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const float y = fmaf(x[r][i], kL2E, -c[r]);
-      const float e = ex2(y);
-      sa[r][i & 1] += e;
-      ta[r][i & 1] = fmaf(e, y, ta[r][i & 1]);
+      const uint64_t y = ffma2(x[r][i], l2e, nc[r]);
+      float y0, y1;
+      f2unpack(y, y0, y1);
+      const uint64_t e = f2pack(ex2(y0), ex2(y1));
+      sa[r] = fadd2(sa[r], e);
+      ta[r] = ffma2(e, y, ta[r]);
     }
   float sv[R], tv[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    sv[r] = sa[r][0] + sa[r][1];
-    tv[r] = ta[r][0] + ta[r][1];
+    float a0, a1;
+    f2unpack(sa[r], a0, a1);
+    sv[r] = a0 + a1;
+    f2unpack(ta[r], a0, a1);
+    tv[r] = a0 + a1;
   }
 #pragma unroll
   for (int o = 1; o <= 4; o <<= 1)
