@@ -84,8 +84,14 @@ def main():
                 traffic[f"{m.group(1)}_{m.group(2)}"] = rw
             if name.startswith("full_grad_"):
                 traffic[name[len("full_"):]] = rw
-    with open(os.path.join(HERE, f"ncu_{tag}.md"), "w") as f:
-        f.write("\n".join(md) + "\n")
+    out = os.path.join(HERE, f"ncu_{tag}.md")
+    keep = ""  # hand-written sections (from "## Fused") survive a regeneration
+    if os.path.exists(out):
+        old_md = open(out).read()
+        i = old_md.find("\n## Fused")
+        keep = old_md[i:] if i >= 0 else ""
+    with open(out, "w") as f:
+        f.write("\n".join(md) + "\n" + keep)
     tpath = os.path.join(HERE, "ncu_traffic.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
     old.update(traffic)
