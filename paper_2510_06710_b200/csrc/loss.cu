@@ -547,10 +547,12 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   if (tid == 0) tl_mark(25);
   double* parts = reinterpret_cast<double*>(a.ws + a.L.loss_partials);
   uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
-  if (tid < RAW_COUNT) {
-    double x = 0.0;
-    for (int w = 0; w < nwarps; ++w) x += s_red[w][tid];
-    parts[blockIdx.x * RAW_COUNT + tid] = x;
+  // warp i < RAW_COUNT sums quantity i over the CTA's warps (a shuffle tree, not a serial loop)
+  if (warp < RAW_COUNT) {
+    double x = lane < nwarps ? s_red[lane][warp] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) parts[blockIdx.x * RAW_COUNT + warp] = x;
   }
   __syncthreads();
   if (tid == 0) tl_mark(26);
@@ -565,41 +567,29 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   if (tid == 0) tl_mark(27);
   if (!*s_last) return;
   if (tid == 0) g_timeline[28] = gtimer();  // probe: last CTA after its ticket
-  // Last CTA: every thread sums a fixed strided subset of the partials (loads in
-  // parallel), then a fixed-shape tree over warps -> deterministic for a given grid.
-  {
-    double x[RAW_COUNT];
+  // Last CTA: warp i < RAW_COUNT sums quantity i over the CTA partials — each lane a fixed
+  // strided subset (its loads in flight together), then a shuffle tree: a fixed order for a
+  // given grid, so the sums are deterministic. Plain L2 loads: the acquire above ordered
+  // every CTA's released partials before them.
+  double* raw = reinterpret_cast<double*>(a.ws + a.L.loss_raw);
+  __shared__ double s_tot[RAW_COUNT];
+  if (warp < RAW_COUNT) {
+    double x = 0.0;
+#pragma unroll 8
+    for (unsigned b = lane; b < gridDim.x; b += 32) x += __ldcg(parts + b * RAW_COUNT + warp);
 #pragma unroll
-    for (int i = 0; i < RAW_COUNT; ++i) x[i] = 0.0;
-    // plain L2 loads (the acquire above ordered every CTA's released partials before them;
-    // volatile loads would serialise the 8 per thread)
-    for (unsigned b = tid; b < gridDim.x; b += nthr_total)
-#pragma unroll
-      for (int i = 0; i < RAW_COUNT; ++i) x[i] += __ldcg(parts + b * RAW_COUNT + i);
-#pragma unroll
-    for (int i = 0; i < RAW_COUNT; ++i) {
-      double y = x[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) y += __shfl_down_sync(0xffffffffu, y, o);
-      x[i] = y;
-    }
-    __syncthreads();
-    if (tid == 0) g_timeline[29] = gtimer();  // probe: partials loaded and warp-reduced
-    if (lane == 0)
-#pragma unroll
-      for (int i = 0; i < RAW_COUNT; ++i) s_red[warp][i] = x[i];
-    __syncthreads();
-    if (tid < RAW_COUNT) {
-      double y = 0.0;
-      for (int w = 0; w < nwarps; ++w) y += s_red[w][tid];
-      reinterpret_cast<double*>(a.ws + a.L.loss_raw)[tid] = y;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      s_tot[warp] = x;
+      raw[warp] = x;
     }
   }
+  if (tid == 0) g_timeline[29] = gtimer();  // probe: partials loaded and warp-reduced
   __syncthreads();
   if (tid == 0) {
     g_timeline[30] = gtimer();  // probe: raw sums written
     tickets[TICKET_LOSS] = 0;
-    if (a.finalize) finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
+    if (a.finalize) finalize_diag(a, k, s_tot, a.diag);
     g_timeline[31] = gtimer();  // probe: finalised
   }
 }
