@@ -552,7 +552,7 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
     double x = lane < nwarps ? s_red[lane][warp] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if (lane == 0) parts[blockIdx.x * RAW_COUNT + warp] = x;
+    if (lane == 0) parts[warp * kMaxLossCtas + blockIdx.x] = x;  // quantity-major: coalesced reads below
   }
   __syncthreads();
   if (tid == 0) tl_mark(26);
@@ -574,9 +574,18 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   double* raw = reinterpret_cast<double*>(a.ws + a.L.loss_raw);
   __shared__ double s_tot[RAW_COUNT];
   if (warp < RAW_COUNT) {
+    const double* q = parts + warp * kMaxLossCtas;
     double x = 0.0;
-#pragma unroll 8
-    for (unsigned b = lane; b < gridDim.x; b += 32) x += __ldcg(parts + b * RAW_COUNT + warp);
+    for (unsigned b0 = 0; b0 < gridDim.x; b0 += 32 * 8) {  // 8 loads in flight per lane
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned b = b0 + lane + 32 * j;
+        v[j] = b < gridDim.x ? __ldcg(q + b) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x += v[j];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
     if (lane == 0) {
