@@ -46,3 +46,9 @@ for rep in range(4):
     print(f"{name} rep{rep}: start p50 {np.median(st_):.1f} max {st_.max():.1f} | roles done p50 "
           f"{np.median(dn):.1f} max {dn.max():.1f} | exit p50 {np.median(ex):.1f} max {ex.max():.1f} | "
           f"last CTA ticket {last[0]:.1f} loaded {last[1]:.1f} synced {last[2]:.1f} final {last[3]:.1f} us")
+# start / roles-done by CTA index (does the late-start set sit at the top of the grid?)
+T = np.array(buf, dtype=np.int64).reshape(3, 1184)[:, :148]
+t0 = T[0].min()
+order = np.argsort(T[0])
+print("CTA ids by start time (first 10 / last 40):", order[:10].tolist(), order[-40:].tolist())
+print("start us by id block of 16:", [round(float(np.mean((T[0][i:i + 16] - t0) / 1e3)), 1) for i in range(0, 148, 16)])
