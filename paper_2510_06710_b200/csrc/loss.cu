@@ -1845,9 +1845,19 @@ static int max_row_bufs() {  // CKRL_NBUF caps the row-buffer count (A/B experim
   return n;
 }
 
+static size_t stage_target() {  // CKRL_STAGE_KB overrides the tile size (A/B experiments)
+  static size_t t = 0;
+  if (t == 0) {
+    const char* env = getenv("CKRL_STAGE_KB");
+    t = env ? (size_t)atoi(env) * 1024 : kStageTarget;
+    if (t == 0) t = kStageTarget;
+  }
+  return t;
+}
+
 static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, uint32_t& tile_bytes) {
   const size_t rec = (size_t)a.C * a.M * 256 * dbytes;
-  rec_per_tile = (int)(kStageTarget / rec);
+  rec_per_tile = (int)(stage_target() / rec);
   if (rec_per_tile < 1) rec_per_tile = 1;
   const int max_rows = kTileRowsMax;
   if (a.C * a.M > max_rows) return false;
