@@ -1868,7 +1868,14 @@ static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, ui
   const size_t buf = rowbuf_bytes(cap) + (grad ? (size_t)cap * 12 : 0);  // + GradSmem
   // up to 3 stages in flight, then as many row buffers (multiples of 4) as fit; the fused
   // gradient keeps the ring at 4 so a tile's re-read (4 tiles later) still hits L2
-  for (nstage = 3; nstage >= 2; --nstage) {
+  static int max_stage = -1;  // CKRL_NSTAGE: stage-count ceiling (A/B experiments; barriers for 4)
+  if (max_stage < 0) {
+    const char* env = getenv("CKRL_NSTAGE");
+    max_stage = env ? atoi(env) : 3;
+    if (max_stage > 4) max_stage = 4;
+    if (max_stage < 2) max_stage = 2;
+  }
+  for (nstage = max_stage; nstage >= 2; --nstage) {
     const size_t used = (size_t)nstage * tile_bytes + 1024;
     if (used >= kSmemBudget) continue;
     int nb = (int)((kSmemBudget - used) / buf) & ~3;
