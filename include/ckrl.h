@@ -383,10 +383,11 @@ int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl
 /* Profiling aid: %globaltimer stamps (ns) of CTA 0 from the last TMA loss / fused-step
  * launch: [0] start, [1] GAE phase done, [2] grid barrier passed, [3] constants ready,
  * [4..7] first unit phase of each buffer warp, [8] last row tile, [9] all roles done,
- * [10] reduction done. Synchronises the device. */
+ * [10] reduction done. Synchronises the device. The stamps exist only in a library built
+ * with -DCKRL_PROBES (they cost ~1 us per step); otherwise this reads back zeros. */
 int32_t ckrl_debug_timeline(uint64_t* out, int32_t n);
 /* Profiling aid: per-CTA %globaltimer stamps of the last TMA loss launch, [3][1184]: start,
- * roles done, exit. Synchronises the device. */
+ * roles done, exit. Synchronises the device. Zeros unless built with -DCKRL_PROBES. */
 int32_t ckrl_debug_cta_times(uint64_t* out, int32_t n);
 
 /* ---- (e) rollout pipeline on CUDA streams / events (cfg5) ----------------------------- */

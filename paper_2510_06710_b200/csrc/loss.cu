@@ -20,18 +20,25 @@
 
 namespace ckrl {
 
-// Optional on-device timeline of CTA 0 (%globaltimer, ns), read with ckrl_debug_timeline().
+// On-device probes (%globaltimer, ns), compiled in only with -DCKRL_PROBES
+// (`make EXTRA=-DCKRL_PROBES`, for profiles/tools/tl_probe.py and tail_probe.py): the timeline
+// of CTA 0 and the last CTA (ckrl_debug_timeline) and per-CTA start / roles-done / exit stamps
+// of the last TMA loss launch (ckrl_debug_cta_times). Without it both read back zeros.
 __device__ uint64_t g_timeline[32];
+__device__ uint64_t g_cta_times[3][1184];
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void tl_mark(int slot) {
-  if (blockIdx.x == 0) g_timeline[slot] = gtimer();
-}
-// Per-CTA start / roles-done / exit stamps of the last TMA loss launch (ckrl_debug_cta_times).
-__device__ uint64_t g_cta_times[3][1184];
+#ifdef CKRL_PROBES
+#define CKRL_PROBE(stmt) stmt
+#else
+#define CKRL_PROBE(stmt) \
+  do {                   \
+  } while (0)
+#endif
+__device__ __forceinline__ void tl_mark(int slot) { CKRL_PROBE(if (blockIdx.x == 0) g_timeline[slot] = gtimer()); }
 
 constexpr float kL2E = 1.4426950408889634f;
 constexpr double kLN2 = 0.6931471805599453;
@@ -566,7 +573,7 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   __syncthreads();
   if (tid == 0) tl_mark(27);
   if (!*s_last) return;
-  if (tid == 0) g_timeline[28] = gtimer();  // probe: last CTA after its ticket
+  CKRL_PROBE(if (tid == 0) g_timeline[28] = gtimer());  // probe: last CTA after its ticket
   // Last CTA: warp i < RAW_COUNT sums quantity i over the CTA partials — each lane a fixed
   // strided subset (its loads in flight together), then a shuffle tree: a fixed order for a
   // given grid, so the sums are deterministic. Plain L2 loads: the acquire above ordered
@@ -593,13 +600,13 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
       raw[warp] = x;
     }
   }
-  if (tid == 0) g_timeline[29] = gtimer();  // probe: partials loaded and warp-reduced
+  CKRL_PROBE(if (tid == 0) g_timeline[29] = gtimer());  // probe: partials loaded and warp-reduced
   __syncthreads();
   if (tid == 0) {
-    g_timeline[30] = gtimer();  // probe: raw sums written
+    CKRL_PROBE(g_timeline[30] = gtimer());  // probe: raw sums written
     tickets[TICKET_LOSS] = 0;
     if (a.finalize) finalize_diag(a, k, s_tot, a.diag);
-    g_timeline[31] = gtimer();  // probe: finalised
+    CKRL_PROBE(g_timeline[31] = gtimer());  // probe: finalised
   }
 }
 
@@ -1553,7 +1560,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
 
   if (tid == 0) {
     tl_mark(0);
-    if (blockIdx.x < 1184) g_cta_times[0][blockIdx.x] = gtimer();
+    CKRL_PROBE(if (blockIdx.x < 1184) g_cta_times[0][blockIdx.x] = gtimer());
     for (int s = 0; s < nstage; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kCW);
@@ -1787,11 +1794,11 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
   if (warp == 1 && lane == 0) tl_mark(8);  // row warp 0 done with its last tile
   __syncthreads();
   if (tid == 0) tl_mark(9);
-  if (tid == 0 && blockIdx.x < 1184) g_cta_times[1][blockIdx.x] = gtimer();
+  CKRL_PROBE(if (tid == 0 && blockIdx.x < 1184) g_cta_times[1][blockIdx.x] = gtimer());
   if (MODE == MODE_STATS) return;
   reduce_and_finish(a, FUSED ? s_kf : s_k, acc, tid, kThreads, s_red, &s_last);
   if (tid == 0) tl_mark(10);
-  if (tid == 0 && blockIdx.x < 1184) g_cta_times[2][blockIdx.x] = gtimer();
+  CKRL_PROBE(if (tid == 0 && blockIdx.x < 1184) g_cta_times[2][blockIdx.x] = gtimer());
 }
 
 __global__ void finalize_kernel(LossArgs a) {

@@ -1,4 +1,5 @@
-"""Tail of the headline loss launch under graph replay: per-CTA start / roles-done / exit stamps
+"""(Needs a probe build: `make -C paper_2510_06710_b200/csrc EXTRA=-DCKRL_PROBES`, or CKRL_LIB=<such a build>.)
+Tail of the headline loss launch under graph replay: per-CTA start / roles-done / exit stamps
 (ckrl_debug_cta_times) and the last CTA's reduction marks (timeline slots 28-31)."""
 import ctypes as C
 import os

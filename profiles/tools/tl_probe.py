@@ -1,3 +1,4 @@
+# Needs a probe build: make -C paper_2510_06710_b200/csrc EXTRA=-DCKRL_PROBES (or CKRL_LIB=<such a build>).
 import sys, os, ctypes as C, torch
 sys.path.insert(0, os.getcwd())
 import paper_2510_06710_b200 as ck
