@@ -198,6 +198,9 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int scan_scratch[kGrpoThreads / 32 + 1];
   __shared__ int s_n, s_status, s_groups, s_total, s_retained;
+  // the weights kernel (programmatic dependent) may launch now; it waits for this grid
+  // before reading the group assignment
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x;
   StatsRecord* st = reinterpret_cast<StatsRecord*>(ws + L.stats_local);
   int32_t* env_len = reinterpret_cast<int32_t*>(ws + L.grpo_env);
@@ -378,6 +381,8 @@ __global__ void grpo_weights_kernel(ckrl_rollout ro, int length_normalized, ckrl
   const int32_t* env_fs = env_len + ro.num_envs;
   const int n = ro.num_chunks * ro.chunk_len;
   const int64_t s0 = (int64_t)e * n;
+  // group assignment / lengths come from grpo_group_kernel, this kernel's PDL primary
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool has = gb.env_group[e] >= 0;
   const int32_t uid = gb.env_episode[e];
   const int64_t len = has ? env_len[e] : 0;
@@ -477,9 +482,19 @@ cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep
   grpo_group_kernel<<<1, kGrpoThreads, smem, s>>>(ep, ro.num_envs, opt, gb, ws, L);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  int grid = (ro.num_envs + 7) / 8;
-  grpo_weights_kernel<<<grid, 256, 0, s>>>(ro, opt.length_normalized, gb, ws, L);
-  return cudaGetLastError();
+  // programmatic dependent of the group kernel: its CTAs are resident (and trigger the loss
+  // kernel's launch) while the single group CTA runs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((ro.num_envs + 7) / 8));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, grpo_weights_kernel, ro, (int)opt.length_normalized, gb,
+                            (const char*)ws, L);
 }
 
 }  // namespace ckrl
