@@ -22,20 +22,32 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   uint32_t* tickets = reinterpret_cast<uint32_t*>(ws + L.tickets);
   if (threadIdx.x == 0) {
     parts[blockIdx.x] = mine;
-    __threadfence();
-    uint32_t t = atomicAdd(&tickets[TICKET_ASM], 1u);
+    // one acq_rel ticket: the release publishes this CTA's partial, the acquire (extended to
+    // the CTA by the barrier below) makes every earlier CTA's visible to the last one
+    uint32_t t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(&tickets[TICKET_ASM]) : "memory");
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   AsmPartial q{0.0, 0.0, 0.0, 0.0};
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-    q.n += __ldcg(&parts[b].n);
-    q.s1 += __ldcg(&parts[b].s1);
-    q.s2 += __ldcg(&parts[b].s2);
-    q.n_pos += __ldcg(&parts[b].n_pos);
+  for (unsigned b0 = 0; b0 < gridDim.x; b0 += 4 * blockDim.x) {  // 4 partials in flight per thread
+    AsmPartial v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned b = b0 + threadIdx.x + j * blockDim.x;
+      v[j] = b < gridDim.x ? AsmPartial{__ldcg(&parts[b].n), __ldcg(&parts[b].s1), __ldcg(&parts[b].s2),
+                                        __ldcg(&parts[b].n_pos)}
+                           : AsmPartial{0.0, 0.0, 0.0, 0.0};
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      q.n += v[j].n;
+      q.s1 += v[j].s1;
+      q.s2 += v[j].s2;
+      q.n_pos += v[j].n_pos;
+    }
   }
   for (int off = 16; off > 0; off >>= 1) {
     q.n += __shfl_down_sync(0xffffffffu, q.n, off);
