@@ -1721,28 +1721,34 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       if (lane == 0) mbar_arrive(&metafull_bar[itx]);
       if (lane == 0 && itx == 0) tl_mark(24);
     }
-    if (FUSED) {
-      fused_phase_a(a, m, lane, &s_kf);
-    } else {
-      // overlapped step: the assembly kernel's outputs (stats record, counted, advantages)
-      // are consumed only from here on (no-op when not launched as a PDL dependent)
-      if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (m == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
-      bufwarps_sync<BW>();
-    }
-    const LossConsts k = FUSED ? s_kf : s_k;
     // Software pipeline: this warp's next tile's unit metadata and the row metadata of the
     // next user of this buffer are issued (raw, into registers) before the current unit
-    // phase, so their memory latency hides behind it.
+    // phase, so their memory latency hides behind it. PPO issues the first tile's loads as
+    // soon as the assembly outputs exist, alongside the constants' loads.
     int it = m;
     int64_t tile = blockIdx.x + (int64_t)m * gridDim.x;
     int64_t r0 = 0;
     int nrec = 0;
     UnitRegs ur;
-    if (tile < a.n_tiles) {
-      nrec = tile_recs(tile, r0);
-      unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);
+    auto first_unit_meta = [&]() {
+      if (tile < a.n_tiles) {
+        nrec = tile_recs(tile, r0);
+        unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);
+      }
+    };
+    if (FUSED) {
+      fused_phase_a(a, m, lane, &s_kf);
+      first_unit_meta();
+    } else {
+      // overlapped step: the assembly kernel's outputs (stats record, counted, advantages)
+      // are consumed only from here on (no-op when not launched as a PDL dependent)
+      if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (MODE == MODE_PPO) first_unit_meta();  // (GRPO: measured slower, register pressure)
+      if (m == 0 && lane == 0) s_k = merge_consts(a);  // off the producer's critical path
+      bufwarps_sync<BW>();
+      if (MODE != MODE_PPO) first_unit_meta();
     }
+    const LossConsts k = FUSED ? s_kf : s_k;
     for (; tile < a.n_tiles; tile += stride, it += BW) {
       const int b = it % nbuf;
       buf_of(it, sm, mt);
