@@ -139,9 +139,10 @@ typedef struct {
 
 /* PpoBatch (advantage/assembler.hpp:16-37) as SoA, device pointers (outputs of assembly). */
 typedef struct {
-  uint8_t* counted;   /* [E][Tc][C] */
-  float* advantages;  /* [E][Tc] (chunk) or [E][Tc][C] (action); raw GAE */
-  float* returns;     /* same shape */
+  uint8_t* counted;    /* [E][Tc][C] */
+  double* advantages;  /* [E][Tc] (chunk) or [E][Tc][C] (action); raw GAE, fp64 as the
+                          reference's PpoBatch (assembler.hpp:16-37) */
+  double* returns;     /* same shape */
 } ckrl_ppo_batch;
 
 /* GrpoBatch (advantage/assembler.hpp:40-62) as SoA: each env owns at most one retained
@@ -152,7 +153,8 @@ typedef struct {
   int32_t* env_episode;     /* [E] episode_id of the trajectory */
   double* env_advantage;    /* [E] group-relative advantage */
   int32_t* env_group_size;  /* [E] trajectories in the group */
-  float* slot_weight;       /* [E][Tc][C] per-step weight (0 outside the trajectory / masked) */
+  double* slot_weight;      /* [E][Tc][C] per-step weight, f64 as the reference's TrajChunk::slot_weights
+                               (0 outside the trajectory / masked, grpo.cpp:57-79) */
   uint8_t* slot_member;     /* [E][Tc][C] slot belongs to the trajectory */
   int32_t* group_counts;    /* [2] groups_total, groups_retained (device) */
 } ckrl_grpo_batch;
@@ -186,8 +188,9 @@ size_t ckrl_workspace_bytes(int32_t num_envs, int32_t num_chunks, int32_t chunk_
 int32_t ckrl_workspace_init(void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
 
 /* Merge `world` per-rank whitening/normaliser stats records (host memory, the layout
- * ckrl_stats_record_bytes() describes) in rank order. Exposed for the multi-rank
- * host tests; the device path merges the same records inside the loss kernel. */
+ * ckrl_stats_record_bytes() describes) in rank order (Chan's pairwise moment update).
+ * Exposed for the multi-rank host tests; the device path merges the same records in the
+ * same order inside the loss kernel. */
 size_t ckrl_stats_record_bytes(void);
 int32_t ckrl_merge_stats_host(const void* records, int32_t world, double* out_mean,
                               double* out_denom, int64_t* out_counts /* n_adv,n_val,n_pos */);
@@ -210,7 +213,11 @@ int32_t ckrl_assemble_ppo_batch(const ckrl_rollout* rollout, const ckrl_gae_para
                                 void* workspace, size_t workspace_bytes, ckrl_stream_t stream);
 
 /* normalize_advantages (optim/update.cpp:14-45), materialised in place over the counted
- * units, using the stats left in `workspace` by ckrl_assemble_ppo_batch. */
+ * units, using the stats left in `workspace` by ckrl_assemble_ppo_batch. The stats record
+ * is then marked whitened: a following ckrl_ppo_loss uses the advantages as they are (as
+ * the reference's ppo_loss does after update_ppo's normalize_advantages), and a second
+ * ckrl_normalize_advantages re-whitens with the moments of the whitened values, as the
+ * reference's recomputation does. */
 int32_t ckrl_normalize_advantages(const ckrl_rollout* rollout, const ckrl_granularity* spec,
                                   ckrl_ppo_batch* batch, void* workspace,
                                   size_t workspace_bytes, ckrl_stream_t stream);
@@ -275,11 +282,12 @@ int32_t ckrl_select_groups(int32_t num_envs, const int32_t* src_env_group, int32
                            size_t workspace_bytes, ckrl_stream_t stream);
 
 /* Reads the rank's 64-byte stats record from a workspace after an assembly (synchronises
- * `stream`): {sum, sumsq} (f64), {n_units, n_adv, n_val, n_pos, groups_retained, status}
- * (int64). Returns the device-detected status (e.g. DegenerateGroup from the GRPO assembly,
- * assembler.cpp:247-252) as the call's status. */
+ * `stream`): the advantage-unit moments {mean, M2 = sum of squared deviations} (f64) and
+ * {n_adv, n_adv, n_val, n_pos, groups_retained, status} (int64). Returns the device-detected
+ * status (e.g. DegenerateGroup from the GRPO assembly, assembler.cpp:247-252) as the call's
+ * status. */
 int32_t ckrl_read_stats(const void* workspace, size_t workspace_bytes, int32_t num_envs,
-                        double* sums_out /* [2] */, int64_t* counts_out /* [6] */,
+                        double* moments_out /* [2] */, int64_t* counts_out /* [6] */,
                         ckrl_stream_t stream);
 
 /* ---- (b) fused action-token kernel ---------------------------------------------------- */
@@ -460,14 +468,15 @@ int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* spec, const double* params,
 
 /* dump_slab (core/types.cpp:9-28) of an SoA slab in HOST memory: the reference's
  * trajectories.txt text ("# env_id episode_uid step tokens[M] reward terminated truncated
- * valid" then one line per atomic slot; uid = env << 32 | episode_id, -1 frozen; reward as
- * %.17g of the f64 reward, e.g. ckrl_pipeline_outputs.reward_f64). Writes at most `capacity`
- * bytes (NUL-terminated when it fits) and the full text length to *length (capacity 0 /
- * out NULL: size query). */
+ * valid" then one line per atomic slot: env_id is the slab row; uid = (first_env_id + row)
+ * << 32 | episode_id, the global env id of a VecEnv partition or rank shard (vec_env.cpp:94),
+ * -1 frozen; reward as %.17g of the f64 reward, e.g. ckrl_pipeline_outputs.reward_f64).
+ * Writes at most `capacity` bytes (NUL-terminated when it fits) and the full text length to
+ * *length (capacity 0 / out NULL: size query). */
 int32_t ckrl_dump_slab(int32_t num_envs, int32_t num_chunks, int32_t chunk_len,
                        int32_t tokens_per_action, int32_t token_dtype, const void* tokens,
                        const double* reward, const uint8_t* flags, const int32_t* episode_id,
-                       char* out, size_t capacity, size_t* length);
+                       int32_t first_env_id, char* out, size_t capacity, size_t* length);
 
 /* save_checkpoint / load_checkpoint (policy/checkpoint.cpp:37-83): the CKRL v1 file of a
  * policy descriptor + its flat f64 parameters (host memory). Load with params NULL queries

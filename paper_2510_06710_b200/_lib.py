@@ -147,7 +147,7 @@ SIGNATURES = {
     "ckrl_debug_cta_times": (C.c_int32, [vp, C.c_int32]),
     "ckrl_adam_workspace_bytes": (C.c_size_t, []),
     "ckrl_dump_slab": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
-                                   C.c_char_p, C.c_size_t, P(C.c_size_t)]),
+                                   C.c_int32, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "ckrl_save_checkpoint": (C.c_int32, [P(PolicyDesc), vp, C.c_char_p]),
     "ckrl_load_checkpoint": (C.c_int32, [C.c_char_p, P(PolicyDesc), vp, C.c_int64, P(C.c_int64)]),
     "ckrl_adam_step": (C.c_int32, [C.c_int32, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp,

@@ -70,8 +70,8 @@ def assemble_ppo_batch(rollout: RolloutBuffer, options: PpoAssemblyOptions,
         shape = (E, Tc) if spec.advantage_level == Level.Chunk else (E, Tc, Cn)
         ws = workspace or Workspace(E, 1, dev)
         out = PpoBatch(spec=spec, counted=torch.empty((E, Tc, Cn), dtype=torch.uint8, device=dev),
-                       advantages=torch.empty(shape, dtype=torch.float32, device=dev),
-                       returns=torch.empty(shape, dtype=torch.float32, device=dev), workspace=ws)
+                       advantages=torch.empty(shape, dtype=torch.float64, device=dev),
+                       returns=torch.empty(shape, dtype=torch.float64, device=dev), workspace=ws)
     bc = out.c()
     _lib.check(_lib.lib().ckrl_assemble_ppo_batch(C.byref(rollout.c()), C.byref(options.gae.c()),
                                                   C.byref(spec.c()), C.byref(bc), out.workspace.ptr,

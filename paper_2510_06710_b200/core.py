@@ -277,6 +277,8 @@ class PpoBatch:
     workspace: Workspace
 
     def c(self):
+        if self.advantages.dtype != torch.float64 or self.returns.dtype != torch.float64:
+            raise TypeError("PpoBatch advantages / returns are float64 (the reference's PpoBatch)")
         return _lib.PpoBatchC(_ptr(self.counted), _ptr(self.advantages), _ptr(self.returns))
 
     def advantage_unit_count(self) -> int:
@@ -324,7 +326,7 @@ class GrpoBatch:
                    env_episode=torch.empty(E, **i32),
                    env_advantage=torch.empty(E, dtype=torch.float64, device=dev),
                    env_group_size=torch.empty(E, **i32),
-                   slot_weight=torch.empty((E, Tc, Cn), dtype=torch.float32, device=dev),
+                   slot_weight=torch.empty((E, Tc, Cn), dtype=torch.float64, device=dev),
                    slot_member=torch.empty((E, Tc, Cn), dtype=torch.uint8, device=dev),
                    group_counts=torch.zeros(2, **i32), workspace=workspace)
 

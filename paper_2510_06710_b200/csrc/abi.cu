@@ -236,19 +236,15 @@ int32_t ckrl_merge_stats_host(const void* records, int32_t world, double* out_me
                               double* out_denom, int64_t* out_counts) {
   CKRL_REQUIRE(records && world >= 1, CKRL_ERR_INVALID_ARGUMENT, "bad stats records");
   const StatsRecord* r = static_cast<const StatsRecord*>(records);
-  double n = 0.0, s1 = 0.0, s2 = 0.0;
   int64_t c[4] = {0, 0, 0, 0};
   for (int i = 0; i < world; ++i) {
-    n += (double)r[i].n_units;
-    s1 += r[i].sum;
-    s2 += r[i].sumsq;
     c[0] += r[i].n_adv;
     c[1] += r[i].n_val;
     c[2] += r[i].n_pos;
     c[3] += r[i].groups_retained;
   }
   double mean, denom;
-  whitening(n, s1, s2, &mean, &denom);
+  whitening(merge_records(r, world), &mean, &denom);
   if (out_mean) *out_mean = mean;
   if (out_denom) *out_denom = denom;
   if (out_counts) std::memcpy(out_counts, c, sizeof(c));
@@ -298,9 +294,12 @@ int32_t ckrl_normalize_advantages(const ckrl_rollout* ro, const ckrl_granularity
   if ((st = check_rollout(ro, false))) return st;
   if ((st = check_ws(workspace, ws_bytes, ro->num_envs, 1))) return st;
   WsLayout L = ws_layout(ro->num_envs, 1);
+  CKRL_REQUIRE(batch && batch->counted && batch->advantages, CKRL_ERR_INVALID_ARGUMENT,
+               "batch counted / advantages required");
   CKRL_CUDA(launch_normalize(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, batch->counted,
                              batch->advantages,
-                             reinterpret_cast<const StatsRecord*>((char*)workspace + L.stats_local), 1,
+                             reinterpret_cast<StatsRecord*>((char*)workspace + L.stats_local), 1,
+                             reinterpret_cast<uint32_t*>((char*)workspace + L.tickets) + TICKET_NORM,
                              (cudaStream_t)stream));
   return CKRL_OK;
 }
@@ -424,8 +423,8 @@ int32_t ckrl_adam_step(int32_t dtype, int64_t n, void* params, void* grad, void*
 }
 
 int32_t ckrl_dump_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
-                       const double* reward, const uint8_t* flags, const int32_t* episode_id, char* out,
-                       size_t capacity, size_t* length) {
+                       const double* reward, const uint8_t* flags, const int32_t* episode_id,
+                       int32_t first_env_id, char* out, size_t capacity, size_t* length) {
   CKRL_REQUIRE(E >= 0 && Tc >= 0 && C >= 1 && M >= 1, CKRL_ERR_LENGTH_MISMATCH, "bad slab dimensions");
   CKRL_REQUIRE(length, CKRL_ERR_INVALID_ARGUMENT, "length output required");
   CKRL_REQUIRE((int64_t)E * Tc == 0 || (tokens && reward && flags && episode_id), CKRL_ERR_INVALID_ARGUMENT,
@@ -433,7 +432,8 @@ int32_t ckrl_dump_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t toke
   CKRL_REQUIRE(token_dtype == CKRL_DTYPE_U8 || token_dtype == CKRL_DTYPE_I32, CKRL_ERR_INVALID_ARGUMENT,
                "token dtype must be u8 or i32");
   std::string text;
-  format_slab(E, Tc, C, M, token_dtype, tokens, reward, flags, episode_id, text);
+  CKRL_REQUIRE(first_env_id >= 0, CKRL_ERR_INVALID_ARGUMENT, "first_env_id must be >= 0");
+  format_slab(E, Tc, C, M, token_dtype, tokens, reward, flags, episode_id, first_env_id, text);
   *length = text.size();
   if (out && capacity) {
     const size_t n = text.size() < capacity ? text.size() : capacity;
@@ -766,11 +766,11 @@ int32_t ckrl_read_stats(const void* ws, size_t ws_bytes, int32_t E, double* sums
                             (cudaStream_t)stream));
   CKRL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   if (sums) {
-    sums[0] = r.sum;
-    sums[1] = r.sumsq;
+    sums[0] = r.mean;
+    sums[1] = r.m2;
   }
   if (counts) {
-    counts[0] = r.n_units;
+    counts[0] = r.n_adv;
     counts[1] = r.n_adv;
     counts[2] = r.n_val;
     counts[3] = r.n_pos;

@@ -31,46 +31,43 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   __syncthreads();
   if (!is_last) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  AsmPartial q{0.0, 0.0, 0.0, 0.0};
+  // thread t merges partials t, t + nthr, ... in order; then a fixed tree (deterministic)
+  AsmPartial q{{0.0, 0.0, 0.0}, 0.0};
   for (unsigned b0 = 0; b0 < gridDim.x; b0 += 4 * blockDim.x) {  // 4 partials in flight per thread
     AsmPartial v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const unsigned b = b0 + threadIdx.x + j * blockDim.x;
-      v[j] = b < gridDim.x ? AsmPartial{__ldcg(&parts[b].n), __ldcg(&parts[b].s1), __ldcg(&parts[b].s2),
+      v[j] = b < gridDim.x ? AsmPartial{{__ldcg(&parts[b].m.n), __ldcg(&parts[b].m.mean), __ldcg(&parts[b].m.m2)},
                                         __ldcg(&parts[b].n_pos)}
-                           : AsmPartial{0.0, 0.0, 0.0, 0.0};
+                           : AsmPartial{{0.0, 0.0, 0.0}, 0.0};
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      q.n += v[j].n;
-      q.s1 += v[j].s1;
-      q.s2 += v[j].s2;
+      q.m = mom_merge(q.m, v[j].m);
       q.n_pos += v[j].n_pos;
     }
   }
   for (int off = 16; off > 0; off >>= 1) {
-    q.n += __shfl_down_sync(0xffffffffu, q.n, off);
-    q.s1 += __shfl_down_sync(0xffffffffu, q.s1, off);
-    q.s2 += __shfl_down_sync(0xffffffffu, q.s2, off);
+    const Moments o{__shfl_down_sync(0xffffffffu, q.m.n, off), __shfl_down_sync(0xffffffffu, q.m.mean, off),
+                    __shfl_down_sync(0xffffffffu, q.m.m2, off)};
+    q.m = mom_merge(q.m, o);
     q.n_pos += __shfl_down_sync(0xffffffffu, q.n_pos, off);
   }
   if (lane == 0) wpart[warp] = q;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  AsmPartial t{0.0, 0.0, 0.0, 0.0};
+  AsmPartial t{{0.0, 0.0, 0.0}, 0.0};
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    t.n += wpart[w].n;
-    t.s1 += wpart[w].s1;
-    t.s2 += wpart[w].s2;
+    t.m = mom_merge(t.m, wpart[w].m);
     t.n_pos += wpart[w].n_pos;
   }
   StatsRecord* st = reinterpret_cast<StatsRecord*>(ws + L.stats_local);
-  st->sum = t.s1;
-  st->sumsq = t.s2;
-  st->n_units = (int64_t)t.n;
-  st->n_adv = (int64_t)t.n;
-  st->n_val = (int64_t)t.n;  // value level == advantage level (assembler.cpp:82)
+  st->mean = t.m.mean;
+  st->m2 = t.m.m2;
+  st->flags = 0;
+  st->n_adv = (int64_t)t.m.n;
+  st->n_val = (int64_t)t.m.n;  // value level == advantage level (assembler.cpp:82)
   st->n_pos = (int64_t)t.n_pos * M;
   st->groups_retained = 0;
   st->status = 0;
@@ -88,21 +85,21 @@ template <bool SERIAL>
 // the loss kernel's persistent CTAs all start at once under programmatic dependent launch.
 __global__ void __launch_bounds__(32 * kAsmWarpsPerCta, 12)
 ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lambda,
-                    uint8_t* counted, float* adv, float* ret, char* ws, WsLayout L) {
+                    uint8_t* counted, double* adv, double* ret, char* ws, WsLayout L) {
   asm volatile("griddepcontrol.launch_dependents;");
   __shared__ GaeSums wsum[kAsmWarpsPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = action_level ? ro.num_chunks * ro.chunk_len : ro.num_chunks;
-  GaeSums g{0.0, 0.0, 0.0, 0.0};
+  GaeSums g{{0.0, 0.0, 0.0}, 0.0};
   if (SERIAL) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < ro.num_envs)
       g = action_level ? serial_gae(ActionAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda)
                        : serial_gae(ChunkAcc{ro, e, counted, adv, ret}, n_items, gamma, lambda);
     for (int off = 16; off > 0; off >>= 1) {
-      g.n += __shfl_down_sync(0xffffffffu, g.n, off);
-      g.s1 += __shfl_down_sync(0xffffffffu, g.s1, off);
-      g.s2 += __shfl_down_sync(0xffffffffu, g.s2, off);
+      const Moments o{__shfl_down_sync(0xffffffffu, g.m.n, off), __shfl_down_sync(0xffffffffu, g.m.mean, off),
+                      __shfl_down_sync(0xffffffffu, g.m.m2, off)};
+      g.m = mom_merge(g.m, o);
       g.counted_slots += __shfl_down_sync(0xffffffffu, g.counted_slots, off);
     }
   } else {
@@ -113,12 +110,10 @@ ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lamb
   }
   if (lane == 0) wsum[warp] = g;
   __syncthreads();
-  AsmPartial p{0.0, 0.0, 0.0, 0.0};
+  AsmPartial p{{0.0, 0.0, 0.0}, 0.0};
   if (threadIdx.x == 0)
     for (int w = 0; w < kAsmWarpsPerCta; ++w) {
-      p.n += wsum[w].n;
-      p.s1 += wsum[w].s1;
-      p.s2 += wsum[w].s2;
+      p.m = mom_merge(p.m, wsum[w].m);
       p.n_pos += wsum[w].counted_slots;
     }
   finish_asm_stats(p, ws, L, ro.tokens_per_action);
@@ -132,35 +127,52 @@ __global__ void flat_gae_kernel(int num_seqs, const int32_t* offs, const double*
   warp_gae(FlatAcc{r, v, b, f, adv, ret, offs[q]}, offs[q + 1] - offs[q], gamma, lambda);
 }
 
-// In-place whitening of the counted advantage units (optim/update.cpp:14-45).
+// In-place whitening of the counted advantage units (optim/update.cpp:14-45). The last CTA
+// then rewrites the rank's record with the moments of the whitened values (mean 0,
+// M2 / denom^2) and marks it whitened, so a following loss uses the advantages as they are
+// and a second normalisation re-whitens them as the reference's recomputation would.
 __global__ void normalize_kernel(ckrl_rollout ro, int action_level, const uint8_t* counted,
-                                 float* adv, const StatsRecord* recs, int world) {
+                                 double* adv, StatsRecord* recs, int world, uint32_t* ticket) {
   __shared__ double s_mean, s_denom;
   __shared__ int s_skip;
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    double n = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int r = 0; r < world; ++r) {
-      n += (double)recs[r].n_units;
-      s1 += recs[r].sum;
-      s2 += recs[r].sumsq;
-    }
-    s_skip = n < 2.0;
-    whitening(n, s1, s2, &s_mean, &s_denom);
+    const Moments m = merge_records(recs, world);
+    s_skip = m.n < 2.0;
+    whitening(m, &s_mean, &s_denom);
   }
   __syncthreads();
-  if (s_skip) return;
-  const int C = ro.chunk_len;
-  const int64_t nunits = (int64_t)ro.num_envs * ro.num_chunks * (action_level ? C : 1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nunits;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    bool is_unit;
-    if (action_level) {
-      is_unit = counted[i];
-    } else {
-      is_unit = false;
-      for (int j = 0; j < C; ++j) is_unit = is_unit || counted[i * C + j];
+  if (!s_skip) {
+    const int C = ro.chunk_len;
+    const int64_t nunits = (int64_t)ro.num_envs * ro.num_chunks * (action_level ? C : 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nunits;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      bool is_unit;
+      if (action_level) {
+        is_unit = counted[i];
+      } else {
+        is_unit = false;
+        for (int j = 0; j < C; ++j) is_unit = is_unit || counted[i * C + j];
+      }
+      if (is_unit) adv[i] = (adv[i] - s_mean) / s_denom;
     }
-    if (is_unit) adv[i] = (float)(((double)adv[i] - s_mean) / s_denom);
+  }
+  // every CTA has read the record (above) before the last one rewrites it
+  if (threadIdx.x == 0) {
+    uint32_t t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
+    s_last = t == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *ticket = 0;
+    for (int r = 0; r < world; ++r) {
+      if (!s_skip) {
+        recs[r].m2 = recs[r].m2 / (s_denom * s_denom);
+        recs[r].mean = (recs[r].mean - s_mean) / s_denom;
+      }
+      recs[r].flags |= STATS_WHITENED;
+    }
   }
 }
 
@@ -370,9 +382,10 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   if (tid == 0) {
     gb.group_counts[0] = s_total;
     gb.group_counts[1] = s_retained;
-    st->sum = 0.0;
-    st->sumsq = 0.0;
-    st->n_units = st->n_adv = st->n_val = st->n_pos = 0;
+    st->mean = 0.0;
+    st->m2 = 0.0;
+    st->flags = 0;
+    st->n_adv = st->n_val = st->n_pos = 0;
     st->groups_retained = s_retained;
     st->status = s_status;
   }
@@ -415,10 +428,10 @@ __global__ void grpo_weights_kernel(ckrl_rollout ro, int length_normalized, ckrl
     unsigned bal = __ballot_sync(0xffffffffu, match);
     int k = k_base + __popc(bal & ((1u << lane) - 1u));
     if (i < n) {
-      float w = 0.0f;
+      double w = 0.0;
       if (match && k < len) {
         bool valid_step = !(success && k > fs);
-        w = (!length_normalized || valid_step) ? (float)u : 0.0f;
+        w = (!length_normalized || valid_step) ? u : 0.0;
       }
       gb.slot_member[s0 + i] = match ? 1 : 0;
       gb.slot_weight[s0 + i] = w;
@@ -473,12 +486,12 @@ cudaError_t launch_flat_gae(int num_seqs, const int32_t* offs, const double* r, 
 }
 
 cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uint8_t* counted,
-                             float* adv, const StatsRecord* recs, int world, cudaStream_t s) {
+                             double* adv, StatsRecord* recs, int world, uint32_t* ticket, cudaStream_t s) {
   int64_t nunits = (int64_t)ro.num_envs * ro.num_chunks * (action_level ? ro.chunk_len : 1);
   int grid = (int)((nunits + 255) / 256);
   if (grid > 1184) grid = 1184;
   if (grid < 1) grid = 1;
-  normalize_kernel<<<grid, 256, 0, s>>>(ro, action_level, counted, adv, recs, world);
+  normalize_kernel<<<grid, 256, 0, s>>>(ro, action_level, counted, adv, recs, world, ticket);
   return cudaGetLastError();
 }
 
@@ -550,7 +563,8 @@ __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
   const int lb = a.sp.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4;
   const int U = a.action_level ? C : 1;
   const int NV = a.value_action ? C : 1;
-  AsmPartial mine{0.0, 0.0, 0.0, 0.0};
+  AsmPartial mine{{0.0, 0.0, 0.0}, 0.0};
+  MomAcc mom;
   for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
     const int64_t r = a.idx[i];
     const int64_t P = (int64_t)C * M;
@@ -587,22 +601,15 @@ __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
       mine.n_pos += cnt;
       if (a.action_level) {
         for (int j = 0; j < C; ++j)
-          if (a.sb.counted[r * C + j]) {
-            const double x = a.sb.advantages[r * C + j];
-            mine.n += 1.0;
-            mine.s1 += x;
-            mine.s2 += x * x;
-          }
+          if (a.sb.counted[r * C + j]) mom.add(a.sb.advantages[r * C + j]);
       } else if (cnt) {
-        const double x = a.sb.advantages[r];
-        mine.n += 1.0;
-        mine.s1 += x;
-        mine.s2 += x * x;
+        mom.add(a.sb.advantages[r]);
       }
     }
     __syncthreads();
   }
   // thread 0 holds the CTA's partial; finish_asm_stats reads it from thread 0
+  mine.m = mom.get();
   finish_asm_stats(mine, a.ws, a.L, M);
 }
 

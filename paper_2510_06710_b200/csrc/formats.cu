@@ -42,7 +42,8 @@ bool get_le(FILE* f, T& v) {
 
 // Appends the dump_slab text of the SoA slab to `out`.
 int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
-                    const double* reward, const uint8_t* flags, const int32_t* episode_id, std::string& out) {
+                    const double* reward, const uint8_t* flags, const int32_t* episode_id, int32_t first_env_id,
+                    std::string& out) {
   char buf[64];
   out += "# env_id episode_uid step tokens[" + std::to_string(M) + "] reward terminated truncated valid\n";
   for (int32_t e = 0; e < E; ++e) {
@@ -51,8 +52,10 @@ int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_d
       for (int32_t j = 0; j < C; ++j, ++step) {
         const int64_t sl = ((int64_t)e * Tc + t) * C + j;
         const int32_t id = episode_id[sl];
-        // uid = env << 32 | k (envsim/vec_env.cpp:14-16); -1 marks a frozen slot
-        const int64_t uid = id < 0 ? -1 : (int64_t)(((uint64_t)(uint32_t)e << 32) | (uint32_t)id);
+        // uid = global env id << 32 | k (envsim/vec_env.cpp:14-16, the env id is first_env_id + i
+        // for a VecEnv partition, vec_env.cpp:94); -1 marks a frozen slot
+        const int64_t uid =
+            id < 0 ? -1 : (int64_t)(((uint64_t)(uint32_t)(first_env_id + e) << 32) | (uint32_t)id);
         int n = std::snprintf(buf, sizeof buf, "%d %" PRId64 " %" PRId64, e, uid, step);
         out.append(buf, (size_t)n);
         for (int32_t m = 0; m < M; ++m) {

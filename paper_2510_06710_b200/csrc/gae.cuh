@@ -29,11 +29,22 @@ struct Unit {
 // with the exact incoming A. Segment ends come from done flags, uid changes between
 // consecutive units and the end of the list (flush_segment's open end).
 // ---------------------------------------------------------------------------------
-// Per-lane GAE statistics: advantage units, sum and sum of squares (fp64; merged by plain
-// addition in a fixed order, so no divisions on the hot path and results are deterministic).
+// Per-lane GAE statistics: advantage-unit moments (shifted sums per lane, merged with Chan's
+// update in a fixed tree order: deterministic) and the counted-slot count.
 struct GaeSums {
-  double n, s1, s2, counted_slots;
+  Moments m;
+  double counted_slots;
 };
+__device__ __forceinline__ GaeSums gae_sums_reduce(const MomAcc& acc, double counted_slots) {
+  GaeSums st{acc.get(), counted_slots};
+  for (int off = 16; off > 0; off >>= 1) {  // fixed-shape tree over lanes (deterministic)
+    Moments o{__shfl_down_sync(0xffffffffu, st.m.n, off), __shfl_down_sync(0xffffffffu, st.m.mean, off),
+              __shfl_down_sync(0xffffffffu, st.m.m2, off)};
+    st.m = mom_merge(st.m, o);
+    st.counted_slots += __shfl_down_sync(0xffffffffu, st.counted_slots, off);
+  }
+  return st;  // valid in lane 0
+}
 
 template <class Acc>
 __device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gamma, double lambda) {
@@ -73,7 +84,8 @@ __device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gam
   // Phases 2 (compose my range's affine map) and 4 (replay with the exact incoming
   // advantage) share one reverse walk; pass 0 composes, pass 1 writes.
   double P = 0.0, Q = 1.0, a_next = 0.0;
-  GaeSums st{0.0, 0.0, 0.0, 0.0};
+  MomAcc mom;
+  double counted_slots = 0.0;
   for (int pass = 0; pass < 2; ++pass) {
     bool nx_has = nx_has0;
     int32_t nx_uid = nx_uid0;
@@ -94,10 +106,8 @@ __device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gam
       } else {
         const double a = __dadd_rn(delta, __dmul_rn(gl, seg_end ? 0.0 : a_next));
         acc.store(i, u, a, __dadd_rn(a, u.v));
-        st.n += 1.0;
-        st.s1 += a;
-        st.s2 += a * a;
-        st.counted_slots += u.counted_slots;
+        mom.add(a);
+        counted_slots += u.counted_slots;
         a_next = a;
       }
       nx_has = true;
@@ -118,14 +128,7 @@ __device__ __noinline__ GaeSums warp_gae(const Acc& acc, int n_items, double gam
       if (lane == 31) a_next = 0.0;
     }
   }
-  // fixed-shape tree over lanes (deterministic)
-  for (int off = 16; off > 0; off >>= 1) {
-    st.n += __shfl_down_sync(0xffffffffu, st.n, off);
-    st.s1 += __shfl_down_sync(0xffffffffu, st.s1, off);
-    st.s2 += __shfl_down_sync(0xffffffffu, st.s2, off);
-    st.counted_slots += __shfl_down_sync(0xffffffffu, st.counted_slots, off);
-  }
-  return st;  // valid in lane 0
+  return gae_sums_reduce(mom, counted_slots);
 }
 
 // Register-resident variant: lane l owns items [l*K, l*K+K), all loaded once up front
@@ -206,7 +209,8 @@ __device__ __noinline__ GaeSums warp_gae_regs(const Acc& acc, int n_items, doubl
   }
   double a_next = __shfl_down_sync(0xffffffffu, P, 1);
   if (lane == 31) a_next = 0.0;
-  GaeSums st{0.0, 0.0, 0.0, 0.0};
+  MomAcc mom;
+  double counted_slots = 0.0;
 #pragma unroll
   for (int q = K - 1; q >= 0; --q) {
     if (lo + q >= n_items) continue;
@@ -216,19 +220,11 @@ __device__ __noinline__ GaeSums warp_gae_regs(const Acc& acc, int n_items, doubl
     }
     const double a = __dadd_rn(delta[q], __dmul_rn(gl, segend[q] ? 0.0 : a_next));
     acc.store(lo + q, u[q], a, __dadd_rn(a, u[q].v));
-    st.n += 1.0;
-    st.s1 += a;
-    st.s2 += a * a;
-    st.counted_slots += u[q].counted_slots;
+    mom.add(a);
+    counted_slots += u[q].counted_slots;
     a_next = a;
   }
-  for (int off = 16; off > 0; off >>= 1) {
-    st.n += __shfl_down_sync(0xffffffffu, st.n, off);
-    st.s1 += __shfl_down_sync(0xffffffffu, st.s1, off);
-    st.s2 += __shfl_down_sync(0xffffffffu, st.s2, off);
-    st.counted_slots += __shfl_down_sync(0xffffffffu, st.counted_slots, off);
-  }
-  return st;
+  return gae_sums_reduce(mom, counted_slots);
 }
 
 // Dispatch on items per lane: register-resident for <= 4 items per lane, else re-reading.
@@ -247,7 +243,8 @@ constexpr int kSerialItems = 256;
 template <class Acc>
 __device__ __forceinline__ GaeSums serial_gae(const Acc& acc, int n_items, double gamma, double lambda) {
   const double gl = __dmul_rn(gamma, lambda);
-  GaeSums st{0.0, 0.0, 0.0, 0.0};
+  MomAcc mom;
+  double counted_slots = 0.0;
   bool nx_has = false;
   int32_t nx_uid = 0;
   double nx_v = 0.0, a_next = 0.0;
@@ -262,16 +259,14 @@ __device__ __forceinline__ GaeSums serial_gae(const Acc& acc, int n_items, doubl
     const double delta = __dadd_rn(__dadd_rn(u.r, __dmul_rn(gamma, vnext)), -u.v);
     const double a = __dadd_rn(delta, __dmul_rn(gl, seg_end ? 0.0 : a_next));
     acc.store(i, u, a, __dadd_rn(a, u.v));
-    st.n += 1.0;
-    st.s1 += a;
-    st.s2 += a * a;
-    st.counted_slots += u.counted_slots;
+    mom.add(a);
+    counted_slots += u.counted_slots;
     a_next = a;
     nx_has = true;
     nx_uid = u.uid;
     nx_v = u.v;
   }
-  return st;
+  return GaeSums{mom.get(), counted_slots};  // per thread (the caller merges)
 }
 
 // ---- accessors ------------------------------------------------------------------
@@ -285,8 +280,8 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   const ckrl_rollout ro;
   int e;
   uint8_t* counted;
-  float* adv;
-  float* ret;
+  double* adv;
+  double* ret;
   __device__ Unit load(int t) const {
     // All C slots' fields are fetched with independent loads first (no data-dependent
     // load chain), then the unit is formed in registers.
@@ -387,8 +382,8 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   __device__ void store(int t, const Unit& u, double a, double R) const {
     const int C = ro.chunk_len;
     const int64_t rec = (int64_t)e * ro.num_chunks + t;
-    adv[rec] = (float)a;
-    ret[rec] = (float)R;
+    adv[rec] = a;
+    ret[rec] = R;
     // counted = the leading episode's contiguous valid prefix from the first valid slot
     if (C == 8 && (reinterpret_cast<uintptr_t>(counted) & 7) == 0) {
       uint64_t w = 0;
@@ -403,8 +398,8 @@ struct ChunkAcc {  // chunk-level units: one per record (assembler.cpp:158-190)
   __device__ void store_empty(int t) const {
     const int C = ro.chunk_len;
     const int64_t rec = (int64_t)e * ro.num_chunks + t;
-    adv[rec] = 0.0f;
-    ret[rec] = 0.0f;
+    adv[rec] = 0.0;
+    ret[rec] = 0.0;
     for (int j = 0; j < C; ++j) counted[rec * C + j] = 0;
   }
 };
@@ -413,8 +408,8 @@ struct ActionAcc {  // action-level units: one per valid slot (assembler.cpp:112
   const ckrl_rollout ro;
   int e;
   uint8_t* counted;
-  float* adv;
-  float* ret;
+  double* adv;
+  double* ret;
   __device__ Unit load(int i) const {
     const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
     uint8_t f = ro.flags[s];
@@ -431,14 +426,14 @@ struct ActionAcc {  // action-level units: one per valid slot (assembler.cpp:112
   }
   __device__ void store(int i, const Unit&, double a, double R) const {
     const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
-    adv[s] = (float)a;
-    ret[s] = (float)R;
+    adv[s] = a;
+    ret[s] = R;
     counted[s] = 1;
   }
   __device__ void store_empty(int i) const {
     const int64_t s = (int64_t)e * ro.num_chunks * ro.chunk_len + i;
-    adv[s] = 0.0f;
-    ret[s] = 0.0f;
+    adv[s] = 0.0;
+    ret[s] = 0.0;
     counted[s] = 0;
   }
 };

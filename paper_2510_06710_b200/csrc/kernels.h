@@ -21,8 +21,8 @@ struct LossArgs {
   const float* old_lp;
   // PPO
   const uint8_t* counted;
-  const float* adv;
-  const float* ret;
+  const double* adv;
+  const double* ret;
   const float* new_values;
   int adv_level, lp_level, val_level;
   double clip, vcoef, ecoef;
@@ -31,7 +31,7 @@ struct LossArgs {
   const int32_t* env_group;
   const double* env_adv;
   const int32_t* env_group_size;
-  const float* slot_weight;
+  const double* slot_weight;
   const uint8_t* slot_member;
   // outputs (nullable)
   float* coeff_lp;
@@ -57,7 +57,8 @@ struct LossArgs {
   int pdl;
   int reserved_sms;
   int nbuf;      // TMA kernel: row-partial buffers (multiple of 4, <= kMaxRowBufs)
-  int rows_cap;  // TMA kernel: rows per buffer (rec_per_tile * C * M)
+  int rows_cap;  // TMA kernel: rows per buffer (rec_per_tile * C * M, rounded up to 8)
+  int slots_cap; // TMA kernel: slots per buffer (rec_per_tile * C, rounded up to 8)
   void* dlogits; // optional fused softmax-backward output [positions][V] (logits dtype)
 };
 
@@ -68,14 +69,15 @@ cudaError_t launch_flat_gae(int num_seqs, const int32_t* offs, const double* r, 
                             const double* b, const uint8_t* f, double gamma, double lambda,
                             double* adv, double* ret, cudaStream_t s);
 cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uint8_t* counted,
-                             float* adv, const StatsRecord* recs, int world, cudaStream_t s);
+                             double* adv, StatsRecord* recs, int world, uint32_t* ticket, cudaStream_t s);
 cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep,
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s);
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t debug_cta_times(uint64_t* out, int n);
 int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
-                    const double* reward, const uint8_t* flags, const int32_t* episode_id, std::string& out);
+                    const double* reward, const uint8_t* flags, const int32_t* episode_id, int32_t first_env_id,
+                    std::string& out);
 int32_t write_checkpoint(const ckrl_policy_desc& d, const double* params, int64_t count, const char* path,
                          std::string& err);
 int32_t read_checkpoint(const char* path, ckrl_policy_desc* d, double* params, int64_t capacity,

@@ -42,6 +42,13 @@ __device__ __forceinline__ void tl_mark(int slot) { CKRL_PROBE(if (blockIdx.x ==
 
 constexpr float kL2E = 1.4426950408889634f;
 constexpr double kLN2 = 0.6931471805599453;
+constexpr double kInvLN2 = 1.4426950408889634;
+// relative error of the fp32 log2(e) the row sums are taken with, and its reciprocal
+constexpr double kL2EDelta = (double)kL2E / 1.4426950408889634 - 1.0;
+constexpr double kInvL2EF = 1.0 / (double)kL2E;
+#ifndef CKRL_ROWFIN
+#define CKRL_ROWFIN 3  // row finish: 3 split log2 (default), 2 fp64 in the unit phase, 1 fp32, 0 MUFU approx
+#endif
 
 __device__ __forceinline__ float ex2(float y) {
   float r;
@@ -84,6 +91,7 @@ struct RowSmem {
   float* old;  // old log-prob
   double* lp;  // new log-prob (unit phase)
   float* ent;  // entropy (unit phase)
+  float* ex;   // TMA kernel, CKRL_ROWFIN 3: the exponent of the shifted sum (s = 2^ex * mant)
 };
 
 __device__ __forceinline__ float grp8_max(float v) {
@@ -214,39 +222,39 @@ struct LossConsts {
 
 __device__ __forceinline__ double drecip(double x) { return __drcp_rn(x); }  // == 1.0 / x (IEEE rn)
 
-// Merge the per-rank stats records (fixed rank order) into the loss constants.
-__device__ LossConsts consts_from(double n, double s1, double s2, int64_t n_adv, int64_t n_val,
-                                  int64_t n_pos, int64_t groups, int status, int normalize) {
+// Loss constants from the merged moments / normalisers.
+__device__ LossConsts consts_from(const Moments& mom, int64_t n_adv, int64_t n_val, int64_t n_pos,
+                                  int64_t groups, int status, int normalize) {
   LossConsts k;
   k.n_adv = n_adv;
   k.groups = groups;
   k.inv_adv = n_adv > 0 ? drecip((double)n_adv) : 0.0;
   k.inv_val = n_val > 0 ? drecip((double)n_val) : 0.0;
   k.inv_pos = n_pos > 0 ? drecip((double)n_pos) : 0.0;
-  k.do_norm = normalize && n >= 2.0;
-  whitening(n, s1, s2, &k.mean, &k.denom);
+  k.do_norm = normalize && mom.n >= 2.0;
+  whitening(mom, &k.mean, &k.denom);
   k.inv_denom = drecip(k.denom);
   k.inv_groups = groups > 0 ? drecip((double)groups) : 0.0;
   k.status = status;
   return k;
 }
 
+// Merge the per-rank stats records (fixed rank order) into the loss constants. Advantages
+// already whitened in place (ckrl_normalize_advantages) are used as they are.
 __device__ LossConsts merge_consts(const LossArgs& a) {
-  double n = 0.0, s1 = 0.0, s2 = 0.0;
-  int64_t n_adv = 0, n_val = 0, n_pos = 0, groups = 0;
-  int status = 0;
+  int64_t n_val = 0, n_pos = 0, groups = 0, n_adv = 0;
+  int status = 0, whitened = 0;
   for (int r = 0; r < a.world; ++r) {
     const StatsRecord& s = a.recs[r];
-    n += (double)s.n_units;
-    s1 += s.sum;
-    s2 += s.sumsq;
     n_adv += s.n_adv;
     n_val += s.n_val;
     n_pos += s.n_pos;
     groups += s.groups_retained;
+    whitened |= (int)(s.flags & STATS_WHITENED);
     if (s.status && !status) status = (int)s.status;
   }
-  return consts_from(n, s1, s2, n_adv, n_val, n_pos, groups, status, a.normalize);
+  return consts_from(merge_records(a.recs, a.world), n_adv, n_val, n_pos, groups, status,
+                     a.normalize && !whitened);
 }
 
 // One advantage unit: ratio, clipped surrogate (losses.cpp:32-46) and the approx-kl term
@@ -367,7 +375,7 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
       }
     } else if (MODE == MODE_GRPO && a.lp_level == CKRL_LEVEL_TOKEN) {
       const int e = (int)(rec / a.Tc);
-      const float w = a.slot_weight[slot];
+      const double w = a.slot_weight[slot];
       float coeff = 0.0f;
       if (a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f) {
         const double inv_g = drecip((double)a.env_group_size[e]);
@@ -414,7 +422,7 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
             if (k.do_norm) adv = (adv - k.mean) * k.inv_denom;
           } else {
             e = (int)(rec / a.Tc);
-            const float w = a.slot_weight[slot];
+            const double w = a.slot_weight[slot];
             on = a.env_group[e] >= 0 && a.slot_member[slot] && w != 0.0f;
             adv = on ? a.env_adv[e] : 0.0;
             scale = on ? k.inv_groups * (drecip((double)a.env_group_size[e])) * (double)w : 0.0;
@@ -478,7 +486,7 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
         if (MODE == MODE_PPO) {
           on = a.counted[slot] != 0;
         } else {
-          on = a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+          on = a.slot_member[slot] && a.slot_weight[slot] != 0.0;
           if (on && (t % M) == 0) wsum += (double)a.slot_weight[slot];
         }
         if (on) {
@@ -518,7 +526,7 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
             if (MODE == MODE_PPO)
               on = a.counted[slot] != 0;
             else
-              on = has_env && a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+              on = has_env && a.slot_member[slot] && a.slot_weight[slot] != 0.0;
             a.coeff_lp[rec * P + t] = on && any ? coeff : 0.0f;
           }
       }
@@ -628,7 +636,7 @@ __host__ __device__ constexpr size_t rowsmem_bytes(int rows_cap) {
 __device__ __forceinline__ bool row_needed(const LossArgs& a, int mode, int64_t slot) {
   if (a.all_rows) return true;
   if (mode == MODE_PPO) return a.counted[slot] != 0;
-  if (mode == MODE_GRPO) return a.slot_member[slot] && a.slot_weight[slot] != 0.0f;
+  if (mode == MODE_GRPO) return a.slot_member[slot] && a.slot_weight[slot] != 0.0;
   return true;
 }
 
@@ -946,46 +954,61 @@ constexpr int kTileRowsMax = 128;  // rows (tokens) per tile
 struct MetaSmem {
   int32_t* tok;
   float* old;
-  float* w;
-  float* adv;
-  float* ret;
+  double* w;
+  double* adv;
+  double* ret;
   float* nv;
   int32_t* esz;
   double* eadv;
   uint8_t* act;   // per slot: bit1 unit active (counted / trajectory slot with weight)
   uint8_t* need;  // per slot: the row phase evaluates this slot's rows
 };
-__host__ __device__ constexpr size_t meta_bytes(int cap) {
-  return (size_t)cap * (4 + 4 + 4 + 4 + 4 + 4 + 4 + 8 + 1 + 1);
+// One row buffer of the TMA kernel: per-row partials + the tile's metadata. Row arrays are
+// sized by `cap` (rows per tile), slot / unit / record arrays by `scap` (slots per tile; a
+// record has C slots, a unit is a record or a slot), both multiples of 8; fp64 arrays first.
+__host__ __device__ constexpr size_t rowbuf_bytes(int cap, int scap) {
+  return (size_t)cap * (8 + 5 * 4 + 4 + 4) + (size_t)scap * (8 * 4 + 4 + 4 + 1 + 1);
 }
-__device__ __forceinline__ MetaSmem carve_meta(unsigned char* p, int cap) {
-  MetaSmem m;
-  m.eadv = reinterpret_cast<double*>(p);
-  m.tok = reinterpret_cast<int32_t*>(m.eadv + cap);
+__device__ __forceinline__ void carve_buf(unsigned char* p, int cap, int scap, RowSmem& sm, MetaSmem& m) {
+  sm.lp = reinterpret_cast<double*>(p);
+  m.eadv = sm.lp + cap;
+  m.adv = m.eadv + scap;
+  m.ret = m.adv + scap;
+  m.w = m.ret + scap;
+  sm.s = reinterpret_cast<float*>(m.w + scap);
+  sm.t2 = sm.s + cap;
+  sm.c = sm.t2 + cap;
+  sm.xt = sm.c + cap;
+  sm.ex = sm.xt + cap;
+  sm.old = nullptr;  // (direct kernel only)
+  sm.ent = nullptr;
+  m.tok = reinterpret_cast<int32_t*>(sm.ex + cap);
   m.old = reinterpret_cast<float*>(m.tok + cap);
-  m.w = m.old + cap;
-  m.adv = m.w + cap;
-  m.ret = m.adv + cap;
-  m.nv = m.ret + cap;
-  m.esz = reinterpret_cast<int32_t*>(m.nv + cap);
-  m.act = reinterpret_cast<uint8_t*>(m.esz + cap);
-  m.need = m.act + cap;
-  return m;
-}
-// One row buffer: per-row partials + the tile's metadata, for `cap` rows (cap % 8 == 0).
-__host__ __device__ constexpr size_t rowbuf_bytes(int cap) {
-  return rowsmem_bytes(cap) + meta_bytes(cap);
+  m.nv = m.old + cap;
+  m.esz = reinterpret_cast<int32_t*>(m.nv + scap);
+  m.act = reinterpret_cast<uint8_t*>(m.esz + scap);
+  m.need = m.act + scap;
 }
 
 // Row metadata (what the row warps read): token ids and per-slot "evaluate" flags. In the
 // fused step the assembly outputs do not exist yet, so every valid slot is evaluated
 // (counted slots are a subset); otherwise the assembled activity decides.
+// Slot-level fields are imaged for the first 32 slots of a tile (q == 0: every tile with M >= 4);
+// slots beyond are read directly at store time.
 struct RowRegs {
   int32_t tok[4];
-  int32_t g[4];   // GRPO: env group id (non-PDL path)
-  float w[4];     // GRPO: slot weight
-  uint8_t fl[4];  // raw slot flags / counted / membership byte
+  int32_t g;      // GRPO: env group id (non-PDL path)
+  double w;       // GRPO: slot weight
+  uint8_t fl;     // raw slot flags / counted / membership byte
 };
+template <int MODE, bool FUSED>
+__device__ __forceinline__ uint8_t row_need_direct(const LossArgs& a, int64_t s, bool from_flags) {
+  if (a.all_rows || MODE == MODE_STATS) return 1;
+  if (FUSED) return (a.ro.flags[s] & CKRL_FLAG_VALID) != 0;
+  if (from_flags) return 1;
+  if (MODE == MODE_PPO) return a.counted[s] != 0;
+  return (a.env_group[(int)(s / a.C) / a.Tc] >= 0) & (a.slot_member[s] != 0) & (a.slot_weight[s] != 0.0);
+}
 template <int MODE, bool FUSED>
 __device__ __forceinline__ void row_meta_load(const LossArgs& a, int64_t r0, int nrec, int lane,
                                               RowRegs& R, bool from_flags) {
@@ -996,25 +1019,25 @@ __device__ __forceinline__ void row_meta_load(const LossArgs& a, int64_t r0, int
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
     if (i < rows) R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
-    R.fl[q] = 1;
-    if (i < slots && !a.all_rows && MODE != MODE_STATS) {
-      if (FUSED) {
-        R.fl[q] = a.ro.flags[s0 + i];
-      } else if (from_flags) {  // overlapped step: every row (the loss masks by counted), no load
-        R.fl[q] = CKRL_FLAG_VALID;
-      } else if (MODE == MODE_PPO) {
-        R.fl[q] = a.counted[s0 + i];
-      } else {
-        R.g[q] = a.env_group[(int)(s0 + i) / C / a.Tc];
-        R.fl[q] = a.slot_member[s0 + i];
-        R.w[q] = a.slot_weight[s0 + i];
-      }
+  }
+  R.fl = 1;
+  if (lane < slots && !a.all_rows && MODE != MODE_STATS) {
+    if (FUSED) {
+      R.fl = a.ro.flags[s0 + lane];
+    } else if (from_flags) {  // overlapped step: every row (the loss masks by counted), no load
+      R.fl = CKRL_FLAG_VALID;
+    } else if (MODE == MODE_PPO) {
+      R.fl = a.counted[s0 + lane];
+    } else {
+      R.g = a.env_group[(int)(s0 + lane) / C / a.Tc];
+      R.fl = a.slot_member[s0 + lane];
+      R.w = a.slot_weight[s0 + lane];
     }
   }
 }
 template <int MODE, bool FUSED>
-__device__ __forceinline__ void row_meta_store(const LossArgs& a, int nrec, int lane, const RowRegs& R,
-                                               const MetaSmem& m, bool from_flags) {
+__device__ __forceinline__ void row_meta_store(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                               const RowRegs& R, const MetaSmem& m, bool from_flags) {
   const int C = a.C, P = C * a.M;
   const int rows = nrec * P, slots = nrec * C;
 #pragma unroll
@@ -1023,13 +1046,15 @@ __device__ __forceinline__ void row_meta_store(const LossArgs& a, int nrec, int 
     if (i < rows) m.tok[i] = R.tok[q];
     if (i < slots) {
       bool n = true;
-      if (!a.all_rows && MODE != MODE_STATS) {
+      if (q > 0) {
+        n = row_need_direct<MODE, FUSED>(a, r0 * C + i, from_flags);
+      } else if (!a.all_rows && MODE != MODE_STATS) {
         if (FUSED || from_flags)
-          n = (R.fl[q] & CKRL_FLAG_VALID) != 0;
+          n = (R.fl & CKRL_FLAG_VALID) != 0;
         else if (MODE == MODE_PPO)
-          n = R.fl[q] != 0;
+          n = R.fl != 0;
         else
-          n = (R.g[q] >= 0) & (R.fl[q] != 0) & (R.w[q] != 0.0f);
+          n = (R.g >= 0) & (R.fl != 0) & (R.w != 0.0);
       }
       m.need[i] = n ? 1 : 0;
     }
@@ -1040,7 +1065,7 @@ __device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec
                                          const MetaSmem& m, bool from_flags) {
   RowRegs R;
   row_meta_load<MODE, FUSED>(a, r0, nrec, lane, R, from_flags);
-  row_meta_store<MODE, FUSED>(a, nrec, lane, R, m, from_flags);
+  row_meta_store<MODE, FUSED>(a, r0, nrec, lane, R, m, from_flags);
 }
 
 // PPO tiles whose advantage, return and new-value units (value level == advantage level for
@@ -1054,11 +1079,14 @@ __device__ __forceinline__ bool small_units(const LossArgs& a, int nrec) {
 // load is computed before the matching *_store, so a *_load only issues loads and their
 // latency hides behind whatever runs in between (the current tile's unit phase).
 struct UnitRegs {
-  float mix;  // PPO small-unit path: this lane's advantage / return / new value (unit_meta_load)
-  float old[4], w[4], adv[4], ret[4], nv[4];
-  int32_t esz[4], g[4];
-  double eadv[4];
-  uint8_t act[4];  // raw: counted (PPO) / slot membership (GRPO)
+  double mix;  // PPO small-unit path: this lane's advantage / return / new value (unit_meta_load)
+  float old[4];
+  // q == 0 only (the tile's first 32 slots / records: every tile with M >= 4); the rare
+  // q >= 1 entries are loaded directly in unit_meta_store
+  float nv;
+  double adv, ret, w, eadv;
+  int32_t esz, g;
+  uint8_t act;  // raw: counted (PPO) / slot membership (GRPO)
 };
 
 // Loads that may read what other CTAs wrote earlier in the same (fused) launch go
@@ -1073,67 +1101,72 @@ __device__ __forceinline__ void unit_meta_load(const LossArgs& a, int64_t r0, in
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
     if (i < rows) R.old[q] = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + k0 + i);
-    if (i < slots) {
-      if (MODE == MODE_PPO) {
-        R.act[q] = __ldcg(a.counted + s0 + i);
-      } else if (MODE == MODE_GRPO) {
-        R.g[q] = a.env_group[(int)(s0 + i) / C / a.Tc];
-        R.act[q] = a.slot_member[s0 + i];
-        R.w[q] = a.slot_weight[s0 + i];
-      }
+  }
+  const int i = lane;
+  if (i < slots) {
+    if (MODE == MODE_PPO) {
+      R.act = __ldcg(a.counted + s0 + i);
+    } else if (MODE == MODE_GRPO) {
+      R.g = a.env_group[(int)(s0 + i) / C / a.Tc];
+      R.act = a.slot_member[s0 + i];
+      R.w = a.slot_weight[s0 + i];
     }
-    if (MODE == MODE_PPO && small_units(a, nrec)) {
-      // one warp-wide load for all three per-unit arrays: lanes [0,U) advantages, [U,2U)
-      // returns, [2U,3U) new values (each global load instruction a buffer warp issues waits
-      // in the MIO queue behind the row warps' shared loads)
-      if (q == 0) {
-        const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;  // == advantage units
-        const int64_t ub = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
-        const float* p = lane < U ? a.adv + ub + lane
-                                  : lane < 2 * U ? a.ret + ub + (lane - U)
-                                                 : (a.new_values ? a.new_values + ub + (lane - 2 * U) : nullptr);
-        R.mix = (lane < 3 * U && p) ? __ldcg(p) : 0.0f;
-      }
-    } else if (MODE == MODE_PPO) {
-      const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
-      const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
-      if (i < adv_units) {
-        const float* p = a.adv + (a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i;
-        R.adv[q] = __ldcg(p);
-      }
-      if (i < val_units) {
-        const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
-        R.ret[q] = __ldcg(a.ret + vb + i);
-        R.nv[q] = a.new_values ? __ldg(a.new_values + vb + i) : 0.0f;
-      }
+  }
+  if (MODE == MODE_PPO && small_units(a, nrec)) {
+    // one warp-wide load for all three per-unit arrays: lanes [0,U) advantages, [U,2U)
+    // returns, [2U,3U) new values (each global load instruction a buffer warp issues waits
+    // in the MIO queue behind the row warps' shared loads)
+    const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;  // == advantage units
+    const int64_t ub = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
+    const double* pd = lane < U ? a.adv + ub + lane : lane < 2 * U ? a.ret + ub + (lane - U) : nullptr;
+    const float* pf = (lane >= 2 * U && lane < 3 * U && a.new_values) ? a.new_values + ub + (lane - 2 * U) : nullptr;
+    R.mix = pd ? __ldcg(pd) : (pf ? (double)__ldg(pf) : 0.0);
+  } else if (MODE == MODE_PPO) {
+    const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+    const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+    if (i < adv_units) R.adv = __ldcg(a.adv + (a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i);
+    if (i < val_units) {
+      const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
+      R.ret = __ldcg(a.ret + vb + i);
+      R.nv = a.new_values ? __ldg(a.new_values + vb + i) : 0.0f;
     }
-    if (MODE == MODE_GRPO && i < nrec) {
-      const int e = (int)(r0 + i) / a.Tc;
-      R.esz[q] = a.env_group_size[e];
-      R.eadv[q] = a.env_adv[e];
-    }
+  }
+  if (MODE == MODE_GRPO && i < nrec) {
+    const int e = (int)(r0 + i) / a.Tc;
+    R.esz = a.env_group_size[e];
+    R.eadv = a.env_adv[e];
   }
 }
 
 template <int MODE>
-__device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int lane, const UnitRegs& R,
-                                                const MetaSmem& m) {
+__device__ __forceinline__ void unit_meta_store(const LossArgs& a, int64_t r0, int nrec, int lane,
+                                                const UnitRegs& R, const MetaSmem& m) {
   const int C = a.C, P = C * a.M;
   const int rows = nrec * P, slots = nrec * C;
+  const int64_t s0 = r0 * C;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int i = lane + 32 * q;
     if (i < rows) m.old[i] = R.old[q];
     if (i < slots) {
       if (MODE == MODE_PPO) {
-        m.act[i] = R.act[q] != 0 ? 2 : 0;
-        m.w[i] = 0.0f;
+        const uint8_t c = q == 0 ? R.act : __ldcg(a.counted + s0 + i);
+        m.act[i] = c != 0 ? 2 : 0;
+        m.w[i] = 0.0;
       } else if (MODE == MODE_GRPO) {
-        m.act[i] = ((R.g[q] >= 0) & (R.act[q] != 0) & (R.w[q] != 0.0f)) ? 2 : 0;
-        m.w[i] = R.w[q];
+        int32_t g;
+        uint8_t mb;
+        double w;
+        if (q == 0) {
+          g = R.g, mb = R.act, w = R.w;
+        } else {
+          g = a.env_group[(int)(s0 + i) / C / a.Tc], mb = a.slot_member[s0 + i], w = a.slot_weight[s0 + i];
+        }
+        m.act[i] = ((g >= 0) & (mb != 0) & (w != 0.0)) ? 2 : 0;
+        m.w[i] = w;
       } else {
         m.act[i] = 0;
-        m.w[i] = 0.0f;
+        m.w[i] = 0.0;
       }
     }
     if (MODE == MODE_PPO && small_units(a, nrec)) {
@@ -1141,16 +1174,33 @@ __device__ __forceinline__ void unit_meta_store(const LossArgs& a, int nrec, int
         const int U = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
         if (lane < U) m.adv[lane] = R.mix;
         else if (lane < 2 * U) m.ret[lane - U] = R.mix;
-        else if (lane < 3 * U) m.nv[lane - 2 * U] = R.mix;
+        else if (lane < 3 * U) m.nv[lane - 2 * U] = (float)R.mix;
       }
     } else if (MODE == MODE_PPO && i < slots) {  // covers both unit kinds (nrec <= slots)
-      m.adv[i] = R.adv[q];
-      m.ret[i] = R.ret[q];
-      m.nv[i] = R.nv[q];
+      const int adv_units = a.adv_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+      const int val_units = a.val_level == CKRL_LEVEL_CHUNK ? nrec : slots;
+      if (q == 0) {
+        m.adv[i] = R.adv;
+        m.ret[i] = R.ret;
+        m.nv[i] = R.nv;
+      } else {  // > 32 units per tile (M < 4 at action level): direct loads
+        if (i < adv_units) m.adv[i] = __ldcg(a.adv + (a.adv_level == CKRL_LEVEL_CHUNK ? r0 : s0) + i);
+        if (i < val_units) {
+          const int64_t vb = a.val_level == CKRL_LEVEL_CHUNK ? r0 : s0;
+          m.ret[i] = __ldcg(a.ret + vb + i);
+          m.nv[i] = a.new_values ? __ldg(a.new_values + vb + i) : 0.0f;
+        }
+      }
     }
     if (MODE == MODE_GRPO && i < nrec) {
-      m.esz[i] = R.esz[q];
-      m.eadv[i] = R.eadv[q];
+      if (q == 0) {
+        m.esz[i] = R.esz;
+        m.eadv[i] = R.eadv;
+      } else {
+        const int e = (int)(r0 + i) / a.Tc;
+        m.esz[i] = a.env_group_size[e];
+        m.eadv[i] = a.env_adv[e];
+      }
     }
   }
 }
@@ -1182,16 +1232,44 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   for (int row = lane; row < rows; row += 32) {
     const int64_t kk = k0 + row;
     const int sl = qdiv(row, inv_m), r = qdiv(row, inv_p);
+#if CKRL_ROWFIN == 3
+    // row warps left log2 s as exponent + log2(mantissa) and E[y] = t / s (y = x fl(log2 e) - c);
+    // finish in fp64, with the first-order correction for the fp32 log2(e) constant (the
+    // sums see x scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x])
+    const double l2s = (double)sm.ex[row] + (double)sm.s[row];
+    const double ls = l2s * kLN2;
+    const double ey = (double)sm.t2[row];
+    const double xc = (double)sm.c[row];
+    const double lp = ((double)sm.xt[row] - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
+    const double entd = ls - kLN2 * ey;  // entropy, fp64
+    if (gkent) sm.s[row] = (float)l2s;  // the fused seam's re-read takes log2 s (grad_row)
+#elif CKRL_ROWFIN == 2
+    // row warps left the raw sums s = sum 2^y, t = sum 2^y * y (y = x * fl(log2 e) - c);
+    // finish in fp64: ln s, E[y] = t / s, and the first-order correction for the fp32
+    // log2(e) constant (the sums see x scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x])
+    const double sd = (double)sm.s[row];
+    const double ls = log(sd);
+    const double ey = (double)sm.t2[row] * drecip(sd);
+    const double xc = (double)sm.c[row];
+    const double lp = ((double)sm.xt[row] - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
+    const double entd = ls - kLN2 * ey;  // entropy, fp64
+    if (gkent) {  // the fused seam's re-read needs log2 s and E[y] (grad_row)
+      sm.s[row] = (float)(ls * kInvLN2);
+      sm.t2[row] = (float)ey;
+    }
+#else
     // row warps left log2(sum) in s and sum(e*y)/sum(e) in t2 (TMA row phase)
     const double ls = (double)sm.s[row] * kLN2;
     const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
-    const float ent = (float)ls - 0.6931471805599453f * sm.t2[row];
+    const double entd = ls - kLN2 * (double)sm.t2[row];  // entropy finished in fp64
+#endif
+    const float ent = (float)entd;
     sm.lp[row] = lp;
     if (o.tok_lp) o.tok_lp[kk] = (float)lp;
     if (o.tok_ent) o.tok_ent[kk] = ent;
     const bool on = (m.act[sl] & 2) != 0;
     if (MODE == MODE_PPO) {
-      if (on) acc.ent += ent;
+      if (on) acc.ent += entd;
       const float cent = (on && a.ecoef != 0.0) ? (float)(-a.ecoef * k.inv_pos) : 0.0f;
       if (o.coeff_ent) o.coeff_ent[kk] = cent;
       if (gkent) gkent[row] = cent;
@@ -1448,17 +1526,15 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
   __shared__ AsmPartial bpart[kBufWarps];
   const ckrl_rollout& ro = a.ro;
   const bool action = a.adv_level == CKRL_LEVEL_ACTION;
-  AsmPartial acc{0.0, 0.0, 0.0, 0.0};
+  AsmPartial acc{{0.0, 0.0, 0.0}, 0.0};
   for (int e = blockIdx.x + b * gridDim.x; e < ro.num_envs; e += kBufWarps * gridDim.x) {
     uint8_t* cnt = const_cast<uint8_t*>(a.counted);
-    float* adv = const_cast<float*>(a.adv);
-    float* ret = const_cast<float*>(a.ret);
+    double* adv = const_cast<double*>(a.adv);
+    double* ret = const_cast<double*>(a.ret);
     const GaeSums g = action ? env_gae(ActionAcc{ro, e, cnt, adv, ret}, ro.num_chunks * ro.chunk_len,
                                       a.gamma, a.lambda)
                              : env_gae(ChunkAcc{ro, e, cnt, adv, ret}, ro.num_chunks, a.gamma, a.lambda);
-    acc.n += g.n;
-    acc.s1 += g.s1;
-    acc.s2 += g.s2;
+    acc.m = mom_merge(acc.m, g.m);
     acc.n_pos += g.counted_slots;
   }
   if (lane == 0) bpart[b] = acc;
@@ -1468,11 +1544,9 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
   AsmPartial* parts = reinterpret_cast<AsmPartial*>(a.ws + a.L.asm_partials);
   uint32_t* tickets = reinterpret_cast<uint32_t*>(a.ws + a.L.tickets);
   if (b == 0 && lane == 0) {
-    AsmPartial p{0.0, 0.0, 0.0, 0.0};
+    AsmPartial p{{0.0, 0.0, 0.0}, 0.0};
     for (int w = 0; w < kBufWarps; ++w) {
-      p.n += bpart[w].n;
-      p.s1 += bpart[w].s1;
-      p.s2 += bpart[w].s2;
+      p.m = mom_merge(p.m, bpart[w].m);
       p.n_pos += bpart[w].n_pos;
     }
     parts[blockIdx.x] = p;
@@ -1491,29 +1565,28 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
   }
   bufwarps_sync();
   if (b == 0) {  // one warp: fixed-order sum of the grid's partials
-    AsmPartial q{0.0, 0.0, 0.0, 0.0};
+    AsmPartial q{{0.0, 0.0, 0.0}, 0.0};
     for (unsigned g = lane; g < gridDim.x; g += 32) {
-      q.n += __ldcg(&parts[g].n);
-      q.s1 += __ldcg(&parts[g].s1);
-      q.s2 += __ldcg(&parts[g].s2);
+      q.m = mom_merge(q.m, Moments{__ldcg(&parts[g].m.n), __ldcg(&parts[g].m.mean), __ldcg(&parts[g].m.m2)});
       q.n_pos += __ldcg(&parts[g].n_pos);
     }
     for (int off = 16; off > 0; off >>= 1) {
-      q.n += __shfl_down_sync(0xffffffffu, q.n, off);
-      q.s1 += __shfl_down_sync(0xffffffffu, q.s1, off);
-      q.s2 += __shfl_down_sync(0xffffffffu, q.s2, off);
+      const Moments o{__shfl_down_sync(0xffffffffu, q.m.n, off), __shfl_down_sync(0xffffffffu, q.m.mean, off),
+                      __shfl_down_sync(0xffffffffu, q.m.m2, off)};
+      q.m = mom_merge(q.m, o);
       q.n_pos += __shfl_down_sync(0xffffffffu, q.n_pos, off);
     }
     if (lane == 0) {
-      const int64_t n = (int64_t)q.n, npos = (int64_t)q.n_pos * a.M;
+      const int64_t n = (int64_t)q.m.n, npos = (int64_t)q.n_pos * a.M;
       // value level == advantage level (assembler.cpp:82): n_val == n_adv
-      *s_kf = consts_from(q.n, q.s1, q.s2, n, n, npos, 0, 0, a.normalize);
+      *s_kf = consts_from(q.m, n, n, npos, 0, 0, a.normalize);
       tl_mark(3);
       if (blockIdx.x == 0) {  // the rank's stats record, as ckrl_assemble_ppo_batch leaves it
         StatsRecord* st = reinterpret_cast<StatsRecord*>(a.ws + a.L.stats_local);
-        st->sum = q.s1;
-        st->sumsq = q.s2;
-        st->n_units = st->n_adv = st->n_val = n;
+        st->mean = q.m.mean;
+        st->m2 = q.m.m2;
+        st->flags = 0;
+        st->n_adv = st->n_val = n;
         st->n_pos = npos;
         st->groups_retained = 0;
         st->status = 0;
@@ -1553,8 +1626,8 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
   const int M = a.M, P = a.C * M;
   unsigned char* stage_base = smem_raw;
   unsigned char* buf_base = smem_raw + (size_t)nstage * tile_bytes;
-  const int nbuf = a.nbuf, cap = a.rows_cap;
-  unsigned char* grad_base = buf_base + (size_t)nbuf * rowbuf_bytes(cap);  // GRAD: GradSmem per buffer
+  const int nbuf = a.nbuf, cap = a.rows_cap, scap = a.slots_cap;
+  unsigned char* grad_base = buf_base + (size_t)nbuf * rowbuf_bytes(cap, scap);  // GRAD: GradSmem per buffer
   auto grad_of = [&](int bi) { return carve_grad(grad_base + (size_t)bi * cap * 12, cap); };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -1627,9 +1700,9 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     };
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it,
                  s = (s + 1 == nstage) ? (sph ^= 1u, 0) : s + 1, b = (b + 1 == nbuf) ? (bph ^= 1u, 0) : b + 1) {
-      unsigned char* bb = buf_base + b * rowbuf_bytes(cap);
-      const RowSmem sm = carve_rows(bb, cap);
-      const MetaSmem mt = carve_meta(bb + rowsmem_bytes(cap), cap);
+      RowSmem sm;
+      MetaSmem mt;
+      carve_buf(buf_base + b * rowbuf_bytes(cap, scap), cap, scap, sm, mt);
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
@@ -1671,10 +1744,35 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
               xt = sizeof(LT) == 4 ? (float)reinterpret_cast<const float*>(rp[q])[tok]
                                    : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
             }
-            // the row's two transcendental finishing ops stay on the row warps (2 MUFU ops per
-            // 256): the unit phase then needs no MUFU, which the row warps keep saturated
-            sm.s[row] = need ? __log2f(s_[q]) : 0.0f;               // log2 of the shifted sum
-            sm.t2[row] = need ? __fdividef(t_[q], s_[q]) : 0.0f;   // sum e*y / sum e
+#if CKRL_ROWFIN == 3
+            // log2 s = ex + log2(mant), mant in [1, 2): the exponent exactly, the mantissa's
+            // log2 by the accurate fp32 log2f (|result| < 1: abs error <= 6e-8), so no fp32
+            // rounding of a value up to 8 (2.4e-7) reaches the log-prob; E[y] = t / s at 2 ulp
+            // (it only feeds the entropy).
+            if (need) {
+              const int ebits = (__float_as_int(s_[q]) >> 23) - 127;  // s >= 1: normal, positive
+              const float mant = __int_as_float((__float_as_int(s_[q]) & 0x007fffff) | 0x3f800000);
+              sm.s[row] = log2f(mant);
+              sm.ex[row] = (float)ebits;
+              sm.t2[row] = __fdividef(t_[q], s_[q]);
+            } else {
+              sm.s[row] = 0.0f;
+              sm.ex[row] = 0.0f;
+              sm.t2[row] = 0.0f;
+            }
+#elif CKRL_ROWFIN == 2
+            // raw sums: the unit phase finishes the row in fp64 (log, reciprocal), so the
+            // row warps carry no finishing op and no fp32 rounding of log2(s) (up to 2.4e-7
+            // absolute at s ~ 2^4..2^8) reaches the log-prob
+            sm.s[row] = need ? s_[q] : 1.0f;   // sum 2^y (>= 1: the max bin contributes 2^0)
+            sm.t2[row] = need ? t_[q] : 0.0f;  // sum 2^y * y
+#elif CKRL_ROWFIN == 1
+            sm.s[row] = need ? log2f(s_[q]) : 0.0f;    // log2 of the shifted sum
+            sm.t2[row] = need ? t_[q] / s_[q] : 0.0f;  // sum e*y / sum e
+#else
+            sm.s[row] = need ? __log2f(s_[q]) : 0.0f;
+            sm.t2[row] = need ? __fdividef(t_[q], s_[q]) : 0.0f;
+#endif
             sm.c[row] = c_[q];
             sm.xt[row] = xt;
           }
@@ -1690,9 +1788,11 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     if (GRAD) {  // the last nbuf tiles' gradient passes (their buffers are not reused)
       for (int li = it > nbuf ? it - nbuf : 0; li < it; ++li) {  // local tile index
         const int bi = li % nbuf;
-        unsigned char* bb = buf_base + bi * rowbuf_bytes(cap);
+        RowSmem gsm;
+        MetaSmem gmt;
+        carve_buf(buf_base + bi * rowbuf_bytes(cap, scap), cap, scap, gsm, gmt);
         mbar_wait(&metafull_bar[bi], (uint32_t)((li / nbuf + 1) & 1));  // its unit phase is done
-        grad_pass(blockIdx.x + (int64_t)li * gridDim.x, carve_rows(bb, cap), grad_of(bi));
+        grad_pass(blockIdx.x + (int64_t)li * gridDim.x, gsm, grad_of(bi));
       }
     }
   } else {
@@ -1703,9 +1803,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     const int m = warp - 1 - kCW;
     const int64_t stride = (int64_t)BW * gridDim.x;
     auto buf_of = [&](int itx, RowSmem& sm, MetaSmem& mt) {
-      unsigned char* bb = buf_base + (itx % nbuf) * rowbuf_bytes(cap);
-      sm = carve_rows(bb, cap);
-      mt = carve_meta(bb + rowsmem_bytes(cap), cap);
+      carve_buf(buf_base + (itx % nbuf) * rowbuf_bytes(cap, scap), cap, scap, sm, mt);
     };
     RowSmem sm;
     MetaSmem mt;
@@ -1756,7 +1854,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       const bool probe = lane == 0 && m == 0;
       if (lane == 0 && it == m) tl_mark(20 + m);
       if (probe && it == BW) tl_mark(3);
-      unit_meta_store<MODE>(a, nrec, lane, ur, mt);
+      unit_meta_store<MODE>(a, r0, nrec, lane, ur, mt);
       __syncwarp();
       if (probe && it == 0) tl_mark(1);
       if (probe && it == BW) tl_mark(28);
@@ -1787,7 +1885,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
       if (probe && it == BW) tl_mark(30);
       if (rtile < a.n_tiles) {
-        row_meta_store<MODE, FUSED>(a, rn, lane, rr, mt, a.pdl != 0);
+        row_meta_store<MODE, FUSED>(a, rr0, rn, lane, rr, mt, a.pdl != 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       } else if (GRAD) {  // no next user: the arrival only releases the tile's gradient pass
@@ -1877,8 +1975,9 @@ static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, ui
   if (rec_per_tile * a.C * a.M > max_rows) rec_per_tile = max_rows / (a.C * a.M);
   tile_bytes = (uint32_t)(rec_per_tile * rec);
   const int cap = (rec_per_tile * a.C * a.M + 7) & ~7;
+  const int scap = (rec_per_tile * a.C + 7) & ~7;
   const bool grad = a.dlogits != nullptr;
-  const size_t buf = rowbuf_bytes(cap) + (grad ? (size_t)cap * 12 : 0);  // + GradSmem
+  const size_t buf = rowbuf_bytes(cap, scap) + (grad ? (size_t)cap * 12 : 0);  // + GradSmem
   // up to 3 stages in flight, then as many row buffers (multiples of 4) as fit; the fused
   // gradient keeps the ring at 4 so a tile's re-read (4 tiles later) still hits L2
   static int max_stage = -1;  // CKRL_NSTAGE: stage-count ceiling (A/B experiments; barriers for 4)
@@ -1897,6 +1996,7 @@ static bool tma_plan(LossArgs& a, int dbytes, int& rec_per_tile, int& nstage, ui
     if (nb >= kRowBufs) {
       a.nbuf = nb;
       a.rows_cap = cap;
+      a.slots_cap = scap;
       return true;
     }
   }
@@ -1908,7 +2008,7 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
   auto kern = tma_tile_kernel<MODE, LT, ROWW, RIF, FUSED, BW, GRAD>;
   if (a.nbuf % BW) a.nbuf -= a.nbuf % BW;
   a.n_tiles = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile;
-  const size_t smem = (size_t)nstage * tile_bytes + (size_t)a.nbuf * rowbuf_bytes(a.rows_cap) +
+  const size_t smem = (size_t)nstage * tile_bytes + (size_t)a.nbuf * rowbuf_bytes(a.rows_cap, a.slots_cap) +
                       (GRAD ? (size_t)a.nbuf * a.rows_cap * 12 : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

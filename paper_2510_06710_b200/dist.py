@@ -2,7 +2,7 @@
 
 The path shards by environment (GAE segments never cross envs, assembler.cpp:108-193)
 and, for GRPO, by whole groups (GroupKey, assembler.cpp:207-226). The only exchanges are
-the 64-byte per-rank stats record before the loss (whitening sums + normalisers or the
+the 64-byte per-rank stats record before the loss (whitening moments + normalisers or the
 retained-group count) and the loss scalars after it — both inside ckrl_*_step on the
 caller's stream. torch.distributed only bootstraps the NCCL unique id.
 """
@@ -43,17 +43,18 @@ def check_group_sharding(env_of_episode, key_of_episode, world: int, shard_of_en
 
 @dataclass
 class StatsRecord:
-    """Host view of the 64-byte record ranks all-gather (csrc/common.cuh StatsRecord)."""
-    sum: float = 0.0
-    sumsq: float = 0.0
-    n_units: int = 0
+    """Host view of the 64-byte record ranks all-gather (csrc/common.cuh StatsRecord):
+    the advantage-unit moments (mean, M2 = sum of squared deviations) and the normalisers."""
+    mean: float = 0.0
+    m2: float = 0.0
+    flags: int = 0
     n_adv: int = 0
     n_val: int = 0
     n_pos: int = 0
     groups_retained: int = 0
     status: int = 0
 
-    DTYPE = np.dtype([("sum", "<f8"), ("sumsq", "<f8"), ("n_units", "<i8"), ("n_adv", "<i8"),
+    DTYPE = np.dtype([("mean", "<f8"), ("m2", "<f8"), ("flags", "<i8"), ("n_adv", "<i8"),
                       ("n_val", "<i8"), ("n_pos", "<i8"), ("groups_retained", "<i8"),
                       ("status", "<i8")])
 
@@ -64,15 +65,23 @@ class StatsRecord:
         return a.tobytes()
 
     @classmethod
+    def from_bytes(cls, raw: bytes) -> "StatsRecord":
+        a = np.frombuffer(raw, cls.DTYPE, count=1)[0]
+        return cls(*(a[k].item() for k in cls.DTYPE.names))
+
+    @classmethod
     def from_units(cls, adv_units, n_val, n_pos, groups=0):
         a = np.asarray(adv_units, dtype=np.float64)
         n = a.size
-        return cls(float(a.sum()), float((a * a).sum()), n, n, int(n_val), int(n_pos), int(groups), 0)
+        mean = float(a.mean()) if n else 0.0
+        return cls(mean, float(((a - mean) ** 2).sum()) if n else 0.0, 0, n, int(n_val), int(n_pos),
+                   int(groups), 0)
 
 
 def merge_stats(records) -> dict:
     """Merges per-rank records in rank order with the same code the device uses
-    (ckrl_merge_stats_host: fp64 sums in rank order, then mean / population std + 1e-8)."""
+    (ckrl_merge_stats_host: Chan's pairwise moment update in rank order, then mean /
+    population std + 1e-8)."""
     raw = b"".join(r.to_bytes() if isinstance(r, StatsRecord) else bytes(r) for r in records)
     assert _lib.lib().ckrl_stats_record_bytes() == StatsRecord.DTYPE.itemsize
     buf = C.create_string_buffer(raw, len(raw))

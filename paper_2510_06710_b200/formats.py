@@ -15,10 +15,12 @@ def _np(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 
 
-def dump_slab(tokens, reward_f64, flags, episode_id) -> str:
+def dump_slab(tokens, reward_f64, flags, episode_id, first_env_id: int = 0) -> str:
     """dump_slab text of an SoA slab: tokens [E][Tc][C][M] (u8/i32), f64 rewards [E][Tc][C]
-    (e.g. the pipeline's reward_f64), flags, episode ids (uid & 0xffffffff, -1 frozen).
-    Tensors are read from wherever they live (device tensors are downloaded)."""
+    (e.g. the pipeline's reward_f64), flags, episode ids (uid & 0xffffffff, -1 frozen);
+    uids are (first_env_id + row) << 32 | id (a VecEnv partition / rank shard starting at
+    global env first_env_id, vec_env.cpp:94). Tensors are read from wherever they live
+    (device tensors are downloaded)."""
     tk = tokens.detach().cpu().numpy() if hasattr(tokens, "detach") else np.asarray(tokens)
     E, Tc, Cn, M = tk.shape
     td = _lib.DTYPE_U8 if tk.dtype == np.uint8 else _lib.DTYPE_I32
@@ -27,9 +29,10 @@ def dump_slab(tokens, reward_f64, flags, episode_id) -> str:
     p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
     n = C.c_size_t(0)
     f = _lib.lib().ckrl_dump_slab
-    _lib.check(f(E, Tc, Cn, M, td, p(tk), p(rw), p(fl), p(ids), None, 0, C.byref(n)))
+    _lib.check(f(E, Tc, Cn, M, td, p(tk), p(rw), p(fl), p(ids), first_env_id, None, 0, C.byref(n)))
     buf = C.create_string_buffer(n.value + 1)
-    _lib.check(f(E, Tc, Cn, M, td, p(tk), p(rw), p(fl), p(ids), buf, n.value + 1, C.byref(n)))
+    _lib.check(f(E, Tc, Cn, M, td, p(tk), p(rw), p(fl), p(ids), first_env_id, buf, n.value + 1,
+                 C.byref(n)))
     return buf.raw[:n.value].decode()
 
 

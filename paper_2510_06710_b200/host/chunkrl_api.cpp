@@ -113,11 +113,11 @@ struct DeviceSlab {
   DevBuf<int32_t> episode_id;
   // PPO batch
   DevBuf<uint8_t> counted;
-  DevBuf<float> adv, ret;
+  DevBuf<double> adv, ret;
   // GRPO batch + episode table
   DevBuf<int32_t> env_group, env_member, env_episode, env_group_size, group_counts;
   DevBuf<double> env_adv;
-  DevBuf<float> slot_weight;
+  DevBuf<double> slot_weight;
   DevBuf<uint8_t> slot_member;
   DevBuf<unsigned char> ws;
 
@@ -708,8 +708,8 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
   // The selected records as a compact [n][1] SoA view, read from the batch's views and
   // their StepRecords as they are now (the reference reads them live, losses.cpp:100-120).
   std::vector<int32_t> tok(n * P, 0), eid(n * C, -1);
-  std::vector<float> olp(n * P, 0.0f), rew(n * C, 0.0f), vs(n, 0.0f), vv(n * C, 0.0f), adv(n * U, 0.0f),
-      ret(n * U, 0.0f), hv(n * NV, 0.0f);
+  std::vector<float> olp(n * P, 0.0f), rew(n * C, 0.0f), vs(n, 0.0f), vv(n * C, 0.0f), hv(n * NV, 0.0f);
+  std::vector<double> adv(n * U, 0.0), ret(n * U, 0.0);
   std::vector<uint8_t> fl(n * C, 0), cnt(n * C, 0);
   std::vector<float> hl;
   if (!net.logits) {
@@ -737,8 +737,8 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
       }
     }
     for (int u = 0; u < U; ++u) {
-      adv[static_cast<std::size_t>(i) * U + u] = static_cast<float>(v.advantages.at(static_cast<std::size_t>(u)));
-      ret[static_cast<std::size_t>(i) * U + u] = static_cast<float>(v.returns.at(static_cast<std::size_t>(u)));
+      adv[static_cast<std::size_t>(i) * U + u] = v.advantages.at(static_cast<std::size_t>(u));
+      ret[static_cast<std::size_t>(i) * U + u] = v.returns.at(static_cast<std::size_t>(u));
     }
     if (!net.logits) {
       fill_record_logits(net, r, C, M, V, hl.data() + static_cast<std::size_t>(i) * P * V);
@@ -746,8 +746,9 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
     }
   }
   DevBuf<int32_t> stok, seid, dtok(n * P), deid(n * C);
-  DevBuf<float> solp, srew, svs, svv, sadv, sret, sboot(n * C), dolp(n * P), drew(n * C), dvs(n), dvv(n * C),
-      dboot(n * C), dadv(n * U), dret(n * U), dvals(n * NV);
+  DevBuf<float> solp, srew, svs, svv, sboot(n * C), dolp(n * P), drew(n * C), dvs(n), dvv(n * C),
+      dboot(n * C), dvals(n * NV);
+  DevBuf<double> sadv, sret, dadv(n * U), dret(n * U);
   DevBuf<uint8_t> sfl, scnt, dfl(n * C), dcnt(n * C);
   stok.upload(tok);
   seid.upload(eid);
@@ -787,13 +788,13 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
     // the gather runs over the full device slab; the batch arrays are refreshed from the
     // host views first (normalize_advantages / caller edits)
     std::vector<uint8_t> fc(nr * C, 0);
-    std::vector<float> fa(nr * U, 0.0f), fr(nr * U, 0.0f);
+    std::vector<double> fa(nr * U, 0.0), fr(nr * U, 0.0);
     for (std::size_t r = 0; r < nr; ++r) {
       const auto& v = batch.records[r];
       for (int j = 0; j < C; ++j) fc[r * C + j] = v.counted[static_cast<std::size_t>(j)] ? 1 : 0;
       for (int u = 0; u < U; ++u) {
-        fa[r * U + u] = static_cast<float>(v.advantages[static_cast<std::size_t>(u)]);
-        fr[r * U + u] = static_cast<float>(v.returns[static_cast<std::size_t>(u)]);
+        fa[r * U + u] = v.advantages[static_cast<std::size_t>(u)];
+        fr[r * U + u] = v.returns[static_cast<std::size_t>(u)];
       }
     }
     d.counted.upload(fc);
@@ -985,6 +986,9 @@ std::string dump_slab(const TrajectorySlab& slab) {
   std::vector<int32_t> tok(S * M), ids(S);
   std::vector<double> rw(S);
   std::vector<uint8_t> fl(S);
+  // the SoA keeps uid & 0xffffffff; the high word is the global env id first_env_id + row
+  // (vec_env.cpp:94), recovered from the first live uid and checked for every slot
+  int64_t first_env = -1;
   for (int e = 0; e < E; ++e)
     for (int t = 0; t < Tc; ++t) {
       const StepRecord& rec = slab.records[static_cast<std::size_t>(e)][static_cast<std::size_t>(t)];
@@ -998,13 +1002,20 @@ std::string dump_slab(const TrajectorySlab& slab) {
                                      (rec.valid[jj] ? CKRL_FLAG_VALID : 0));
         const std::int64_t uid = rec.episode_uid[jj];
         ids[s] = uid < 0 ? -1 : static_cast<int32_t>(uid & 0xffffffff);
+        if (uid >= 0) {
+          const int64_t env = (uid >> 32) - e;
+          if (first_env < 0) first_env = env;
+          if (env != first_env || env < 0)
+            throw ConfigError("dump_slab: episode uids must be (first_env_id + env) << 32 | k");
+        }
       }
     }
+  const int32_t off = first_env < 0 ? 0 : static_cast<int32_t>(first_env);
   std::size_t n = 0;
-  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(), nullptr,
-                                0, &n));
+  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(), off,
+                                nullptr, 0, &n));
   std::string out(n, '\0');
-  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(),
+  throw_if_error(ckrl_dump_slab(E, Tc, C, M, CKRL_DTYPE_I32, tok.data(), rw.data(), fl.data(), ids.data(), off,
                                 out.data(), n, &n));
   return out;
 }

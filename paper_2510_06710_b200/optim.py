@@ -84,8 +84,9 @@ def ppo_loss_minibatch(rollout: RolloutBuffer, policy: PolicyOutputs, batch: Ppo
                         bootstrap=torch.empty((n, 1, Cn), **f32), vocab=V)
     ws = Workspace(n, 1, dev)
     sb = PpoBatch(spec=spec, counted=torch.empty((n, 1, Cn), dtype=torch.uint8, device=dev),
-                  advantages=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), **f32),
-                  returns=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), **f32), workspace=ws)
+                  advantages=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), dtype=torch.float64, device=dev),
+                  returns=torch.empty((n, 1, ulen) if ulen > 1 else (n, 1), dtype=torch.float64, device=dev),
+                  workspace=ws)
     sp = PolicyOutputs(torch.empty((n, 1, Cn, M, V), dtype=policy.logits.dtype, device=dev),
                        torch.empty((n, 1, vlen) if vlen > 1 else (n, 1), **f32)
                        if policy.values is not None else None)
@@ -135,8 +136,8 @@ class PpoStep:
         shape = (E, Tc) if spec.advantage_level == Level.Chunk else (E, Tc, Cn)
         self.batch = PpoBatch(spec=spec,
                               counted=torch.empty((E, Tc, Cn), dtype=torch.uint8, device=dev),
-                              advantages=torch.empty(shape, dtype=torch.float32, device=dev),
-                              returns=torch.empty(shape, dtype=torch.float32, device=dev),
+                              advantages=torch.empty(shape, dtype=torch.float64, device=dev),
+                              returns=torch.empty(shape, dtype=torch.float64, device=dev),
                               workspace=self.ws)
         self.outputs = LossOutputs.allocate(rollout, spec.value_level) if outputs else None
         self.diag = _diag_buffer(dev)

@@ -45,6 +45,20 @@ def test_dump_slab_golden_fixture():
     assert text == bytes(g["text"]).decode()
 
 
+def test_dump_slab_partition_keeps_global_env_ids():
+    """A VecEnv partition / rank shard whose first global env is 3 (vec_env.cpp:94): uids
+    carry the global env id in their high word, the env column stays the slab row."""
+    g = load_golden("dump_toyreach.npz")
+    want = []
+    for line in bytes(g["text"]).decode().splitlines(keepends=True):
+        f = line.split(" ")
+        if not line.startswith("#") and int(f[1]) >= 0:
+            f[1] = str(int(f[1]) + (3 << 32))
+        want.append(" ".join(f))
+    text = formats.dump_slab(g["tokens"], g["reward"], g["flags"], g["episode_id"], first_env_id=3)
+    assert text == "".join(want)
+
+
 def _desc_of(sc):
     cfg = sc.cfg
     return PolicyDescriptor(obs_dim=6 if cfg["env_kind"] == 0 else 2, hidden=cfg["hidden"],

@@ -91,8 +91,8 @@ def ppo_loss_case(spec, rho_log, adv, clip=0.2):
     d, logits, counted, a = ppo_case((int(spec.advantage_level), int(spec.logprob_level), int(spec.value_level)), rho_log, adv)
     ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], 3)
     ws = Workspace(1)
-    batch = PpoBatch(spec=spec, counted=dev(counted, torch.uint8), advantages=dev(a),
-                     returns=torch.zeros_like(dev(a)), workspace=ws)
+    batch = PpoBatch(spec=spec, counted=dev(counted, torch.uint8), advantages=dev(a, torch.float64),
+                     returns=torch.zeros_like(dev(a, torch.float64)), workspace=ws)
     # stats record for this hand-built batch: the assembly normally leaves it
     advantage.assemble_ppo_batch(ro, PpoAssemblyOptions(GaeParams(), GranularitySpec(spec.advantage_level, spec.logprob_level, spec.advantage_level)),
                                  workspace=ws)
