@@ -65,7 +65,7 @@ typedef enum {
 enum { CKRL_LEVEL_CHUNK = 0, CKRL_LEVEL_ACTION = 1, CKRL_LEVEL_TOKEN = 2 };
 enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3, CKRL_DTYPE_F64 = 4 };
 
-/* NCCL communicator of a multi-rank job (ckrl_comm_create, below). */
+/* Communicator of a multi-rank job: peer-memory exchange buffers (+ optional NCCL), below. */
 typedef struct ckrl_comm ckrl_comm;
 enum { CKRL_FLAG_TERMINATED = 1, CKRL_FLAG_TRUNCATED = 2, CKRL_FLAG_VALID = 4 };
 
@@ -179,8 +179,9 @@ const char* ckrl_last_error(void); /* thread-local message of the last failing c
 /* validate_granularity (core/granularity.cpp:47-60). */
 int32_t ckrl_validate_granularity(const ckrl_granularity* spec);
 
-/* Workspace bytes for a slab of this shape (whole step incl. cross-rank stats for
- * `world` ranks). Caller allocates device memory of at least this size once. */
+/* Workspace bytes for a slab of this shape (whole step; the cross-rank records live in the
+ * communicator, so `world` does not change the size). Caller allocates device memory of at
+ * least this size once. */
 size_t ckrl_workspace_bytes(int32_t num_envs, int32_t num_chunks, int32_t chunk_len,
                             int32_t tokens_per_action, int32_t world);
 
@@ -369,8 +370,10 @@ int32_t ckrl_grpo_loss(const ckrl_rollout* rollout, const ckrl_grpo_batch* batch
                        double* diag_device, void* workspace, size_t workspace_bytes,
                        ckrl_stream_t stream);
 
-/* Whole step (the measured hot path): assemble -> [stats allgather over `comm`] -> fused
- * loss. comm may be NULL (single rank). */
+/* Whole step (the measured hot path): assemble -> fused loss, two launches (the loss a
+ * programmatic dependent of the assembly). comm may be NULL (single rank); with a multi-rank
+ * comm the stats record and loss sums cross ranks inside the two kernels (see ckrl_comm_*
+ * below) and diag_device holds the job-wide diagnostics on every rank. */
 int32_t ckrl_ppo_step(const ckrl_rollout* rollout, const ckrl_policy_outputs* policy,
                       const ckrl_gae_params* gae, const ckrl_granularity* spec,
                       const ckrl_ppo_params* params, ckrl_ppo_batch* batch,
@@ -486,9 +489,28 @@ int32_t ckrl_save_checkpoint(const ckrl_policy_desc* desc, const double* params,
 int32_t ckrl_load_checkpoint(const char* path, ckrl_policy_desc* desc, double* params,
                              int64_t capacity, int64_t* count);
 
-/* ---- multi-GPU (NCCL over NVLink): stats + loss scalars only -------------------------- */
+/* ---- multi-GPU: stats record + loss scalars over NVLink peer memory ------------------------
+ * The path shards by env (PPO) / whole group (GRPO); its only cross-rank values are the
+ * 64-byte stats record before the loss (whitening moments, n_adv / n_val / n_pos, retained
+ * groups: optim/update.cpp:14-45, optim/losses.cpp:75-87, 246) and the raw loss sums after
+ * it (losses.cpp:221-227). Each rank owns a small exchange buffer in its HBM; inside
+ * ckrl_*_step the assembly kernel stores the rank's record into every rank's buffer and the
+ * loss kernel's last CTA does the same with its sums (P2P stores + system-scope flags), so a
+ * multi-rank step is the same two launches as a single-rank one. Every rank must run the
+ * same sequence of steps (the exchange is collective).
+ *
+ * ckrl_comm_create: a rank of a `world`-rank job on the current device; unique_id (from
+ * ckrl_comm_unique_id on one rank, 128 bytes) additionally creates an NCCL communicator,
+ * used only by a sharded ckrl_adam_step; NULL skips NCCL. Before the first step the peers'
+ * buffers must be mapped: across processes, all-gather every rank's ckrl_comm_ipc_handle
+ * (CUDA IPC, CKRL_IPC_HANDLE_BYTES each, rank order) and pass them to ckrl_comm_open_peers;
+ * in one process driving several ranks, ckrl_comm_set_peers with the ranks' communicators. */
+#define CKRL_IPC_HANDLE_BYTES 64
 int32_t ckrl_comm_unique_id(void* out_id /* 128 bytes */);
 int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out);
+int32_t ckrl_comm_ipc_handle(ckrl_comm* comm, void* out_handle /* CKRL_IPC_HANDLE_BYTES */);
+int32_t ckrl_comm_open_peers(ckrl_comm* comm, const void* handles /* world x CKRL_IPC_HANDLE_BYTES */);
+int32_t ckrl_comm_set_peers(ckrl_comm* comm, ckrl_comm* const* comms /* [world], rank order */);
 int32_t ckrl_comm_destroy(ckrl_comm* comm);
 
 #if defined(__GNUC__)

@@ -170,6 +170,9 @@ SIGNATURES = {
                                       vp]),
     "ckrl_comm_unique_id": (C.c_int32, [vp]),
     "ckrl_comm_create": (C.c_int32, [C.c_int32, C.c_int32, vp, P(vp)]),
+    "ckrl_comm_ipc_handle": (C.c_int32, [vp, vp]),
+    "ckrl_comm_open_peers": (C.c_int32, [vp, vp]),
+    "ckrl_comm_set_peers": (C.c_int32, [vp, P(vp)]),
     "ckrl_comm_destroy": (C.c_int32, [vp]),
 }
 

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -175,9 +176,39 @@ NcclApi& nccl() {
 }  // namespace
 
 struct ckrl_comm {
-  ncclComm_t nc;
-  int world, rank;
+  ncclComm_t nc = nullptr;          // optional (Adam's gradient-norm all-reduce)
+  int world = 1, rank = 0, device = 0;
+  char* xbuf = nullptr;             // this rank's exchange buffer (ex_buffer_bytes(world))
+  char** peers_dev = nullptr;       // device table: every rank's exchange buffer
+  std::vector<char*> ipc_opened;    // peers' buffers mapped with cudaIpcOpenMemHandle
+  bool ready = false;               // peers opened
+  int co_resident = 1;              // ranks of this job on this device (test / debug setups)
 };
+
+namespace {
+// Several ranks on one device (a single-GPU test of the multi-rank path): every rank's loss
+// kernel spins until all ranks' records arrive, so all of them must be resident at once —
+// each rank's persistent loss grid takes an equal share of the SMs, minus one SM per rank
+// for the assembly kernels.
+int loss_cta_cap(const ckrl_comm* c) {
+  if (!c || c->co_resident <= 1) return 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int cap = (sms - c->co_resident) / c->co_resident;
+  return cap > 1 ? cap : 1;
+}
+
+ckrl::ExchangeView exchange_view(const ckrl_comm* c) {
+  ckrl::ExchangeView x{};
+  if (c && c->world > 1) {
+    x.peers = c->peers_dev;
+    x.local = c->xbuf;
+    x.world = c->world;
+    x.rank = c->rank;
+  }
+  return x;
+}
+}  // namespace
 
 #define CKRL_NCCL(x)                                                                    \
   do {                                                                                  \
@@ -413,6 +444,8 @@ int32_t ckrl_adam_step(int32_t dtype, int64_t n, void* params, void* grad, void*
   const double bc1 = 1.0 - std::pow(p->beta1, (double)t), bc2 = 1.0 - std::pow(p->beta2, (double)t);
   CKRL_CUDA(launch_adam_norm(f64, grad, n, ws, s));
   const bool shard = comm && comm->world > 1;
+  CKRL_REQUIRE(!shard || comm->nc, CKRL_ERR_INVALID_ARGUMENT,
+               "a sharded Adam step needs an NCCL communicator (ckrl_comm_create with a unique id)");
   if (shard)
     CKRL_NCCL(nccl().AllReduce(adam_norm_sq_slot(ws), adam_norm_sq_slot(ws), 1, ncclFloat64, ncclSum,
                                comm->nc, s));
@@ -558,8 +591,11 @@ static int32_t grpo_loss_impl(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
                               const ckrl_policy_outputs* po, const ckrl_granularity* spec,
                               const ckrl_grpo_params* p, ckrl_loss_outputs* out, double* diag,
                               void* ws, int world, const StatsRecord* recs, int finalize,
-                              cudaStream_t s, int pdl = 0) {
+                              cudaStream_t s, int pdl = 0, const ExchangeView& ex = ExchangeView{},
+                              int max_ctas = 0) {
   LossArgs a = base_args(ro, po, (char*)ws, world);
+  a.ex = ex;
+  a.max_ctas = max_ctas;
   if (pdl) {  // programmatic dependent of the GRPO assembly (grpo_weights_kernel)
     a.pdl = 1;
     a.ro = *ro;
@@ -604,13 +640,23 @@ int32_t ckrl_grpo_loss(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
                         (cudaStream_t)stream);
 }
 
-// Exchange the rank-local stats record (before the loss) over NCCL.
-static int32_t gather_stats(ckrl_comm* comm, char* ws, const WsLayout& L, cudaStream_t s) {
-  CKRL_NCCL(nccl().AllGather(ws + L.stats_local, ws + L.stats_all, sizeof(StatsRecord), ncclUint8,
-                             comm->nc, s));
+static int32_t check_comm(const ckrl_comm* comm) {
+  if (comm && comm->world > 1 && !comm->ready)
+    return fail(CKRL_ERR_INVALID_ARGUMENT,
+                "communicator peers not opened (ckrl_comm_open_peers / ckrl_comm_set_peers)");
+  if (comm && comm->world > 1) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != comm->device) return fail(CKRL_ERR_INVALID_ARGUMENT, "communicator belongs to another device");
+  }
   return CKRL_OK;
 }
 
+// The whole step. Multi-rank (comm->world > 1): the assembly kernel's last CTA stores the
+// rank's stats record into every rank's exchange buffer (NVLink P2P stores) and the loss
+// kernel -- still the assembly's programmatic dependent, streaming logits from the start --
+// waits for all records before its first unit phase; its last CTA exchanges the raw loss
+// sums the same way and finalises the diagnostics. No NCCL kernel and no extra launch.
 int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
                       const ckrl_gae_params* gae, const ckrl_granularity* spec,
                       const ckrl_ppo_params* p, ckrl_ppo_batch* b, ckrl_loss_outputs* out,
@@ -623,6 +669,7 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, true))) return st;
   if ((st = check_policy(ro, po))) return st;
+  if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
   CKRL_REQUIRE(gae && p && b && diag && b->counted && b->advantages && b->returns,
@@ -632,10 +679,11 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
   cudaStream_t s = (cudaStream_t)stream;
   WsLayout L = ws_layout(ro->num_envs, world);
   char* w = (char*)ws;
+  const ExchangeView ex = exchange_view(comm);
+  const StatsRecord* local = reinterpret_cast<const StatsRecord*>(w + L.stats_local);
   if (world == 1 && fused_enabled() && !(out && out->dlogits)) {
     // one persistent launch: GAE assembly overlapped with the logits stream
-    LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
-                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1);
+    LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1, local, 1);
     a.ro = *ro;
     a.gamma = gae->gamma;
     a.lambda = gae->lambda;
@@ -644,40 +692,18 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
     if (e != cudaErrorNotSupported) return fail(CKRL_ERR_CUDA, std::string("fused step: ") + cudaGetErrorString(e));
     cudaGetLastError();
   }
-  if (world == 1 && overlap_sms() > 0 && po->logits_dtype >= 0) {
-    // Overlapped step: assembly on `overlap_sms()` SMs, the loss kernel launched as its
-    // programmatic dependent on the others — logits stream while the GAE scan runs.
-    const int rs = overlap_sms();
-    CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
-                                  gae->lambda, *b, w, L, s, rs));
-    LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
-                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1);
-    a.pdl = 1;
-    a.reserved_sms = 0;
-    (void)rs;
-    a.ro = *ro;
-    CKRL_CUDA(launch_tile(a, s, nullptr));
-    return CKRL_OK;
-  }
   CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma,
-                                gae->lambda, *b, w, L, s));
-  if (world == 1)
-    return ppo_loss_impl(ro, b, po, spec, p, out, diag, ws, 1,
-                         reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s);
-  if ((st = gather_stats(comm, w, L, s))) return st;
-  if ((st = ppo_loss_impl(ro, b, po, spec, p, out, diag, ws, world,
-                          reinterpret_cast<const StatsRecord*>(w + L.stats_all), 0, s)))
-    return st;
-  CKRL_NCCL(nccl().AllReduce(w + L.loss_raw, w + L.loss_raw, RAW_COUNT, ncclFloat64, ncclSum,
-                             comm->nc, s));
-  LossArgs a = base_args(ro, po, w, world);
-  a.mode = MODE_PPO;
-  a.vcoef = p->value_loss_coef;
-  a.ecoef = p->entropy_coef;
-  a.normalize = p->advantage_normalization;
-  a.recs = reinterpret_cast<const StatsRecord*>(w + L.stats_all);
-  a.diag = diag;
-  CKRL_CUDA(launch_finalize(a, s));
+                                gae->lambda, *b, w, L, s, ex));
+  // the loss as the assembly's programmatic dependent: logits stream while the GAE scan
+  // runs; the unit phases start once the assembly's outputs (and every rank's record) exist
+  LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1, local, 1);
+  a.ex = ex;
+  a.max_ctas = loss_cta_cap(comm);
+  if (overlap_sms() > 0 && po->logits_dtype >= 0) {
+    a.pdl = 1;
+    a.ro = *ro;
+  }
+  CKRL_CUDA(launch_tile(a, s, nullptr));
   return CKRL_OK;
 }
 
@@ -691,6 +717,7 @@ int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
   if ((st = check_policy(ro, po))) return st;
+  if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
   CKRL_REQUIRE(ep && opt && p && gb && diag, CKRL_ERR_INVALID_ARGUMENT,
@@ -698,23 +725,11 @@ int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
   cudaStream_t s = (cudaStream_t)stream;
   WsLayout L = ws_layout(ro->num_envs, world);
   char* w = (char*)ws;
-  CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, w, L, s));
-  if (world == 1)
-    return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
-                          reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s,
-                          overlap_sms() > 0 && po->logits_dtype >= 0);
-  if ((st = gather_stats(comm, w, L, s))) return st;
-  if ((st = grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, world,
-                           reinterpret_cast<const StatsRecord*>(w + L.stats_all), 0, s)))
-    return st;
-  CKRL_NCCL(nccl().AllReduce(w + L.loss_raw, w + L.loss_raw, RAW_COUNT, ncclFloat64, ncclSum,
-                             comm->nc, s));
-  LossArgs a = base_args(ro, po, w, world);
-  a.mode = MODE_GRPO;
-  a.recs = reinterpret_cast<const StatsRecord*>(w + L.stats_all);
-  a.diag = diag;
-  CKRL_CUDA(launch_finalize(a, s));
-  return CKRL_OK;
+  const ExchangeView ex = exchange_view(comm);
+  CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, w, L, s, ex));
+  return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
+                        reinterpret_cast<const StatsRecord*>(w + L.stats_local), 1, s,
+                        overlap_sms() > 0 && po->logits_dtype >= 0, ex, loss_cta_cap(comm));
 }
 
 int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream) {
@@ -902,26 +917,110 @@ int32_t ckrl_comm_unique_id(void* out_id) {
 }
 
 int32_t ckrl_comm_create(int32_t world, int32_t rank, const void* unique_id, ckrl_comm** out) {
-  CKRL_REQUIRE(out && unique_id && world >= 1 && world <= kMaxRanks && rank >= 0 && rank < world,
+  CKRL_REQUIRE(out && world >= 1 && world <= kMaxRanks && rank >= 0 && rank < world,
                CKRL_ERR_INVALID_ARGUMENT, "bad communicator arguments");
-  if (!nccl().ok) return fail(CKRL_ERR_NCCL, "NCCL library not found");
-  ncclUniqueId id;
-  std::memcpy(&id, unique_id, sizeof(id));
+  int32_t st = check_device();
+  if (st) return st;
   ckrl_comm* c = new ckrl_comm;
   c->world = world;
   c->rank = rank;
-  ncclResult_t r = nccl().CommInitRank(&c->nc, world, id, rank);
-  if (r != ncclSuccess) {
-    delete c;
-    return fail(CKRL_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+  cudaGetDevice(&c->device);
+  const size_t xb = ex_buffer_bytes(world);
+  cudaError_t e = cudaMalloc(&c->xbuf, xb);
+  if (e == cudaSuccess) e = cudaMemset(c->xbuf, 0, xb);
+  if (e == cudaSuccess) e = cudaMalloc(&c->peers_dev, sizeof(char*) * (size_t)world);
+  if (e != cudaSuccess) {
+    ckrl_comm_destroy(c);
+    return fail(CKRL_ERR_CUDA, std::string("exchange buffer: ") + cudaGetErrorString(e));
+  }
+  if (world == 1) c->ready = true;
+  if (unique_id) {  // NCCL communicator too (Adam's sharded gradient norm)
+    if (!nccl().ok) {
+      ckrl_comm_destroy(c);
+      return fail(CKRL_ERR_NCCL, "NCCL library not found");
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclResult_t r = nccl().CommInitRank(&c->nc, world, id, rank);
+    if (r != ncclSuccess) {
+      c->nc = nullptr;
+      ckrl_comm_destroy(c);
+      return fail(CKRL_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+    }
   }
   *out = c;
   return CKRL_OK;
 }
 
+int32_t ckrl_comm_ipc_handle(ckrl_comm* comm, void* out_handle) {
+  CKRL_REQUIRE(comm && out_handle, CKRL_ERR_INVALID_ARGUMENT, "communicator / handle buffer required");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CKRL_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CKRL_CUDA(cudaIpcGetMemHandle(&h, comm->xbuf));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return CKRL_OK;
+}
+
+static int32_t install_peers(ckrl_comm* c, const std::vector<char*>& ptrs, int co_resident) {
+  CKRL_CUDA(cudaMemcpy(c->peers_dev, ptrs.data(), sizeof(char*) * ptrs.size(), cudaMemcpyHostToDevice));
+  c->co_resident = co_resident;
+  c->ready = true;
+  return CKRL_OK;
+}
+
+int32_t ckrl_comm_open_peers(ckrl_comm* comm, const void* handles) {
+  CKRL_REQUIRE(comm && handles, CKRL_ERR_INVALID_ARGUMENT, "communicator / handles required");
+  CKRL_REQUIRE(!comm->ready || comm->world == 1, CKRL_ERR_INVALID_ARGUMENT, "peers already opened");
+  std::vector<char*> ptrs((size_t)comm->world, nullptr);
+  const cudaIpcMemHandle_t* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  int same = 1;
+  for (int q = 0; q < comm->world; ++q) {
+    if (q == comm->rank) {
+      ptrs[q] = comm->xbuf;
+      continue;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hs[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(CKRL_ERR_CUDA, "cudaIpcOpenMemHandle(rank " + std::to_string(q) + "): " + cudaGetErrorString(e));
+    comm->ipc_opened.push_back((char*)p);
+    ptrs[q] = (char*)p;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.device == comm->device) ++same;
+    cudaGetLastError();
+  }
+  return install_peers(comm, ptrs, same);
+}
+
+int32_t ckrl_comm_set_peers(ckrl_comm* comm, ckrl_comm* const* comms) {
+  CKRL_REQUIRE(comm && comms, CKRL_ERR_INVALID_ARGUMENT, "communicator / peers required");
+  std::vector<char*> ptrs((size_t)comm->world, nullptr);
+  int same = 0;
+  for (int q = 0; q < comm->world; ++q) {
+    CKRL_REQUIRE(comms[q] && comms[q]->world == comm->world && comms[q]->rank == q,
+                 CKRL_ERR_INVALID_ARGUMENT, "peer communicators must be ranks 0..world-1 of one world");
+    if (comms[q]->device != comm->device) {  // one process driving several GPUs: direct P2P
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaSetDevice(comm->device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(comms[q]->device, 0);
+      cudaSetDevice(dev);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(CKRL_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    ptrs[q] = comms[q]->xbuf;
+    same += comms[q]->device == comm->device;
+  }
+  return install_peers(comm, ptrs, same);
+}
+
 int32_t ckrl_comm_destroy(ckrl_comm* comm) {
   if (!comm) return CKRL_OK;
-  if (nccl().ok) nccl().CommDestroy(comm->nc);
+  if (comm->nc && nccl().ok) nccl().CommDestroy(comm->nc);
+  for (char* p : comm->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (comm->peers_dev) cudaFree(comm->peers_dev);
+  if (comm->xbuf) cudaFree(comm->xbuf);
   delete comm;
   return CKRL_OK;
 }

@@ -15,7 +15,7 @@ namespace ckrl {
 
 // Last-block reduction of the per-CTA assembly partials into the rank's StatsRecord
 // (fixed order: thread t sums partials t, t+nthr, ...; then a fixed tree).
-__device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, int M) {
+__device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, int M, const ExchangeView& ex) {
   __shared__ bool is_last;
   __shared__ AsmPartial wpart[32];  // any block size up to 1024
   AsmPartial* parts = reinterpret_cast<AsmPartial*>(ws + L.asm_partials);
@@ -72,6 +72,7 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   st->groups_retained = 0;
   st->status = 0;
   tickets[TICKET_ASM] = 0;  // self-reset for the next launch
+  if (ex.world > 1) ex_publish_stats(ex, *st);  // to every rank's exchange buffer (NVLink stores)
 }
 
 // Two schedules: thread-per-env serial walk (short envs: <= kSerialItems items, the common
@@ -85,7 +86,7 @@ template <bool SERIAL>
 // the loss kernel's persistent CTAs all start at once under programmatic dependent launch.
 __global__ void __launch_bounds__(32 * kAsmWarpsPerCta, 12)
 ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lambda,
-                    uint8_t* counted, double* adv, double* ret, char* ws, WsLayout L) {
+                    uint8_t* counted, double* adv, double* ret, char* ws, WsLayout L, ExchangeView ex) {
   asm volatile("griddepcontrol.launch_dependents;");
   __shared__ GaeSums wsum[kAsmWarpsPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -116,7 +117,7 @@ ppo_assemble_kernel(ckrl_rollout ro, int action_level, double gamma, double lamb
       p.m = mom_merge(p.m, wsum[w].m);
       p.n_pos += wsum[w].counted_slots;
     }
-  finish_asm_stats(p, ws, L, ro.tokens_per_action);
+  finish_asm_stats(p, ws, L, ro.tokens_per_action, ex);
 }
 
 __global__ void flat_gae_kernel(int num_seqs, const int32_t* offs, const double* r,
@@ -218,7 +219,7 @@ constexpr int kGrpoThreads = 1024;
 
 __global__ void __launch_bounds__(kGrpoThreads)
 grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_grpo_batch gb,
-                  char* ws, WsLayout L) {
+                  char* ws, WsLayout L, ExchangeView ex) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int scan_scratch[kGrpoThreads / 32 + 1];
   __shared__ int s_n, s_status, s_groups, s_total, s_retained;
@@ -253,9 +254,9 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   const int n = s_n;
   if (n > kGrpoMaxEligible) {
     if (tid == 0) {
-      st->status = CKRL_ERR_INVALID_ARGUMENT;
-      st->groups_retained = 0;
+      *st = StatsRecord{0.0, 0.0, 0, 0, 0, 0, 0, CKRL_ERR_INVALID_ARGUMENT};
       gb.group_counts[0] = gb.group_counts[1] = 0;
+      if (ex.world > 1) ex_publish_stats(ex, *st);  // peers must not wait for a record
     }
     return;
   }
@@ -388,6 +389,7 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
     st->n_adv = st->n_val = st->n_pos = 0;
     st->groups_retained = s_retained;
     st->status = s_status;
+    if (ex.world > 1) ex_publish_stats(ex, *st);  // to every rank's exchange buffer
   }
 }
 
@@ -452,7 +454,7 @@ static bool serial_gae_enabled() {  // thread-per-env schedule (measured slower;
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
                                 double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
-                                cudaStream_t s, int /*reserved_sms*/) {
+                                cudaStream_t s, const ExchangeView& ex) {
   // The overlapped step's loss kernel (one ~217 KB-smem CTA per SM) starts while this runs:
   // an SM whose L1/shared split was configured for this kernel's small footprint cannot take
   // the loss CTA until it drains and reconfigures, so ask for the maximum carveout here too.
@@ -467,11 +469,11 @@ cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double
     const int nt = 32 * kAsmWarpsPerCta;
     const int grid = (ro.num_envs + nt - 1) / nt;
     ppo_assemble_kernel<true><<<grid > 0 ? grid : 1, nt, 0, s>>>(
-        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
+        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L, ex);
   } else {
     const int grid = (ro.num_envs + kAsmWarpsPerCta - 1) / kAsmWarpsPerCta;
     ppo_assemble_kernel<false><<<grid > 0 ? grid : 1, 32 * kAsmWarpsPerCta, 0, s>>>(
-        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L);
+        ro, action_level, gamma, lambda, b.counted, b.advantages, b.returns, ws, L, ex);
   }
   return cudaGetLastError();
 }
@@ -497,14 +499,14 @@ cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uin
 
 cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep,
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
-                                 const WsLayout& L, cudaStream_t s) {
+                                 const WsLayout& L, cudaStream_t s, const ExchangeView& ex) {
   size_t smem = (size_t)kGrpoMaxEligible * 16 + sizeof(int32_t) * (kGrpoMaxEligible + 1);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(grpo_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  grpo_group_kernel<<<1, kGrpoThreads, smem, s>>>(ep, ro.num_envs, opt, gb, ws, L);
+  grpo_group_kernel<<<1, kGrpoThreads, smem, s>>>(ep, ro.num_envs, opt, gb, ws, L, ex);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   // programmatic dependent of the group kernel: its CTAs are resident (and trigger the loss
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
   }
   // thread 0 holds the CTA's partial; finish_asm_stats reads it from thread 0
   mine.m = mom.get();
-  finish_asm_stats(mine, a.ws, a.L, M);
+  finish_asm_stats(mine, a.ws, a.L, M, ExchangeView{});
 }
 
 cudaError_t launch_select_records(const ckrl_rollout& src, const ckrl_ppo_batch& sb, const ckrl_policy_outputs& sp,

@@ -74,23 +74,117 @@ enum { STATS_WHITENED = 1 };
 // Raw loss sums (reduced across CTAs, then across ranks) before normalisation.
 enum { RAW_SURR = 0, RAW_VALSQ, RAW_ENT, RAW_KL, RAW_CLIPPED, RAW_LPUNITS, RAW_COUNT = 8 };
 
+// ---- cross-rank exchange over peer memory (NVLink P2P stores) ----------------------------
+// Every rank owns one exchange buffer in its own HBM: a header (the rank's step epoch) and,
+// per epoch parity, one slot per rank. A producer (the assembly's last CTA for the stats
+// record, the loss's last CTA for the raw loss sums) stores its data into slot [p][rank] of
+// EVERY rank's buffer, fences at system scope, then stores the epoch into that slot's flag;
+// consumers spin (acquire, system scope) on the flags of their own buffer only, so every
+// wait is a local-HBM poll and every transfer a remote store. Two parities: rank q can only
+// reach epoch e+2's stores after every rank has finished reading epoch e (the loss tail of
+// e+1 needs every rank's e+1 sums, posted after its e reads).
+struct ExSlot {
+  StatsRecord rec;                 // the producer rank's stats record
+  double raw[RAW_COUNT];           // its raw loss sums (before normalisation)
+  unsigned long long stats_epoch;  // == epoch once rec is visible
+  unsigned long long raw_epoch;    // == epoch once raw is visible
+  unsigned long long pad[14];
+};
+static_assert(sizeof(ExSlot) == 256, "exchange slot is 256 bytes");
+constexpr size_t kExHeader = 256;  // [0]: the rank's epoch counter (u64)
+__host__ __device__ inline size_t ex_buffer_bytes(int world) {
+  return kExHeader + 2 * (size_t)world * sizeof(ExSlot);
+}
+// Kernel-side view of a rank's exchange (world == 0: single rank, no exchange).
+struct ExchangeView {
+  char* const* peers;          // device array [world]: every rank's exchange buffer (peer-mapped)
+  char* local;                 // this rank's buffer (== peers[rank])
+  int world, rank;
+};
+__host__ __device__ inline ExSlot* ex_slots(char* buf, int world, unsigned long long epoch) {
+  return reinterpret_cast<ExSlot*>(buf + kExHeader) + (size_t)(epoch & 1ull) * world;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ex_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kExTimeoutNs = 20ull * 1000 * 1000 * 1000;  // a peer that never posts
+// Spin until *flag == e (own HBM, system-scope acquire); false after kExTimeoutNs.
+__device__ inline bool ex_wait(const unsigned long long* flag, unsigned long long e) {
+  if (ld_acquire_sys(flag) == e) return true;
+  const unsigned long long t0 = ex_now();
+  for (unsigned it = 1;; ++it) {
+    if (ld_acquire_sys(flag) == e) return true;
+    if ((it & 255u) == 0 && ex_now() - t0 > kExTimeoutNs) return false;
+    __nanosleep(64);
+  }
+}
+// Assembly side (one thread, after the rank's record is final): bump the epoch and store the
+// record into slot [p][rank] of every rank's buffer, then release the flags.
+static __device__ __noinline__ void ex_publish_stats(const ExchangeView& x, const StatsRecord& r) {
+  unsigned long long* ep = reinterpret_cast<unsigned long long*>(x.local);
+  const unsigned long long e = *ep + 1;
+  *ep = e;
+  for (int q = 0; q < x.world; ++q) ex_slots(x.peers[q], x.world, e)[x.rank].rec = r;
+  __threadfence_system();
+  for (int q = 0; q < x.world; ++q) st_release_sys(&ex_slots(x.peers[q], x.world, e)[x.rank].stats_epoch, e);
+}
+// The loss's last CTA (one thread): post the rank's raw sums, wait for every rank's, and sum
+// them in rank order (identical on every rank). False on a peer timeout.
+static __device__ __noinline__ bool ex_allreduce_raw(const ExchangeView& x, unsigned long long e, double* raw) {
+  for (int q = 0; q < x.world; ++q) {
+    ExSlot* s = ex_slots(x.peers[q], x.world, e) + x.rank;
+    for (int i = 0; i < RAW_COUNT; ++i) s->raw[i] = raw[i];
+  }
+  __threadfence_system();
+  for (int q = 0; q < x.world; ++q) st_release_sys(&ex_slots(x.peers[q], x.world, e)[x.rank].raw_epoch, e);
+  ExSlot* mine = ex_slots(x.local, x.world, e);
+  double tot[RAW_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool ok = true;
+  for (int q = 0; q < x.world && ok; ++q) {
+    ok = ex_wait(&mine[q].raw_epoch, e);
+    for (int i = 0; i < RAW_COUNT; ++i) tot[i] += ok ? mine[q].raw[i] : 0.0;
+  }
+  for (int i = 0; i < RAW_COUNT; ++i) raw[i] = tot[i];
+  return ok;
+}
+#endif
+
 // Whitening parameters from merged moments: mean, population std + 1e-8 (update.cpp:33-43).
 __host__ __device__ inline void whitening(const Moments& m, double* mean, double* denom) {
   const double var = m.n > 0.0 ? m.m2 / m.n : 0.0;
   *mean = m.n > 0.0 ? m.mean : 0.0;
   *denom = sqrt(var) + 1e-8;
 }
-// Fixed rank-order merge of `world` records.
-__host__ __device__ inline Moments merge_records(const StatsRecord* r, int world) {
+// Fixed rank-order merge of `world` records `stride` bytes apart (contiguous records, or the
+// stats records of a rank's exchange slots).
+__host__ __device__ inline const StatsRecord& rec_at(const StatsRecord* r, size_t stride, int i) {
+  return *reinterpret_cast<const StatsRecord*>(reinterpret_cast<const char*>(r) + stride * (size_t)i);
+}
+__host__ __device__ inline Moments merge_records(const StatsRecord* r, int world,
+                                                 size_t stride = sizeof(StatsRecord)) {
   Moments m{0.0, 0.0, 0.0};
-  for (int i = 0; i < world; ++i) m = mom_merge(m, Moments{(double)r[i].n_adv, r[i].mean, r[i].m2});
+  for (int i = 0; i < world; ++i) {
+    const StatsRecord& q = rec_at(r, stride, i);
+    m = mom_merge(m, Moments{(double)q.n_adv, q.mean, q.m2});
+  }
   return m;
 }
 
 // Workspace carve-up (all offsets 256-byte aligned). Must match ckrl_workspace_bytes.
 struct WsLayout {
   size_t stats_local;   // StatsRecord
-  size_t stats_all;     // StatsRecord[world] (last: the only world-dependent region)
   size_t tickets;       // uint32[8] last-block counters (self-resetting)
   size_t loss_raw;      // double[RAW_COUNT]
   size_t asm_partials;  // AsmPartial per assembly CTA
@@ -116,15 +210,15 @@ __host__ __device__ inline WsLayout ws_layout(int E, int world) {
   };
   int asm_ctas = (E + kAsmWarpsPerCta - 1) / kAsmWarpsPerCta;
   if (asm_ctas < kMaxLossCtas) asm_ctas = kMaxLossCtas;  // also the fused step's CTA partials
-  // every world-independent region first (fixed offsets whatever `world` a workspace is
-  // used with); the all-gathered records last
+  // no region depends on `world`: the cross-rank records live in the communicator's
+  // exchange buffer, so one workspace serves any world size
+  (void)world;
   L.stats_local = take(sizeof(StatsRecord));
   L.tickets = take(sizeof(uint32_t) * 8);
   L.loss_raw = take(sizeof(double) * RAW_COUNT);
   L.asm_partials = take(sizeof(AsmPartial) * (size_t)asm_ctas);
   L.loss_partials = take(sizeof(double) * RAW_COUNT * kMaxLossCtas);
   L.grpo_env = take(sizeof(int32_t) * 2 * (size_t)(E < 1 ? 1 : E));
-  L.stats_all = take(sizeof(StatsRecord) * (size_t)(world < 1 ? 1 : world));
   L.total = off;
   return L;
 }

@@ -42,13 +42,15 @@ struct LossArgs {
   double* action_lp;
   double* chunk_lp;
   int all_rows;  // evaluate every row (token outputs requested / MODE_STATS)
-  // cross-rank stats
+  // stats: the rank's own record (single rank), or every rank's through the exchange
   const StatsRecord* recs;
   int world;
+  ExchangeView ex;   // ex.world > 1: records and raw sums cross ranks over peer memory
+  int max_ctas;      // > 0: loss grid cap (several ranks of one job share this device)
   char* ws;
   WsLayout L;
-  double* diag;      // finalised diagnostics (world == 1); raw sums go to ws.loss_raw
-  int finalize;      // 1: last CTA finalises into diag; 0: leave raw sums for an allreduce
+  double* diag;      // finalised diagnostics; raw sums also go to ws.loss_raw
+  int finalize;      // 1: last CTA finalises into diag
   // fused PPO step (assembly inside the loss launch)
   ckrl_rollout ro;
   double gamma, lambda;
@@ -64,7 +66,7 @@ struct LossArgs {
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
                                 double lambda, ckrl_ppo_batch& b, char* ws, const WsLayout& L,
-                                cudaStream_t s, int reserved_sms = 0);
+                                cudaStream_t s, const ExchangeView& ex = ExchangeView{});
 cudaError_t launch_flat_gae(int num_seqs, const int32_t* offs, const double* r, const double* v,
                             const double* b, const uint8_t* f, double gamma, double lambda,
                             double* adv, double* ret, cudaStream_t s);
@@ -72,7 +74,8 @@ cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uin
                              double* adv, StatsRecord* recs, int world, uint32_t* ticket, cudaStream_t s);
 cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep,
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
-                                 const WsLayout& L, cudaStream_t s);
+                                 const WsLayout& L, cudaStream_t s,
+                                 const ExchangeView& ex = ExchangeView{});
 cudaError_t launch_tile(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t debug_cta_times(uint64_t* out, int n);
 int32_t format_slab(int32_t E, int32_t Tc, int32_t C, int32_t M, int32_t token_dtype, const void* tokens,
@@ -91,7 +94,6 @@ cudaError_t launch_adam_update(int f64, void* p, void* g, void* m, void* v, int6
 cudaError_t launch_logits_grad(const void* logits, int logits_bf16, const void* tokens, int tok_i32,
                                const float* coeff_lp, const float* coeff_ent, int64_t rows, int V,
                                void* out, int out_bf16, int32_t* status, cudaStream_t s);
-cudaError_t launch_finalize(LossArgs& a, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
 cudaError_t read_timeline(uint64_t* out, int n);
 size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp);

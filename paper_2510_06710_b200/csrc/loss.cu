@@ -218,6 +218,7 @@ struct LossConsts {
   int do_norm;
   int64_t n_adv, groups;
   int status;
+  unsigned long long epoch;  // exchange epoch of this step (multi-rank)
 };
 
 __device__ __forceinline__ double drecip(double x) { return __drcp_rn(x); }  // == 1.0 / x (IEEE rn)
@@ -236,16 +237,32 @@ __device__ LossConsts consts_from(const Moments& mom, int64_t n_adv, int64_t n_v
   k.inv_denom = drecip(k.denom);
   k.inv_groups = groups > 0 ? drecip((double)groups) : 0.0;
   k.status = status;
+  k.epoch = 0;
   return k;
 }
 
 // Merge the per-rank stats records (fixed rank order) into the loss constants. Advantages
 // already whitened in place (ckrl_normalize_advantages) are used as they are.
-__device__ LossConsts merge_consts(const LossArgs& a) {
+// Multi-rank (a.ex.world > 1): the records are this step's exchange slots in the rank's own
+// buffer, waited for first (every rank's assembly stored its record there over NVLink).
+__device__ __noinline__ LossConsts merge_consts(const LossArgs& a) {
   int64_t n_val = 0, n_pos = 0, groups = 0, n_adv = 0;
   int status = 0, whitened = 0;
-  for (int r = 0; r < a.world; ++r) {
-    const StatsRecord& s = a.recs[r];
+  const StatsRecord* recs = a.recs;
+  int world = a.world;
+  size_t stride = sizeof(StatsRecord);
+  unsigned long long e = 0;
+  if (a.ex.world > 1) {
+    e = *reinterpret_cast<const unsigned long long*>(a.ex.local);  // this step's epoch
+    ExSlot* sl = ex_slots(a.ex.local, a.ex.world, e);
+    for (int q = 0; q < a.ex.world; ++q)
+      if (!ex_wait(&sl[q].stats_epoch, e)) status = CKRL_ERR_NCCL;  // a peer never posted
+    recs = &sl[0].rec;
+    world = a.ex.world;
+    stride = sizeof(ExSlot);
+  }
+  for (int r = 0; r < world; ++r) {
+    const StatsRecord& s = rec_at(recs, stride, r);
     n_adv += s.n_adv;
     n_val += s.n_val;
     n_pos += s.n_pos;
@@ -253,8 +270,10 @@ __device__ LossConsts merge_consts(const LossArgs& a) {
     whitened |= (int)(s.flags & STATS_WHITENED);
     if (s.status && !status) status = (int)s.status;
   }
-  return consts_from(merge_records(a.recs, a.world), n_adv, n_val, n_pos, groups, status,
-                     a.normalize && !whitened);
+  LossConsts k = consts_from(merge_records(recs, world, stride), n_adv, n_val, n_pos, groups, status,
+                             a.normalize && !whitened);
+  k.epoch = e;
+  return k;
 }
 
 // One advantage unit: ratio, clipped surrogate (losses.cpp:32-46) and the approx-kl term
@@ -613,7 +632,14 @@ __device__ void reduce_and_finish(const LossArgs& a, const LossConsts& k, const 
   if (tid == 0) {
     CKRL_PROBE(g_timeline[30] = gtimer());  // probe: raw sums written
     tickets[TICKET_LOSS] = 0;
-    if (a.finalize) finalize_diag(a, k, s_tot, a.diag);
+    if (a.ex.world > 1) {  // cross-rank sum of the raw sums over peer memory (rank order)
+      LossConsts kk = k;
+      if (!ex_allreduce_raw(a.ex, k.epoch, s_tot) && !kk.status) kk.status = CKRL_ERR_NCCL;
+      for (int i = 0; i < RAW_COUNT; ++i) raw[i] = s_tot[i];
+      if (a.finalize) finalize_diag(a, kk, s_tot, a.diag);
+    } else if (a.finalize) {
+      finalize_diag(a, k, s_tot, a.diag);
+    }
     CKRL_PROBE(g_timeline[31] = gtimer());  // probe: finalised
   }
 }
@@ -1905,12 +1931,6 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
   CKRL_PROBE(if (tid == 0 && blockIdx.x < 1184) g_cta_times[2][blockIdx.x] = gtimer());
 }
 
-__global__ void finalize_kernel(LossArgs a) {
-  if (threadIdx.x != 0) return;
-  LossConsts k = merge_consts(a);
-  finalize_diag(a, k, reinterpret_cast<double*>(a.ws + a.L.loss_raw), a.diag);
-}
-
 static int device_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1935,6 +1955,7 @@ static cudaError_t launch_direct(LossArgs& a, cudaStream_t s, int* grid_out) {
   int64_t grid = (int64_t)device_sms() * occ;
   if (grid > a.n_tiles) grid = a.n_tiles;
   if (grid > kMaxLossCtas) grid = kMaxLossCtas;
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = (int)grid;
   kern<<<(unsigned)grid, kLossThreads, smem, s>>>(a);
@@ -2014,6 +2035,7 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
   if (e != cudaSuccess) return e;
   int64_t grid = device_sms();
   if (grid > a.n_tiles) grid = a.n_tiles;
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = (int)grid;
   if (!FUSED && a.pdl) {  // programmatic dependent of the assembly kernel
@@ -2122,11 +2144,6 @@ cudaError_t read_timeline(uint64_t* out, int n) {
 
 cudaError_t debug_cta_times(uint64_t* out, int n) {
   return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(uint64_t) * (n < 3 * 1184 ? n : 3 * 1184));
-}
-
-cudaError_t launch_finalize(LossArgs& a, cudaStream_t s) {
-  finalize_kernel<<<1, 32, 0, s>>>(a);
-  return cudaGetLastError();
 }
 
 }  // namespace ckrl

@@ -3,8 +3,10 @@
 The path shards by environment (GAE segments never cross envs, assembler.cpp:108-193)
 and, for GRPO, by whole groups (GroupKey, assembler.cpp:207-226). The only exchanges are
 the 64-byte per-rank stats record before the loss (whitening moments + normalisers or the
-retained-group count) and the loss scalars after it — both inside ckrl_*_step on the
-caller's stream. torch.distributed only bootstraps the NCCL unique id.
+retained-group count) and the loss scalars after it — both inside the step's two kernels,
+as NVLink stores into every rank's exchange buffer (csrc/common.cuh ExSlot). torch.distributed
+only bootstraps the communicator: it all-gathers the buffers' CUDA IPC handles (and, for a
+sharded Adam step, broadcasts an NCCL unique id).
 """
 from __future__ import annotations
 
@@ -94,13 +96,14 @@ def merge_stats(records) -> dict:
 
 
 class Comm:
-    """Owns a ckrl_comm (an NCCL communicator over NVLink) for one rank."""
+    """One rank's ckrl_comm: its exchange buffer (peer-mapped into every rank) and, when
+    `unique_id` is given, an NCCL communicator for the sharded Adam step."""
 
-    def __init__(self, world: int, rank: int, unique_id: bytes):
+    def __init__(self, world: int, rank: int, unique_id: bytes | None = None):
         self.world, self.rank = world, rank
         h = C.c_void_p()
-        _lib.check(_lib.lib().ckrl_comm_create(world, rank, C.create_string_buffer(unique_id, 128),
-                                               C.byref(h)))
+        uid = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
+        _lib.check(_lib.lib().ckrl_comm_create(world, rank, uid, C.byref(h)))
         self.handle = h
 
     @staticmethod
@@ -109,13 +112,55 @@ class Comm:
         _lib.check(_lib.lib().ckrl_comm_unique_id(buf))
         return buf.raw
 
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _lib.check(_lib.lib().ckrl_comm_ipc_handle(self.handle, buf))
+        return buf.raw
+
+    def open_peers(self, handles) -> None:
+        """Maps every other rank's exchange buffer (CUDA IPC handles in rank order)."""
+        if len(handles) != self.world or any(len(h) != IPC_HANDLE_BYTES for h in handles):
+            raise ConfigError("need one IPC handle per rank")
+        raw = b"".join(handles)
+        _lib.check(_lib.lib().ckrl_comm_open_peers(self.handle, C.create_string_buffer(raw, len(raw))))
+
+    def set_peers(self, comms) -> None:
+        arr = (C.c_void_p * self.world)(*[c.handle.value for c in comms])
+        _lib.check(_lib.lib().ckrl_comm_set_peers(self.handle, arr))
+
     @classmethod
-    def from_torch(cls) -> "Comm":
+    def from_torch(cls, nccl: bool = False) -> "Comm":
+        """Collective over the default torch.distributed group: creates this rank's comm and
+        maps every rank's exchange buffer."""
         import torch.distributed as dist
         rank, world = dist.get_rank(), dist.get_world_size()
-        obj = [cls.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        return cls(world, rank, obj[0])
+        uid = None
+        if nccl:
+            obj = [cls.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        c = cls(world, rank, uid)
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, c.ipc_handle())
+            c.open_peers(handles)
+        return c
+
+    @classmethod
+    def local_group(cls, world: int, devices=None) -> list:
+        """`world` ranks driven by this one process (one per device in `devices`, or all on
+        the current device): the exchange runs through the same kernels as across processes."""
+        import torch
+        cur = torch.cuda.current_device()
+        comms = []
+        for r in range(world):
+            torch.cuda.set_device(devices[r] if devices else cur)
+            comms.append(cls(world, r))
+        for r, c in enumerate(comms):
+            torch.cuda.set_device(devices[r] if devices else cur)
+            c.set_peers(comms)
+        torch.cuda.set_device(cur)
+        return comms
 
     def close(self):
         if self.handle:
@@ -127,3 +172,6 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+IPC_HANDLE_BYTES = 64
