@@ -132,7 +132,7 @@ __device__ inline bool ex_wait(const unsigned long long* flag, unsigned long lon
 }
 // Assembly side (one thread, after the rank's record is final): bump the epoch and store the
 // record into slot [p][rank] of every rank's buffer, then release the flags.
-static __device__ __noinline__ void ex_publish_stats(const ExchangeView& x, const StatsRecord& r) {
+static __device__ __noinline__ void ex_publish_stats(ExchangeView x, StatsRecord r) {
   unsigned long long* ep = reinterpret_cast<unsigned long long*>(x.local);
   const unsigned long long e = *ep + 1;
   *ep = e;
@@ -142,7 +142,7 @@ static __device__ __noinline__ void ex_publish_stats(const ExchangeView& x, cons
 }
 // The loss's last CTA (one thread): post the rank's raw sums, wait for every rank's, and sum
 // them in rank order (identical on every rank). False on a peer timeout.
-static __device__ __noinline__ bool ex_allreduce_raw(const ExchangeView& x, unsigned long long e, double* raw) {
+static __device__ __noinline__ bool ex_allreduce_raw(ExchangeView x, unsigned long long e, double* raw) {
   for (int q = 0; q < x.world; ++q) {
     ExSlot* s = ex_slots(x.peers[q], x.world, e) + x.rank;
     for (int i = 0; i < RAW_COUNT; ++i) s->raw[i] = raw[i];

@@ -26,6 +26,9 @@ namespace ckrl {
 // of the last TMA loss launch (ckrl_debug_cta_times). Without it both read back zeros.
 __device__ uint64_t g_timeline[32];
 __device__ uint64_t g_cta_times[3][1184];
+// probe build: CTA 0's per-tile trace: [0] row phase start (stage full), [1] row phase done,
+// [2] unit phase start (buffer rows full), [3] unit phase done; local tile index < 64
+__device__ uint64_t g_tile_times[4][64];
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -245,7 +248,7 @@ __device__ LossConsts consts_from(const Moments& mom, int64_t n_adv, int64_t n_v
 // already whitened in place (ckrl_normalize_advantages) are used as they are.
 // Multi-rank (a.ex.world > 1): the records are this step's exchange slots in the rank's own
 // buffer, waited for first (every rank's assembly stored its record there over NVLink).
-__device__ __noinline__ LossConsts merge_consts(const LossArgs& a) {
+__device__ LossConsts merge_consts(const LossArgs& a) {
   int64_t n_val = 0, n_pos = 0, groups = 0, n_adv = 0;
   int status = 0, whitened = 0;
   const StatsRecord* recs = a.recs;
@@ -1016,84 +1019,6 @@ __device__ __forceinline__ void carve_buf(unsigned char* p, int cap, int scap, R
   m.need = m.act + scap;
 }
 
-// Row metadata (what the row warps read): token ids and per-slot "evaluate" flags. In the
-// fused step the assembly outputs do not exist yet, so every valid slot is evaluated
-// (counted slots are a subset); otherwise the assembled activity decides.
-// Slot-level fields are imaged for the first 32 slots of a tile (q == 0: every tile with M >= 4);
-// slots beyond are read directly at store time.
-struct RowRegs {
-  int32_t tok[4];
-  int32_t g;      // GRPO: env group id (non-PDL path)
-  double w;       // GRPO: slot weight
-  uint8_t fl;     // raw slot flags / counted / membership byte
-};
-template <int MODE, bool FUSED>
-__device__ __forceinline__ uint8_t row_need_direct(const LossArgs& a, int64_t s, bool from_flags) {
-  if (a.all_rows || MODE == MODE_STATS) return 1;
-  if (FUSED) return (a.ro.flags[s] & CKRL_FLAG_VALID) != 0;
-  if (from_flags) return 1;
-  if (MODE == MODE_PPO) return a.counted[s] != 0;
-  return (a.env_group[(int)(s / a.C) / a.Tc] >= 0) & (a.slot_member[s] != 0) & (a.slot_weight[s] != 0.0);
-}
-template <int MODE, bool FUSED>
-__device__ __forceinline__ void row_meta_load(const LossArgs& a, int64_t r0, int nrec, int lane,
-                                              RowRegs& R, bool from_flags) {
-  const int C = a.C, P = C * a.M;
-  const int rows = nrec * P, slots = nrec * C;
-  const int64_t k0 = r0 * P, s0 = r0 * C;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = lane + 32 * q;
-    if (i < rows) R.tok[q] = load_token(a.tokens, a.tok_i32, k0 + i);
-  }
-  R.fl = 1;
-  if (lane < slots && !a.all_rows && MODE != MODE_STATS) {
-    if (FUSED) {
-      R.fl = a.ro.flags[s0 + lane];
-    } else if (from_flags) {  // overlapped step: every row (the loss masks by counted), no load
-      R.fl = CKRL_FLAG_VALID;
-    } else if (MODE == MODE_PPO) {
-      R.fl = a.counted[s0 + lane];
-    } else {
-      R.g = a.env_group[(int)(s0 + lane) / C / a.Tc];
-      R.fl = a.slot_member[s0 + lane];
-      R.w = a.slot_weight[s0 + lane];
-    }
-  }
-}
-template <int MODE, bool FUSED>
-__device__ __forceinline__ void row_meta_store(const LossArgs& a, int64_t r0, int nrec, int lane,
-                                               const RowRegs& R, const MetaSmem& m, bool from_flags) {
-  const int C = a.C, P = C * a.M;
-  const int rows = nrec * P, slots = nrec * C;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = lane + 32 * q;
-    if (i < rows) m.tok[i] = R.tok[q];
-    if (i < slots) {
-      bool n = true;
-      if (q > 0) {
-        n = row_need_direct<MODE, FUSED>(a, r0 * C + i, from_flags);
-      } else if (!a.all_rows && MODE != MODE_STATS) {
-        if (FUSED || from_flags)
-          n = (R.fl & CKRL_FLAG_VALID) != 0;
-        else if (MODE == MODE_PPO)
-          n = R.fl != 0;
-        else
-          n = (R.g >= 0) & (R.fl != 0) & (R.w != 0.0);
-      }
-      m.need[i] = n ? 1 : 0;
-    }
-  }
-}
-template <int MODE, bool FUSED>
-__device__ __forceinline__ void row_meta(const LossArgs& a, int64_t r0, int nrec, int lane,
-                                         const MetaSmem& m, bool from_flags) {
-  RowRegs R;
-  row_meta_load<MODE, FUSED>(a, r0, nrec, lane, R, from_flags);
-  row_meta_store<MODE, FUSED>(a, r0, nrec, lane, R, m, from_flags);
-}
-
 // PPO tiles whose advantage, return and new-value units (value level == advantage level for
 // GAE assembly) fit one warp three times over.
 __device__ __forceinline__ bool small_units(const LossArgs& a, int nrec) {
@@ -1712,7 +1637,6 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     // ring positions and phase bits kept incrementally (no integer division per tile)
     int s = 0, b = 0;
     uint32_t sph = 0, bph = 0;
-    const float inv_m = 1.0f / (float)M;  // slot of row r: (r + 0.5) / M, exact for rows < 2^10
     // GRAD: dlogits of an earlier tile whose coefficients the unit phase left in buffer b
     auto grad_pass = [&](int64_t gtile, const RowSmem& gsm, const GradSmem& gs) {
       int64_t gr0;
@@ -1724,6 +1648,22 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         if (row < grows) grad_row<LT>(a, gsm, gs, row, gr0 * P + row, l8);
       }
     };
+    // The token ids of this lane's rows (one per pass) come straight from global memory,
+    // loaded one tile ahead into registers: their latency hides behind a whole tile, and no
+    // other warp stages row metadata (a serial load -> store chain per tile under a
+    // saturated HBM, which held the first unit phases back by microseconds).
+    int tk_next[kPasses];
+    auto load_toks = [&](int64_t tl, int* tk) {
+      if (tl >= a.n_tiles) return;
+      int64_t tr0;
+      const int trows = tile_recs(tl, tr0) * P;
+#pragma unroll
+      for (int p = 0; p < kPasses; ++p) {
+        const int row = (p * kCW + cwarp) * 4 + sub;
+        tk[p] = row < trows ? load_token(a.tokens, a.tok_i32, tr0 * P + row) : 0;
+      }
+    };
+    load_toks(blockIdx.x, tk_next);
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it,
                  s = (s + 1 == nstage) ? (sph ^= 1u, 0) : s + 1, b = (b + 1 == nbuf) ? (bph ^= 1u, 0) : b + 1) {
       RowSmem sm;
@@ -1732,11 +1672,16 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       int64_t r0;
       const int nrec = tile_recs(tile, r0);
       const int rows = nrec * P;
-      mbar_wait(&metafull_bar[b], bph);  // buffer b holds tile it's row metadata
+      int tk[kPasses];
+#pragma unroll
+      for (int p = 0; p < kPasses; ++p) tk[p] = tk_next[p];
+      load_toks(tile + gridDim.x, tk_next);
+      mbar_wait(&metafull_bar[b], bph);  // buffer b is free (its previous tile's unit phase is done)
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(11 + 3 * it);
       if (GRAD && it >= nbuf) grad_pass(tile - (int64_t)nbuf * gridDim.x, sm, grad_of(b));
       mbar_wait(&full_bar[s], sph);
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
+      CKRL_PROBE(if (blockIdx.x == 0 && cwarp == 0 && lane == 0 && it < 64) g_tile_times[0][it] = gtimer());
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
 #pragma unroll
       for (int p = 0; p < kPasses; p += RIF) {
@@ -1762,14 +1707,14 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
           for (int q = 0; q < RIF; ++q) {
             const int row = rowq[q];
             if (!live[q] || row >= rows) continue;
-            const bool need = mt.need[(int)(((float)row + 0.5f) * inv_m)] != 0;
-            if (GRAD) grad_of(b).tok[row] = mt.tok[row];
-            float xt = 0.0f;
-            if (need) {
-              const int tok = mt.tok[row];
-              xt = sizeof(LT) == 4 ? (float)reinterpret_cast<const float*>(rp[q])[tok]
-                                   : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
-            }
+            // every row is finished (the unit phase masks by counted / membership); a token
+            // id outside [0, V) of an unused row must not read outside the staged row
+            constexpr bool need = true;
+            const int tok = tk[p + q] & (V - 1);
+            if (GRAD) grad_of(b).tok[row] = tk[p + q];
+            const float xt = sizeof(LT) == 4
+                                 ? (float)reinterpret_cast<const float*>(rp[q])[tok]
+                                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
 #if CKRL_ROWFIN == 3
             // log2 s = ex + log2(mant), mant in [1, 2): the exponent exactly, the mantissa's
             // log2 by the accurate fp32 log2f (|result| < 1: abs error <= 6e-8), so no fp32
@@ -1809,6 +1754,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         mbar_arrive(&empty_bar[s]);    // stage s fully read by this warp
         mbar_arrive(&rowfull_bar[b]);  // my rows' results are in buffer b
         if (cwarp == 0 && it < 3) tl_mark(13 + 3 * it);
+        CKRL_PROBE(if (blockIdx.x == 0 && cwarp == 0 && it < 64) g_tile_times[1][it] = gtimer());
       }
     }
     if (GRAD) {  // the last nbuf tiles' gradient passes (their buffers are not reused)
@@ -1833,18 +1779,12 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     };
     RowSmem sm;
     MetaSmem mt;
-    // rows of the first nbuf tiles can start right away
-    for (int itx = m; itx < nbuf; itx += BW) {
-      const int64_t tl = blockIdx.x + (int64_t)itx * gridDim.x;
-      if (tl >= a.n_tiles) break;
-      int64_t rr0;
-      const int nr = tile_recs(tl, rr0);
-      buf_of(itx, sm, mt);
-      row_meta<MODE, FUSED>(a, rr0, nr, lane, mt, a.pdl != 0);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&metafull_bar[itx]);
-      if (lane == 0 && itx == 0) tl_mark(24);
-    }
+    // the first nbuf buffers are free: rows of the first nbuf tiles can start right away
+    if (lane == 0)
+      for (int itx = m; itx < nbuf; itx += BW) {
+        if (blockIdx.x + (int64_t)itx * gridDim.x >= a.n_tiles) break;
+        mbar_arrive(&metafull_bar[itx]);
+      }
     // Software pipeline: this warp's next tile's unit metadata and the row metadata of the
     // next user of this buffer are issued (raw, into registers) before the current unit
     // phase, so their memory latency hides behind it. PPO issues the first tile's loads as
@@ -1877,6 +1817,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       const int b = it % nbuf;
       buf_of(it, sm, mt);
       mbar_wait(&rowfull_bar[b], (it / nbuf) & 1);
+      CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && it < 64) g_tile_times[2][it] = gtimer());
       const bool probe = lane == 0 && m == 0;
       if (lane == 0 && it == m) tl_mark(20 + m);
       if (probe && it == BW) tl_mark(3);
@@ -1892,13 +1833,6 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         unit_meta_load<MODE, FUSED>(a, r0, nrec, lane, ur);
       }
       const int64_t rtile = tile + (int64_t)nbuf * gridDim.x;  // next user of buffer b
-      RowRegs rr;
-      int64_t rr0 = 0;
-      int rn = 0;
-      if (rtile < a.n_tiles) {
-        rn = tile_recs(rtile, rr0);
-        row_meta_load<MODE, FUSED>(a, rr0, rn, lane, rr, a.pdl != 0);
-      }
       if (probe && it == 0) tl_mark(2);
       if (probe && it == BW) tl_mark(29);
       if constexpr (GRAD) {
@@ -1908,14 +1842,11 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
         unit_phase_smem<MODE>(a, k, acc, sm, mt, cr0, cn, lane, outs_of(a));
       }
       __syncwarp();
+      CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && it < 64) g_tile_times[3][it] = gtimer());
       if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
       if (probe && it == BW) tl_mark(30);
-      if (rtile < a.n_tiles) {
-        row_meta_store<MODE, FUSED>(a, rr0, rn, lane, rr, mt, a.pdl != 0);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&metafull_bar[b]);
-      } else if (GRAD) {  // no next user: the arrival only releases the tile's gradient pass
-        __syncwarp();
+      if (rtile < a.n_tiles || GRAD) {  // buffer b free for its next tile (GRAD without a
+        __syncwarp();                    // next user: releases the tile's gradient pass)
         if (lane == 0) mbar_arrive(&metafull_bar[b]);
       }
     }
@@ -2143,7 +2074,9 @@ cudaError_t read_timeline(uint64_t* out, int n) {
 }
 
 cudaError_t debug_cta_times(uint64_t* out, int n) {
-  return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(uint64_t) * (n < 3 * 1184 ? n : 3 * 1184));
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_cta_times, sizeof(uint64_t) * (n < 3 * 1184 ? n : 3 * 1184));
+  if (e != cudaSuccess || n < 3 * 1184 + 4 * 64) return e;
+  return cudaMemcpyFromSymbol(out + 3 * 1184, g_tile_times, sizeof(uint64_t) * 4 * 64);
 }
 
 }  // namespace ckrl
