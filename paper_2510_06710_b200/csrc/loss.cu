@@ -28,7 +28,7 @@ __device__ uint64_t g_timeline[32];
 __device__ uint64_t g_cta_times[3][1184];
 // probe build: CTA 0's per-tile trace: [0] row phase start (stage full), [1] row phase done,
 // [2] unit phase start (buffer rows full), [3] unit phase done; local tile index < 64
-__device__ uint64_t g_tile_times[4][64];
+__device__ uint64_t g_tile_times[7][64];  // [4]: unit metadata in shared memory, [5] token pass, [6] slot pass
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -49,9 +49,6 @@ constexpr double kInvLN2 = 1.4426950408889634;
 // relative error of the fp32 log2(e) the row sums are taken with, and its reciprocal
 constexpr double kL2EDelta = (double)kL2E / 1.4426950408889634 - 1.0;
 constexpr double kInvL2EF = 1.0 / (double)kL2E;
-#ifndef CKRL_ROWFIN
-#define CKRL_ROWFIN 3  // row finish: 3 split log2 (default), 2 fp64 in the unit phase, 1 fp32, 0 MUFU approx
-#endif
 
 __device__ __forceinline__ float ex2(float y) {
   float r;
@@ -94,7 +91,6 @@ struct RowSmem {
   float* old;  // old log-prob
   double* lp;  // new log-prob (unit phase)
   float* ent;  // entropy (unit phase)
-  float* ex;   // TMA kernel, CKRL_ROWFIN 3: the exponent of the shifted sum (s = 2^ex * mant)
 };
 
 __device__ __forceinline__ float grp8_max(float v) {
@@ -292,22 +288,16 @@ struct UnitOut {
 __device__ __forceinline__ UnitOut surrogate_unit(double d, double adv, double eps) {
   double rho, kl;
   if (fabs(d) < 0.5) {
-    double p = 1.0 / 355687428096000.0;                 // 1/17!
-    p = fma(p, d, 1.0 / 20922789888000.0);              // 1/16!
-    p = fma(p, d, 1.0 / 1307674368000.0);
-    p = fma(p, d, 1.0 / 87178291200.0);
-    p = fma(p, d, 1.0 / 6227020800.0);
-    p = fma(p, d, 1.0 / 479001600.0);
-    p = fma(p, d, 1.0 / 39916800.0);
-    p = fma(p, d, 1.0 / 3628800.0);
-    p = fma(p, d, 1.0 / 362880.0);
-    p = fma(p, d, 1.0 / 40320.0);
-    p = fma(p, d, 1.0 / 5040.0);
-    p = fma(p, d, 1.0 / 720.0);
-    p = fma(p, d, 1.0 / 120.0);
-    p = fma(p, d, 1.0 / 24.0);
-    p = fma(p, d, 1.0 / 6.0);
-    p = fma(p, d, 0.5);
+    // sum_{k=0..15} d^k / (k+2)! by Estrin's scheme (dependency depth 4 instead of 16)
+    const double d2 = d * d, d4 = d2 * d2, d8 = d4 * d4;
+    const double q0 = fma(1.0 / 6.0, d, 0.5), q1 = fma(1.0 / 120.0, d, 1.0 / 24.0);
+    const double q2 = fma(1.0 / 5040.0, d, 1.0 / 720.0), q3 = fma(1.0 / 362880.0, d, 1.0 / 40320.0);
+    const double q4 = fma(1.0 / 39916800.0, d, 1.0 / 3628800.0);
+    const double q5 = fma(1.0 / 6227020800.0, d, 1.0 / 479001600.0);
+    const double q6 = fma(1.0 / 1307674368000.0, d, 1.0 / 87178291200.0);
+    const double q7 = fma(1.0 / 355687428096000.0, d, 1.0 / 20922789888000.0);
+    const double r0 = fma(q1, d2, q0), r1 = fma(q3, d2, q2), r2 = fma(q5, d2, q4), r3 = fma(q7, d2, q6);
+    const double p = fma(fma(r3, d4, r2), d8, fma(r1, d4, r0));
     kl = d * d * p;          // exp(d) - 1 - d
     rho = 1.0 + (d + kl);
   } else {
@@ -981,7 +971,6 @@ constexpr int kTileRowsMax = 128;  // rows (tokens) per tile
 // trajectory member with non-zero weight) and weight, per-unit advantage / return / new
 // value, and (GRPO) the per-record env's group data.
 struct MetaSmem {
-  int32_t* tok;
   float* old;
   double* w;
   double* adv;
@@ -990,13 +979,14 @@ struct MetaSmem {
   int32_t* esz;
   double* eadv;
   uint8_t* act;   // per slot: bit1 unit active (counted / trajectory slot with weight)
-  uint8_t* need;  // per slot: the row phase evaluates this slot's rows
 };
-// One row buffer of the TMA kernel: per-row partials + the tile's metadata. Row arrays are
+// One row buffer of the TMA kernel: per-row results + the tile's metadata. Row arrays are
 // sized by `cap` (rows per tile), slot / unit / record arrays by `scap` (slots per tile; a
 // record has C slots, a unit is a record or a slot), both multiples of 8; fp64 arrays first.
+//   per row:  lp (f64), ent, s / t2 / c (the fused seam's row statistics), old (f32)
+//   per slot: eadv, adv, ret, w (f64), nv, esz (4 B), act (1 B)
 __host__ __device__ constexpr size_t rowbuf_bytes(int cap, int scap) {
-  return (size_t)cap * (8 + 5 * 4 + 4 + 4) + (size_t)scap * (8 * 4 + 4 + 4 + 1 + 1);
+  return (size_t)cap * (8 + 5 * 4) + (size_t)scap * (4 * 8 + 4 + 4 + 1);
 }
 __device__ __forceinline__ void carve_buf(unsigned char* p, int cap, int scap, RowSmem& sm, MetaSmem& m) {
   sm.lp = reinterpret_cast<double*>(p);
@@ -1004,19 +994,16 @@ __device__ __forceinline__ void carve_buf(unsigned char* p, int cap, int scap, R
   m.adv = m.eadv + scap;
   m.ret = m.adv + scap;
   m.w = m.ret + scap;
-  sm.s = reinterpret_cast<float*>(m.w + scap);
+  sm.ent = reinterpret_cast<float*>(m.w + scap);
+  sm.s = sm.ent + cap;
   sm.t2 = sm.s + cap;
   sm.c = sm.t2 + cap;
-  sm.xt = sm.c + cap;
-  sm.ex = sm.xt + cap;
-  sm.old = nullptr;  // (direct kernel only)
-  sm.ent = nullptr;
-  m.tok = reinterpret_cast<int32_t*>(sm.ex + cap);
-  m.old = reinterpret_cast<float*>(m.tok + cap);
+  sm.xt = nullptr;  // (direct kernel only)
+  sm.old = nullptr;
+  m.old = sm.c + cap;
   m.nv = m.old + cap;
   m.esz = reinterpret_cast<int32_t*>(m.nv + scap);
   m.act = reinterpret_cast<uint8_t*>(m.esz + scap);
-  m.need = m.act + scap;
 }
 
 // PPO tiles whose advantage, return and new-value units (value level == advantage level for
@@ -1183,39 +1170,9 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   for (int row = lane; row < rows; row += 32) {
     const int64_t kk = k0 + row;
     const int sl = qdiv(row, inv_m), r = qdiv(row, inv_p);
-#if CKRL_ROWFIN == 3
-    // row warps left log2 s as exponent + log2(mantissa) and E[y] = t / s (y = x fl(log2 e) - c);
-    // finish in fp64, with the first-order correction for the fp32 log2(e) constant (the
-    // sums see x scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x])
-    const double l2s = (double)sm.ex[row] + (double)sm.s[row];
-    const double ls = l2s * kLN2;
-    const double ey = (double)sm.t2[row];
-    const double xc = (double)sm.c[row];
-    const double lp = ((double)sm.xt[row] - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
-    const double entd = ls - kLN2 * ey;  // entropy, fp64
-    if (gkent) sm.s[row] = (float)l2s;  // the fused seam's re-read takes log2 s (grad_row)
-#elif CKRL_ROWFIN == 2
-    // row warps left the raw sums s = sum 2^y, t = sum 2^y * y (y = x * fl(log2 e) - c);
-    // finish in fp64: ln s, E[y] = t / s, and the first-order correction for the fp32
-    // log2(e) constant (the sums see x scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x])
-    const double sd = (double)sm.s[row];
-    const double ls = log(sd);
-    const double ey = (double)sm.t2[row] * drecip(sd);
-    const double xc = (double)sm.c[row];
-    const double lp = ((double)sm.xt[row] - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
-    const double entd = ls - kLN2 * ey;  // entropy, fp64
-    if (gkent) {  // the fused seam's re-read needs log2 s and E[y] (grad_row)
-      sm.s[row] = (float)(ls * kInvLN2);
-      sm.t2[row] = (float)ey;
-    }
-#else
-    // row warps left log2(sum) in s and sum(e*y)/sum(e) in t2 (TMA row phase)
-    const double ls = (double)sm.s[row] * kLN2;
-    const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
-    const double entd = ls - kLN2 * (double)sm.t2[row];  // entropy finished in fp64
-#endif
-    const float ent = (float)entd;
-    sm.lp[row] = lp;
+    const double lp = sm.lp[row];  // finished by the row warps (fp64 log-prob, entropy)
+    const float ent = sm.ent[row];
+    const double entd = (double)ent;
     if (o.tok_lp) o.tok_lp[kk] = (float)lp;
     if (o.tok_ent) o.tok_ent[kk] = ent;
     const bool on = (m.act[sl] & 2) != 0;
@@ -1252,6 +1209,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   }
   __syncwarp();
 
+  CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && r0 / a.rec_per_tile / gridDim.x < 64) g_tile_times[5][r0 / a.rec_per_tile / gridDim.x] = gtimer());
   if (MODE == MODE_STATS) {
     if (a.action_lp)
       for (int sl = lane; sl < slots; sl += 32) {
@@ -1287,12 +1245,11 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
             adv = m.eadv[r];
             scale = k.inv_groups * drecip((double)m.esz[r]) * (double)m.w[sl];
           }
-          double an = 0.0, ao = 0.0;
-          for (int j = 0; j < M; ++j) {
-            an += sm.lp[sl * M + j];
-            ao += (double)m.old[sl * M + j];
-          }
-          const UnitOut su = surrogate_unit(an - ao, adv, a.clip);
+          // new - old log-ratio of the action: one sum of per-token differences (fp64;
+          // equal to sum(new) - sum(old) up to fp64 rounding)
+          double dd = 0.0;
+          for (int j = 0; j < M; ++j) dd += sm.lp[sl * M + j] - (double)m.old[sl * M + j];
+          const UnitOut su = surrogate_unit(dd, adv, a.clip);
           acc.surr += MODE == MODE_PPO ? su.value : scale * su.value;
           acc.units += 1.0;
           acc.clipped += su.clipped;
@@ -1315,26 +1272,25 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
       }
     }
 
+  CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && r0 / a.rec_per_tile / gridDim.x < 64) g_tile_times[6][r0 / a.rec_per_tile / gridDim.x] = gtimer());
   const bool chunk_lp = a.lp_level == CKRL_LEVEL_CHUNK;
   const bool chunk_val = MODE == MODE_PPO && a.val_level == CKRL_LEVEL_CHUNK;
   if (chunk_lp || chunk_val)
     for (int r = 0; r < nrec; ++r) {
       const int64_t rec = r0 + r;
-      double lpn = 0.0, lpo = 0.0, wsum = 0.0;
+      double dd = 0.0, wsum = 0.0;  // chunk log-ratio as one sum of per-token differences
       int any = 0;
       for (int t = lane; t < P; t += 32) {
         const int sl = r * C + qdiv(t, inv_m);
         if (m.act[sl] & 2) {
-          lpn += sm.lp[r * P + t];
-          lpo += (double)m.old[r * P + t];
+          dd += sm.lp[r * P + t] - (double)m.old[r * P + t];
           if (MODE == MODE_GRPO && (t % M) == 0) wsum += (double)m.w[sl];
           any = 1;
         }
       }
       any = __any_sync(0xffffffffu, any);
       if (chunk_lp) {
-        lpn = warp_sum(lpn);
-        lpo = warp_sum(lpo);
+        dd = warp_sum(dd);
         if (MODE == MODE_GRPO) wsum = warp_sum(wsum);
         float coeff = 0.0f;
         if (any) {
@@ -1347,7 +1303,7 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
             adv = m.eadv[r];
             scale = k.inv_groups * drecip((double)m.esz[r]) * wsum;
           }
-          const UnitOut su = surrogate_unit(lpn - lpo, adv, a.clip);
+          const UnitOut su = surrogate_unit(dd, adv, a.clip);
           if (lane == 0) {
             acc.units += 1.0;
             acc.clipped += su.clipped;
@@ -1709,43 +1665,32 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
             if (!live[q] || row >= rows) continue;
             // every row is finished (the unit phase masks by counted / membership); a token
             // id outside [0, V) of an unused row must not read outside the staged row
-            constexpr bool need = true;
             const int tok = tk[p + q] & (V - 1);
             if (GRAD) grad_of(b).tok[row] = tk[p + q];
             const float xt = sizeof(LT) == 4
                                  ? (float)reinterpret_cast<const float*>(rp[q])[tok]
                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
-#if CKRL_ROWFIN == 3
-            // log2 s = ex + log2(mant), mant in [1, 2): the exponent exactly, the mantissa's
-            // log2 by the accurate fp32 log2f (|result| < 1: abs error <= 6e-8), so no fp32
-            // rounding of a value up to 8 (2.4e-7) reaches the log-prob; E[y] = t / s at 2 ulp
-            // (it only feeds the entropy).
-            if (need) {
-              const int ebits = (__float_as_int(s_[q]) >> 23) - 127;  // s >= 1: normal, positive
-              const float mant = __int_as_float((__float_as_int(s_[q]) & 0x007fffff) | 0x3f800000);
-              sm.s[row] = log2f(mant);
-              sm.ex[row] = (float)ebits;
-              sm.t2[row] = __fdividef(t_[q], s_[q]);
-            } else {
-              sm.s[row] = 0.0f;
-              sm.ex[row] = 0.0f;
-              sm.t2[row] = 0.0f;
+            // The row is finished here, by the lane that holds its sums: log2 s = ex +
+            // log2(mant), mant in [1, 2) (the exponent exactly, the mantissa's log2 by the
+            // accurate fp32 log2f, |result| < 1: abs error <= 6e-8, so no fp32 rounding of a
+            // value up to 8 reaches the log-prob), E[y] = t / s at 2 ulp (entropy only), then
+            // in fp64 the first-order correction for the fp32 log2(e) constant (the sums see x
+            // scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x]). The unit phase then
+            // reads one fp64 log-prob and one entropy per row.
+            const int ebits = (__float_as_int(s_[q]) >> 23) - 127;  // s >= 1: normal, positive
+            const float mant = __int_as_float((__float_as_int(s_[q]) & 0x007fffff) | 0x3f800000);
+            const float l2m = log2f(mant);
+            const float eyf = __fdividef(t_[q], s_[q]);
+            const double l2s = (double)ebits + (double)l2m;
+            const double ls = l2s * kLN2;
+            const double ey = (double)eyf, xc = (double)c_[q];
+            sm.lp[row] = ((double)xt - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
+            sm.ent[row] = (float)(ls - kLN2 * ey);
+            if (GRAD) {  // the fused seam's re-read (grad_row): shift, log2 s, E[y]
+              sm.s[row] = (float)l2s;
+              sm.t2[row] = eyf;
+              sm.c[row] = c_[q];
             }
-#elif CKRL_ROWFIN == 2
-            // raw sums: the unit phase finishes the row in fp64 (log, reciprocal), so the
-            // row warps carry no finishing op and no fp32 rounding of log2(s) (up to 2.4e-7
-            // absolute at s ~ 2^4..2^8) reaches the log-prob
-            sm.s[row] = need ? s_[q] : 1.0f;   // sum 2^y (>= 1: the max bin contributes 2^0)
-            sm.t2[row] = need ? t_[q] : 0.0f;  // sum 2^y * y
-#elif CKRL_ROWFIN == 1
-            sm.s[row] = need ? log2f(s_[q]) : 0.0f;    // log2 of the shifted sum
-            sm.t2[row] = need ? t_[q] / s_[q] : 0.0f;  // sum e*y / sum e
-#else
-            sm.s[row] = need ? __log2f(s_[q]) : 0.0f;
-            sm.t2[row] = need ? __fdividef(t_[q], s_[q]) : 0.0f;
-#endif
-            sm.c[row] = c_[q];
-            sm.xt[row] = xt;
           }
         }
       }
@@ -1823,6 +1768,7 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       if (probe && it == BW) tl_mark(3);
       unit_meta_store<MODE>(a, r0, nrec, lane, ur, mt);
       __syncwarp();
+      CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && it < 64) g_tile_times[4][it] = gtimer());
       if (probe && it == 0) tl_mark(1);
       if (probe && it == BW) tl_mark(28);
       const int64_t cr0 = r0;
@@ -2075,8 +2021,8 @@ cudaError_t read_timeline(uint64_t* out, int n) {
 
 cudaError_t debug_cta_times(uint64_t* out, int n) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_cta_times, sizeof(uint64_t) * (n < 3 * 1184 ? n : 3 * 1184));
-  if (e != cudaSuccess || n < 3 * 1184 + 4 * 64) return e;
-  return cudaMemcpyFromSymbol(out + 3 * 1184, g_tile_times, sizeof(uint64_t) * 4 * 64);
+  if (e != cudaSuccess || n < 3 * 1184 + 7 * 64) return e;
+  return cudaMemcpyFromSymbol(out + 3 * 1184, g_tile_times, sizeof(uint64_t) * 7 * 64);
 }
 
 }  // namespace ckrl

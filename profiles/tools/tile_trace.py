@@ -27,7 +27,8 @@ spec = GranularitySpec(Level(a), Level(l), Level(v))
 if cfg.algo == "ppo":
     nv = d["new_value_scalar"] if v == 0 else d["new_value_vector"]
     pol = PolicyOutputs(lg, torch.tensor(nv, dtype=torch.float32, device="cuda"))
-    st = optim.PpoStep(ro, GaeParams(), spec, PpoParams(0.2, 0.5, 0.01, True))
+    outs = os.environ.get("TRACE_NO_OUTPUTS") != "1"  # A/B: the loss without coefficient stores
+    st = optim.PpoStep(ro, GaeParams(), spec, PpoParams(0.2, 0.5, 0.01, True), outputs=outs)
     run = lambda: st(ro, pol)  # noqa: E731
     if loss_only:
         st(ro, pol)
@@ -48,7 +49,7 @@ torch.cuda.synchronize()
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
     run()
-n = 3 * 1184 + 4 * 64
+n = 3 * 1184 + 7 * 64
 buf = (C.c_uint64 * n)()
 for rep in range(3):
     g.replay()
@@ -57,11 +58,11 @@ for rep in range(3):
     A = np.array(buf, dtype=np.int64)
     T = A[:3 * 1184].reshape(3, 1184)[:, :148]
     t0 = T[0].min()
-    tt = A[3 * 1184:].reshape(4, 64)
+    tt = A[3 * 1184:].reshape(7, 64)
     nt = int((tt[0] > 0).sum())
     print(f"{name} rep{rep}: CTA0 start {(T[0][0] - t0) / 1e3:.2f} roles done {(T[1][0] - t0) / 1e3:.2f} "
           f"exit {(T[2][0] - t0) / 1e3:.2f}; grid exit max {(T[2].max() - t0) / 1e3:.2f} us; {nt} tiles")
     for i in range(nt):
-        r0, r1, u0, u1 = ((tt[:, i] - t0) / 1e3)
-        print(f"  tile {i:2d}: rows {r0:6.2f}-{r1:6.2f} ({r1 - r0:4.2f})  unit {u0:6.2f}-{u1:6.2f} ({u1 - u0:4.2f})"
-              f"  lag {u1 - r1:5.2f}")
+        r0, r1, u0, u1, um, ut, us = ((tt[:, i] - t0) / 1e3)
+        print(f"  tile {i:2d}: rows {r0:6.2f}-{r1:6.2f} ({r1 - r0:4.2f})  unit {u0:6.2f}-{u1:6.2f} ({u1 - u0:4.2f}:"
+              f" meta {um - u0:4.2f} tok {ut - um:4.2f} slot {us - ut:4.2f} rec {u1 - us:4.2f})  lag {u1 - r1:5.2f}")
