@@ -146,7 +146,8 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "impl": "reference", "value": res["value"], "unit": "env-steps/s",
             "n_gpus": world, "steps": res["steps"], "warmup": res["warmup"],
             "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the reference's own rollout (ToyReach env, random-init policy) of the same shape",
             "config": workload(args, cfg, world),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
@@ -221,8 +222,63 @@ def cpu_reference_timing(cfg, spec, name, threads, warmup=1, steps=None, budget_
             break
     per = sum(times) / len(times)
     return {"value": env_steps(cfg) / per, "unit": "env-steps/s", "cores": threads, "kind": kind,
-            "sample": sample + f"; {len(times)} timed iterations", "steps": len(times),
+            "sample": sample + f"; {len(times)} timed iterations (rate per env-step: a per-host figure, "
+                               "unchanged by the GPU count)", "steps": len(times),
             "warmup": warmup, "ms_per_step": per * 1e3}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_variants(cfg, spec, name, budget_s=5.0):
+    """SURVEY §8(d)'s other CPU-baseline variants of the reference (oracle/_ref): as shipped
+    (single-threaded, the hot path has no threading) with the minimal trunk, and as shipped
+    with the H=32 trunk (policy MLP re-run per position inside evaluate_chunk), each on a
+    bounded env sample of the same workload (env-steps/s is per env-step, so the sample size
+    does not change the rate)."""
+    from oracle import bindings
+    if not bindings.ref_available() or cfg.algo != "ppo":
+        return []
+    out = []
+    for label, E, kw in (("1 thread, minimal trunk (hidden=1)", min(cfg.num_envs, 64), dict(hidden=1, trunk_layers=0)),
+                         ("1 thread, as shipped H=32 trunk", min(cfg.num_envs, 8), dict(hidden=32, trunk_layers=1))):
+        sc = bindings.RefScenario(num_envs=E, num_chunks=cfg.num_chunks, chunk_length=cfg.chunk_len,
+                                  vocab=cfg.vocab, tokens_per_action=cfg.tokens_per_action,
+                                  value_hidden=4, max_episode_steps=cfg.max_episode_steps, env_seed=4, **kw)
+        sc.bench_ppo(spec, 1, 1)  # warm
+        times, t0 = [], time.perf_counter()
+        while not times or time.perf_counter() - t0 < budget_s:
+            times.append(sc.bench_ppo(spec, 1, 1)[0])
+        per = sum(times) / len(times)
+        out.append({"variant": label, "value": E * cfg.num_chunks * cfg.chunk_len / per, "unit": "env-steps/s",
+                    "cores": 1, "sample": f"{E} of {cfg.num_envs} envs x {cfg.num_chunks * cfg.chunk_len} steps "
+                                          f"of {name}, {len(times)} iterations"})
+    return out
+
+
+def host_link_gbs(dev):
+    """Pinned host -> device copy bandwidth (GB/s) of this box, for the e2e PCIe share."""
+    import torch
+    h = torch.empty(1 << 28, dtype=torch.uint8).pin_memory()
+    d = torch.empty(1 << 28, dtype=torch.uint8, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(4):
+        d.copy_(h, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return 4 * h.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
 
 def workload(args, cfg, world):
@@ -243,6 +299,65 @@ def workload(args, cfg, world):
 
 
 # ----------------------------------------------------------------------------- our arm
+def _spawned(local, n, port):
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(n),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    main()
+
+
+def _pg_init(dev):
+    """Process group for bootstrap / barriers / the max-over-ranks timing: NCCL, or gloo when
+    ranks share a GPU (CKRL_BENCH_SHARE_GPU test mode: NCCL refuses duplicate devices)."""
+    import torch.distributed as dist
+    if os.environ.get("CKRL_BENCH_SHARE_GPU") == "1":
+        dist.init_process_group("gloo")
+    else:
+        _pg_init(dev)
+
+
+def _barrier(local):
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.barrier(device_ids=[local])
+    else:
+        dist.barrier()
+
+
+def _max_over_ranks(vals, dev):
+    """Element-wise max over ranks of a list of floats."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def launch():
+    """`python bench.py --gpus N` without a launcher spawns the N ranks itself (one process per
+    GPU, 127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal --gpus."""
+    args = parse()
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus and not (args.gpus == 1 and "--gpus" not in sys.argv):
+            raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        main()
+        return
+    if args.gpus <= 1:
+        main()
+        return
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    if (args.impl == "ours" and torch.cuda.device_count() < args.gpus
+            and os.environ.get("CKRL_BENCH_SHARE_GPU") != "1"):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} GPUs visible")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    mp.spawn(_spawned, args=(args.gpus, port), nprocs=args.gpus, join=True)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -264,6 +379,9 @@ def main():
     import numpy as np
     import torch
 
+    shared = os.environ.get("CKRL_BENCH_SHARE_GPU") == "1"  # test mode: all ranks on the visible GPUs
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2510_06710_b200 as ck
@@ -277,13 +395,13 @@ def main():
     if world > 1:
         import torch.distributed as dist
         from paper_2510_06710_b200 import dist as ckdist
-        dist.init_process_group("nccl", device_id=dev)
+        _pg_init(dev)
         comm = ckdist.Comm.from_torch()
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[local])
+            _barrier(local)
 
     cfg = synth.CONFIGS[args.config]
     a, l, v = synth.SPECS[args.config]
@@ -335,8 +453,6 @@ def main():
             run0(i)
             grad(i)
         launches_per_step += 1
-    if world > 1:
-        launches_per_step += 1  # finalize after the loss-scalar all-reduce
 
     stream = torch.cuda.current_stream()
     for i in range(max(3, args.warmup)):
@@ -344,9 +460,12 @@ def main():
     torch.cuda.synchronize()
     diag0 = step.diagnostics()
 
-    # --- optional CUDA graph of one step per replica (removes host launch overhead)
+    # --- CUDA graph of exactly K steps (step i on replica i mod R): no host launch overhead,
+    # and --steps is honoured as given. Multi-rank steps exchange over peer memory inside the
+    # kernels (no NCCL calls), so they capture too.
+    K = args.steps
     graph = None
-    if not args.no_graph and world == 1 and not args.profile:
+    if not args.no_graph and not args.profile:
         try:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
@@ -356,25 +475,24 @@ def main():
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
             with torch.cuda.graph(g):
-                for i in range(R):
+                for i in range(K):
                     run(i)
             graph = g
+            barrier()
+            graph.replay()  # one untimed replay: first-replay upload / cold instruction caches
+            torch.cuda.synchronize()
         except Exception as e:  # eager launches are the fallback, still the CUDA path
             print(f"# graph capture failed ({e}); timing eager launches", file=sys.stderr)
             graph = None
             torch.cuda.synchronize()
 
-    K = args.steps
-    if graph is not None:
-        K = max(R, (K // R) * R)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
         if graph is not None:
-            for _ in range(K // R):
-                graph.replay()
+            graph.replay()
         else:
             for i in range(K):
                 run(i)
@@ -383,10 +501,7 @@ def main():
     barrier()
     ms = ev0.elapsed_time(ev1) / K
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks([ms], dev)[0]
     value = world * env_steps(cfg) / (ms * 1e-3)
     diag = step.diagnostics()
 
@@ -458,6 +573,7 @@ def main():
     e2e = None
     if not args.profile:
         e2e = e2e_timing(args, cfg, reps[0], step, run, R, dev, world)
+        e2e["device_frac"] = ms / e2e["ms_per_step"]  # share of the e2e step spent in the device step
 
     if rank != 0:
         return
@@ -467,16 +583,20 @@ def main():
             cpu = cpu_reference_timing(cfg, (a, l, v), args.config, os.cpu_count() or 1,
                                        warmup=1, budget_s=args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu["cpu_model"] = cpu_model()
+            cpu["variants"] = cpu_variants(cfg, (a, l, v), args.config, budget_s=args.cpu_seconds / 2)
         except Exception as e:  # report, never hide
             cpu = {"value": None, "unit": "env-steps/s", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {e}"}
     line = {
         "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {**workload(args, cfg, world),
-                   "l2": f"inputs rotate over {R} replicas ({R * per_rep / 2**20:.0f} MiB of logits > 126 MB L2)",
-                   "cuda_graph": graph is not None},
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic slab (synth.py, fixed seeds) of the workload's shape",
+        "config": workload(args, cfg, world),
+        "timing": {"l2": f"inputs rotate over {R} replicas ({R * per_rep / 2**20:.0f} MiB of logits > 126 MB L2)",
+                   "cuda_graph": f"one graph of all {K} steps" if graph is not None else "eager launches",
+                   "untimed_replay_before_timing": graph is not None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),
@@ -488,6 +608,8 @@ def main():
         "e2e": e2e,
         "gpu_launches": K * launches_per_step,
         "clocks": clk.summary(),
+        **({"test_mode": "CKRL_BENCH_SHARE_GPU: ranks share GPUs (exercises the multi-rank path; "
+                         "not a scaling number)"} if shared else {}),
         "diagnostics": {k: diag[k] for k in ("loss", "surrogate", "value_loss", "entropy",
                                               "clip_frac", "approx_kl", "units")},
     }
@@ -587,7 +709,7 @@ def bench_pipeline(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         from paper_2510_06710_b200 import dist as ckdist
-        dist.init_process_group("nccl", device_id=dev)
+        _pg_init(dev)
         comm = ckdist.Comm.from_torch()
     E, T, Cn = CFG5["num_envs"], CFG5["num_chunks"], CFG5["chunk_len"]
     env, pol = cfg5_specs(E, seed=1000 + rank)
@@ -618,7 +740,7 @@ def bench_pipeline(args, rank, world, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
-            torch.distributed.barrier(device_ids=[local])
+            _barrier(local)
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
             e0.record(stream)
@@ -635,9 +757,7 @@ def bench_pipeline(args, rank, world, local):
         torch.cuda.synchronize()
         rms = r0.elapsed_time(r1) / K
         if world > 1:
-            t = torch.tensor([ms, rms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms, rms = (float(x) for x in t.tolist())
+            ms, rms = _max_over_ranks([ms, rms], dev)
         # e2e: parameters host->device (pinned) each epoch, loss scalars back
         hp = params.cpu().pin_memory()
         out = torch.empty(8, dtype=torch.float64).pin_memory()
@@ -754,13 +874,14 @@ def e2e_timing(args, cfg, rep, step, run, R, dev, world):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks([ms], dev)[0]
+    link = host_link_gbs(dev)
+    h2d_gbs = h2d / (ms * 1e-3) / 1e9
     return {"value": world * env_steps(cfg) / (ms * 1e-3), "unit": "env-steps/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "h2d_gbs": h2d_gbs, "host_link_gbs": link, "host_link_frac": h2d_gbs / link,
+            "device_frac": None}
 
 
 if __name__ == "__main__":
-    main()
+    launch()
