@@ -169,6 +169,10 @@ typedef struct {
   void* dlogits;         /* [E][Tc][C][M][V] optional, logits dtype: the softmax-backward seam
                             (accumulate_chunk_gradient's dlogits, policy_net.cpp:431-456) fused
                             into the loss launch (V = 256; ckrl_logits_grad otherwise) */
+  double* action_entropy; /* [E][Tc][C] entropy at action granularity: sum of the slot's token
+                             entropies (ascending j) on unit-active slots (PPO: counted; GRPO:
+                             weighted trajectory slots), 0 elsewhere */
+  double* chunk_entropy;  /* [E][Tc] sum of the record's action entropies (ascending i) */
 } ckrl_loss_outputs;
 
 /* ---- host-only helpers (no device work) ---------------------------------------------- */
@@ -295,11 +299,15 @@ int32_t ckrl_read_stats(const void* workspace, size_t workspace_bytes, int32_t n
 
 /* PolicyNet::evaluate_chunk (policy/policy_net.cpp:333-357) + aggregate_logprob
  * (core/granularity.cpp:83-113): per-token log-prob and entropy from logits rows, and the
- * action / chunk aggregates in canonical order. Any output may be NULL. */
+ * action / chunk log-prob aggregates in canonical order. Entropy at action and chunk
+ * granularity: per slot the sum of its M token entropies (ascending j), per chunk the sum of
+ * its slots' (ascending i), over the slots slot_mask ([num_chunks][chunk_len] u8, nonzero =
+ * valid action; NULL = all) selects, 0 elsewhere. Any output may be NULL. */
 int32_t ckrl_token_stats(int64_t num_chunks, int32_t chunk_len, int32_t tokens_per_action,
                          int32_t vocab, int32_t logits_dtype, const void* logits,
                          int32_t token_dtype, const void* tokens, float* token_logprob,
                          float* token_entropy, double* action_logprob, double* chunk_logprob,
+                         const uint8_t* slot_mask, double* action_entropy, double* chunk_entropy,
                          ckrl_stream_t stream);
 
 /* ---- (f1) softmax-backward seam --------------------------------------------------------- */

@@ -114,6 +114,18 @@ class Oracle:
         self.lib.orc_token_stats(C.c_int64(rows), V, _p(lg), _p(tk), _p(lp), _p(ent))
         return lp, ent
 
+    def entropy_aggregates(self, ent, chunk_len, tokens_per_action, mask=None):
+        """Per-token entropies [chunks*C*M] -> (action [chunks][C], chunk [chunks]) entropy in
+        canonical order over the `mask` [chunks][C] slots (default all)."""
+        Cn, M = chunk_len, tokens_per_action
+        e = np.ascontiguousarray(ent, dtype=np.float64).reshape(-1)
+        n = e.size // (Cn * M)
+        act, chk = np.zeros((n, Cn)), np.zeros(n)
+        mk = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        self.lib.orc_entropy_aggregates(C.c_int64(n), Cn, M, _p(e), _p(mk) if mk is not None else None,
+                                        _p(act), _p(chk))
+        return act, chk
+
     def logits_grad(self, logits, tokens, coeff_lp, coeff_ent):
         """dlogits per position (policy/policy_net.cpp:431-456); returns (status, [rows][V])."""
         lg = _c64(logits)

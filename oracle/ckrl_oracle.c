@@ -82,6 +82,28 @@ void orc_token_stats(int64_t rows, int V, const double* logits, const int32_t* t
   free(ls);
 }
 
+/* Entropy at action and chunk granularity (north star (b); the reference has only the
+ * per-token entropy, policy_net.cpp:333-357 / losses.cpp:181-190): the canonical
+ * aggregation order of core/granularity.cpp:83-113 applied to per-token entropies, over the
+ * slots `mask` ([chunks][C], nonzero = included; NULL = all) selects, 0 elsewhere:
+ *   action[s] = sum_{j ascending} H[s][j];  chunk[r] = sum_{i ascending, mask} action[r][i]. */
+void orc_entropy_aggregates(int64_t chunks, int C, int M, const double* ent, const uint8_t* mask,
+                            double* action, double* chunk) {
+  for (int64_t r = 0; r < chunks; ++r) {
+    double c = 0.0;
+    for (int i = 0; i < C; ++i) {
+      const int64_t s = r * C + i;
+      double a = 0.0;
+      if (!mask || mask[s]) {
+        for (int j = 0; j < M; ++j) a += ent[s * M + j];
+        c += a;
+      }
+      action[s] = a;
+    }
+    chunk[r] = c;
+  }
+}
+
 /* policy/policy_net.cpp:431-456 (accumulate_chunk_gradient, the per-position logits
  * gradient before outer_add / the trunk backward): positions with klp == 0 && kent == 0
  * are skipped (zero row here), non-finite coefficients throw NonFinite (:437-438). */

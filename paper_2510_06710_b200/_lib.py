@@ -77,7 +77,8 @@ class GrpoBatchC(C.Structure):
 
 class LossOutputs(C.Structure):
     _fields_ = [("coeff_logprob", vp), ("coeff_entropy", vp), ("coeff_value", vp),
-                ("token_logprob", vp), ("token_entropy", vp), ("dlogits", vp)]
+                ("token_logprob", vp), ("token_entropy", vp), ("dlogits", vp),
+                ("action_entropy", vp), ("chunk_entropy", vp)]
 
 
 class EnvConfig(C.Structure):
@@ -129,7 +130,7 @@ SIGNATURES = {
     "ckrl_assemble_grpo_batch": (C.c_int32, [P(Rollout), P(Episodes), P(Granularity),
                                              P(GrpoOptions), P(GrpoBatchC), vp, C.c_size_t, vp]),
     "ckrl_token_stats": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
-                                     C.c_int32, vp, vp, vp, vp, vp, vp]),
+                                     C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "ckrl_ppo_loss": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
                                   P(PpoParams), P(LossOutputs), vp, vp, C.c_size_t, vp]),
     "ckrl_grpo_loss": (C.c_int32, [P(Rollout), P(GrpoBatchC), P(PolicyOutputs), P(Granularity),

@@ -227,14 +227,17 @@ class LossOutputs:
     token_logprob: Optional[torch.Tensor] = None
     token_entropy: Optional[torch.Tensor] = None
     dlogits: Optional[torch.Tensor] = None  # fused softmax-backward seam, logits' shape and dtype
+    action_entropy: Optional[torch.Tensor] = None  # [E][Tc][C] f64, unit-active slots
+    chunk_entropy: Optional[torch.Tensor] = None   # [E][Tc] f64
 
     def c(self) -> _lib.LossOutputs:
         return _lib.LossOutputs(*[_ptr(t) for t in (
             self.coeff_logprob, self.coeff_entropy, self.coeff_value, self.token_logprob,
-            self.token_entropy, self.dlogits)])
+            self.token_entropy, self.dlogits, self.action_entropy, self.chunk_entropy)])
 
     @classmethod
-    def allocate(cls, rollout: RolloutBuffer, value_level: Level, tokens: bool = False):
+    def allocate(cls, rollout: RolloutBuffer, value_level: Level, tokens: bool = False,
+                 entropy: bool = False):
         E, Tc, Cn, M = rollout.shape
         dev = rollout.tokens.device
         f = dict(dtype=torch.float32, device=dev)
@@ -243,7 +246,9 @@ class LossOutputs:
                    coeff_entropy=torch.empty((E, Tc, Cn, M), **f),
                    coeff_value=torch.empty(vshape, **f),
                    token_logprob=torch.empty((E, Tc, Cn, M), **f) if tokens else None,
-                   token_entropy=torch.empty((E, Tc, Cn, M), **f) if tokens else None)
+                   token_entropy=torch.empty((E, Tc, Cn, M), **f) if tokens else None,
+                   action_entropy=torch.empty((E, Tc, Cn), dtype=torch.float64, device=dev) if entropy else None,
+                   chunk_entropy=torch.empty((E, Tc), dtype=torch.float64, device=dev) if entropy else None)
 
 
 def stream_ptr(stream: Optional[torch.cuda.Stream] = None):

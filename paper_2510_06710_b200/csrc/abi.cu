@@ -121,6 +121,8 @@ void set_outputs(LossArgs& a, const ckrl_loss_outputs* o) {
   a.tok_lp = o->token_logprob;
   a.tok_ent = o->token_entropy;
   a.dlogits = o->dlogits;
+  a.action_ent = o->action_entropy;
+  a.chunk_ent = o->chunk_entropy;
   a.all_rows = (o->token_logprob || o->token_entropy) ? 1 : 0;
 }
 
@@ -357,7 +359,8 @@ int32_t ckrl_assemble_grpo_batch(const ckrl_rollout* ro, const ckrl_episodes* ep
 int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, int32_t logits_dtype,
                          const void* logits, int32_t token_dtype, const void* tokens,
                          float* token_logprob, float* token_entropy, double* action_logprob,
-                         double* chunk_logprob, ckrl_stream_t stream) {
+                         double* chunk_logprob, const uint8_t* slot_mask, double* action_entropy,
+                         double* chunk_entropy, ckrl_stream_t stream) {
   int32_t st = check_device();
   if (st) return st;
   CKRL_REQUIRE(num_chunks >= 0 && C >= 1 && M >= 1 && V >= 1 && (int64_t)C * M <= 8192,
@@ -381,6 +384,9 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, in
   a.tok_ent = token_entropy;
   a.action_lp = action_logprob;
   a.chunk_lp = chunk_logprob;
+  a.action_ent = action_entropy;
+  a.chunk_ent = chunk_entropy;
+  a.stats_mask = slot_mask;
   a.all_rows = 1;
   a.world = 0;
   CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));

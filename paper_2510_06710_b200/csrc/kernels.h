@@ -41,6 +41,9 @@ struct LossArgs {
   float* tok_ent;
   double* action_lp;
   double* chunk_lp;
+  double* action_ent;        // [slots] canonical-order sum of the slot's token entropies (masked)
+  double* chunk_ent;         // [records] sum of the record's action entropies (masked)
+  const uint8_t* stats_mask; // MODE_STATS: per-slot valid mask for the entropy aggregates (NULL: all)
   int all_rows;  // evaluate every row (token outputs requested / MODE_STATS)
   // stats: the rank's own record (single rank), or every rank's through the exchange
   const StatsRecord* recs;

@@ -342,6 +342,37 @@ __device__ void finalize_diag(const LossArgs& a, const LossConsts& k, const doub
 // units and values. Record pass (one warp per record): chunk-level units as a warp
 // reduction over the record's tokens. fp64 throughout.
 // ---------------------------------------------------------------------------------
+// Entropy at action and chunk granularity (north star (b)): per slot the canonical-order sum
+// (ascending j) of its token entropies, per record the sum (ascending i) of its slots' sums —
+// the order aggregate_logprob uses for log-probs (core/granularity.cpp:83-113) — over the
+// slots `on(sl)` selects (counted slots for PPO, weighted trajectory slots for GRPO, the
+// caller's valid mask for token stats); other slots contribute 0. Rows' entropies are in
+// shared memory (`ent`, tile-local rows); `tid`/`nthr` stride the slots / records.
+template <class On>
+__device__ __forceinline__ void entropy_aggregates(const LossArgs& a, const float* ent, int64_t r0, int nrec,
+                                                   int tid, int nthr, On on) {
+  const int C = a.C, M = a.M;
+  if (a.action_ent)
+    for (int sl = tid; sl < nrec * C; sl += nthr) {
+      double e = 0.0;
+      if (on(sl))
+        for (int j = 0; j < M; ++j) e += (double)ent[sl * M + j];
+      a.action_ent[r0 * C + sl] = e;
+    }
+  if (a.chunk_ent)
+    for (int r = tid; r < nrec; r += nthr) {
+      double c = 0.0;
+      for (int i = 0; i < C; ++i) {
+        const int sl = r * C + i;
+        if (!on(sl)) continue;
+        double e = 0.0;
+        for (int j = 0; j < M; ++j) e += (double)ent[sl * M + j];
+        c += e;
+      }
+      a.chunk_ent[r0 + r] = c;
+    }
+}
+
 template <int MODE>
 __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& k, Acc& acc,
                                            const RowSmem& sm, int64_t r0, int nrec, int tid,
@@ -364,6 +395,7 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
     const float old = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + kk);
     sm.lp[row] = lp;
     sm.old[row] = old;
+    sm.ent[row] = ent;
     if (a.tok_lp) a.tok_lp[kk] = (float)lp;
     if (a.tok_ent) a.tok_ent[kk] = ent;
     if (MODE == MODE_PPO) {
@@ -408,6 +440,16 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
     asm volatile("bar.sync 1, %0;" ::"n"(kLossThreads));
   else if (nthr != 32)
     __syncthreads();
+
+  // ---- entropy aggregates (optional outputs) ----
+  if (a.action_ent || a.chunk_ent)
+    entropy_aggregates(a, sm.ent, r0, nrec, tid, nthr, [&](int sl) {
+      const int64_t slot = r0 * C + sl;
+      if (MODE == MODE_STATS) return !a.stats_mask || a.stats_mask[slot] != 0;
+      if (MODE == MODE_PPO) return a.counted[slot] != 0;
+      const int e = (int)((slot / C) / a.Tc);
+      return a.env_group[e] >= 0 && a.slot_member[slot] && a.slot_weight[slot] != 0.0;
+    });
 
   // ---- slot pass ----
   if (MODE == MODE_STATS) {
@@ -1210,6 +1252,11 @@ __device__ __forceinline__ void unit_phase_smem(const LossArgs& a, const LossCon
   __syncwarp();
 
   CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && r0 / a.rec_per_tile / gridDim.x < 64) g_tile_times[5][r0 / a.rec_per_tile / gridDim.x] = gtimer());
+  if (a.action_ent || a.chunk_ent)
+    entropy_aggregates(a, sm.ent, r0, nrec, lane, 32, [&](int sl) {
+      if (MODE == MODE_STATS) return !a.stats_mask || a.stats_mask[r0 * C + sl] != 0;
+      return (m.act[sl] & 2) != 0;
+    });
   if (MODE == MODE_STATS) {
     if (a.action_lp)
       for (int sl = lane; sl < slots; sl += 32) {

@@ -12,10 +12,12 @@ from . import _lib
 from .core import _ptr, stream_ptr
 
 
-def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, stream=None):
+def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, valid=None, stream=None):
     """logits [..., C, M, V] (f32/bf16), tokens [..., C, M] -> dict of token log-probs and
     entropies [..., C, M] (f32), action log-probs [..., C] and chunk log-probs [...] (f64,
-    canonical summation order)."""
+    canonical summation order), and entropy at action / chunk granularity (f64: per slot the
+    sum of its token entropies, per chunk the sum of its slots', over the `valid` [..., C]
+    slots (bool / u8; default all), 0 elsewhere)."""
     *lead, Cn, M, V = logits.shape
     n = 1
     for d in lead:
@@ -25,13 +27,17 @@ def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, stream=None):
     ent = torch.empty_like(lp)
     act = torch.empty((*lead, Cn), dtype=torch.float64, device=dev)
     chk = torch.empty(tuple(lead), dtype=torch.float64, device=dev)
+    aent = torch.empty_like(act)
+    cent = torch.empty_like(chk)
+    mask = None if valid is None else valid.to(device=dev, dtype=torch.uint8).contiguous()
     ld = _lib.DTYPE_BF16 if logits.dtype == torch.bfloat16 else _lib.DTYPE_F32
     td = _lib.DTYPE_U8 if tokens.dtype == torch.uint8 else _lib.DTYPE_I32
     tokens = tokens.contiguous() if tokens.dtype in (torch.uint8, torch.int32) else tokens.to(torch.int32).contiguous()
     _lib.check(_lib.lib().ckrl_token_stats(n, Cn, M, V, ld, _ptr(logits.contiguous()), td,
                                            _ptr(tokens), _ptr(lp), _ptr(ent), _ptr(act), _ptr(chk),
-                                           stream_ptr(stream)))
-    return {"token_logprob": lp, "token_entropy": ent, "action_logprob": act, "chunk_logprob": chk}
+                                           _ptr(mask), _ptr(aent), _ptr(cent), stream_ptr(stream)))
+    return {"token_logprob": lp, "token_entropy": ent, "action_logprob": act, "chunk_logprob": chk,
+            "action_entropy": aent, "chunk_entropy": cent}
 
 
 def logits_grad(logits: torch.Tensor, tokens: torch.Tensor, coeff_logprob: torch.Tensor,

@@ -80,3 +80,30 @@ def test_degenerate_fixture_covers_error_paths():
     statuses = {int(d[k]) for k in d if k.endswith("/status")}
     assert 8 in statuses  # SkipUpdate: every group filtered
     assert 7 in statuses  # DegenerateGroup: unfiltered, eps_std == 0
+
+
+@pytest.mark.parametrize("name", golden_files("ppo_"))
+def test_entropy_aggregates_of_reference_entropies(oracle, name):
+    """Entropy at action / chunk granularity (north star (b)): the reference computes only the
+    per-token entropy (policy_net.cpp:333-357, fixture `ent_cur`); the aggregates are its
+    canonical-order sums (core/granularity.cpp:83-113) — pinned here as sequential sums of
+    the reference's own per-token values, with and without a slot mask."""
+    d = load_golden(name)
+    E, Tc, Cn, M = d["ent_cur"].shape
+    ent = d["ent_cur"].reshape(E * Tc, Cn, M)
+    act, chk = oracle.entropy_aggregates(ent, Cn, M)
+    want_a = np.zeros((E * Tc, Cn))
+    for j in range(M):
+        want_a = want_a + ent[:, :, j]
+    want_c = np.zeros(E * Tc)
+    for i in range(Cn):
+        want_c = want_c + want_a[:, i]
+    np.testing.assert_array_equal(act, want_a)
+    np.testing.assert_array_equal(chk, want_c)
+    mask = (d["flags"].reshape(E * Tc, Cn) & 4) != 0  # valid-action mask (StepRecord::valid)
+    act_m, chk_m = oracle.entropy_aggregates(ent, Cn, M, mask)
+    np.testing.assert_array_equal(act_m, np.where(mask, want_a, 0.0))
+    want_cm = np.zeros(E * Tc)
+    for i in range(Cn):
+        want_cm = want_cm + np.where(mask[:, i], want_a[:, i], 0.0)
+    np.testing.assert_array_equal(chk_m, want_cm)
