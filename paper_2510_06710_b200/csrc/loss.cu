@@ -1590,11 +1590,11 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     CKRL_PROBE(if (blockIdx.x < 1184) g_cta_times[0][blockIdx.x] = gtimer());
     for (int s = 0; s < nstage; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kCW);
+      mbar_init(&empty_bar[s], kCW * 32);
     }
     for (int b = 0; b < a.nbuf; ++b) {
-      mbar_init(&metafull_bar[b], 1);
-      mbar_init(&rowfull_bar[b], kCW);
+      mbar_init(&metafull_bar[b], 32);
+      mbar_init(&rowfull_bar[b], kCW * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1741,10 +1741,12 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
           }
         }
       }
-      __syncwarp();
+      // Every lane arrives (barrier counts are per thread): each lane's own shared-memory
+      // writes are ordered before its arrival (release, CTA scope), which the consumers'
+      // try_wait acquires — a per-thread happens-before that racecheck can also see.
+      mbar_arrive(&empty_bar[s]);    // stage s fully read by this lane
+      mbar_arrive(&rowfull_bar[b]);  // this lane's rows' results are in buffer b
       if (lane == 0) {
-        mbar_arrive(&empty_bar[s]);    // stage s fully read by this warp
-        mbar_arrive(&rowfull_bar[b]);  // my rows' results are in buffer b
         if (cwarp == 0 && it < 3) tl_mark(13 + 3 * it);
         CKRL_PROBE(if (blockIdx.x == 0 && cwarp == 0 && it < 64) g_tile_times[1][it] = gtimer());
       }
@@ -1772,11 +1774,10 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
     RowSmem sm;
     MetaSmem mt;
     // the first nbuf buffers are free: rows of the first nbuf tiles can start right away
-    if (lane == 0)
-      for (int itx = m; itx < nbuf; itx += BW) {
-        if (blockIdx.x + (int64_t)itx * gridDim.x >= a.n_tiles) break;
-        mbar_arrive(&metafull_bar[itx]);
-      }
+    for (int itx = m; itx < nbuf; itx += BW) {
+      if (blockIdx.x + (int64_t)itx * gridDim.x >= a.n_tiles) break;
+      mbar_arrive(&metafull_bar[itx]);  // every lane (count 32)
+    }
     // Software pipeline: this warp's next tile's unit metadata and the row metadata of the
     // next user of this buffer are issued (raw, into registers) before the current unit
     // phase, so their memory latency hides behind it. PPO issues the first tile's loads as
@@ -1838,10 +1839,8 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(Lo
       CKRL_PROBE(if (blockIdx.x == 0 && lane == 0 && it < 64) g_tile_times[3][it] = gtimer());
       if (lane == 0 && it == m) tl_mark(4 + m);  // first unit phase of each buffer warp
       if (probe && it == BW) tl_mark(30);
-      if (rtile < a.n_tiles || GRAD) {  // buffer b free for its next tile (GRAD without a
-        __syncwarp();                    // next user: releases the tile's gradient pass)
-        if (lane == 0) mbar_arrive(&metafull_bar[b]);
-      }
+      if (rtile < a.n_tiles || GRAD)  // buffer b free for its next tile (GRAD without a next
+        mbar_arrive(&metafull_bar[b]);  // user: releases the tile's gradient pass); every lane
     }
 
   }
