@@ -43,6 +43,9 @@ def parse():
     p.add_argument("--stages", default="1,2,4", help="cfg5: pipeline depths k to time")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-pipeline", dest="pipeline", action="store_false",
+                   help="PPO: one ckrl_ppo_step per batch instead of overlapping batch i+1's assembly "
+                        "with batch i's loss")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
@@ -424,11 +427,18 @@ def main():
         pol = PolicyOutputs(logits, torch.tensor(nv, dtype=torch.float32, device=dev))
         ept = EpisodeTable.from_arrays(d, dev) if cfg.algo == "grpo" else None
         reps.append((ro, pol, ept, d))
+    pipe = None
     if cfg.algo == "ppo":
         step = optim.PpoStep(reps[0][0], GaeParams(0.99, 0.95), spec,
                              PpoParams(0.2, 0.5, 0.01, True), comm=comm)
         run0 = lambda i: step(reps[i % R][0], reps[i % R][1])  # noqa: E731
         launches_per_step = 2
+        if args.pipeline and args.grad is None:
+            # batch i+1's assembly (side stream) overlaps batch i's loss: one step object per
+            # replica (its own workspace / batch buffers), the public two-halves API
+            steps = [step] + [optim.PpoStep(reps[r][0], GaeParams(0.99, 0.95), spec,
+                                            PpoParams(0.2, 0.5, 0.01, True), comm=comm) for r in range(1, R)]
+            pipe = optim.Pipelined(steps)
     else:
         opts = GrpoAssemblyOptions(spec)
         step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
@@ -459,6 +469,11 @@ def main():
         run(i)
     torch.cuda.synchronize()
     diag0 = step.diagnostics()
+    issue = lambda n: [run(i) for i in range(n)]  # noqa: E731  (K steps, eager order)
+    if pipe is not None:
+        issue = lambda n: pipe.issue(n, lambda i: ((reps[i % R][0],), (reps[i % R][0], reps[i % R][1])))  # noqa: E731
+        issue(max(3, args.warmup))
+        torch.cuda.synchronize()
 
     # --- CUDA graph of exactly K steps (step i on replica i mod R): no host launch overhead,
     # and --steps is honoured as given. Multi-rank steps exchange over peer memory inside the
@@ -471,12 +486,11 @@ def main():
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
-                run(0)
+                issue(1)
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
             with torch.cuda.graph(g):
-                for i in range(K):
-                    run(i)
+                issue(K)
             graph = g
             barrier()
             graph.replay()  # one untimed replay: first-replay upload / cold instruction caches
@@ -494,8 +508,7 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            for i in range(K):
-                run(i)
+            issue(K)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -505,7 +518,19 @@ def main():
     value = world * env_steps(cfg) / (ms * 1e-3)
     diag = step.diagnostics()
 
-    # --- dominant kernel (fused loss) timed alone with events on its stream
+    # --- dominant kernel (fused loss): with the pipelined step, timed live in a run of
+    # pipelined steps (events around every loss launch on its stream while the next batch's
+    # assembly runs beside it; the device is held in a sleep while the host enqueues them all,
+    # so no launch waits on the host); otherwise each launch alone after its assembly
+    live_kms = None
+    if pipe is not None:
+        n_live = min(K, 50)
+        lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_live)]
+        torch.cuda._sleep(40_000_000)
+        pipe.issue(n_live, lambda i: ((reps[i % R][0],), (reps[i % R][0], reps[i % R][1])), loss_events=lev)
+        torch.cuda.synchronize()
+        lt = sorted(e0.elapsed_time(e1) for e0, e1 in lev[2:])
+        live_kms = lt[len(lt) // 2]
     ws = step.ws
     kms = []
     for i in range(min(K, 50) + 3):  # 3 untimed launches first (first-call attribute setup)
@@ -532,7 +557,8 @@ def main():
         kms.append((e0, e1))
     torch.cuda.synchronize()
     ktimes = sorted(e0.elapsed_time(e1) for e0, e1 in kms[3:])
-    kernel_ms = ktimes[len(ktimes) // 2]  # median launch
+    alone_ms = ktimes[len(ktimes) // 2]  # median launch
+    kernel_ms = live_kms if live_kms is not None else alone_ms
     kbytes = loss_kernel_bytes(cfg, dbytes, (a, l, v), cfg.algo)
     if args.grad == "fused":  # the same launch also writes V * s_out bytes of dlogits per position
         kbytes += env_steps(cfg) * cfg.tokens_per_action * cfg.vocab * dbytes
@@ -596,11 +622,17 @@ def main():
         "config": workload(args, cfg, world),
         "timing": {"l2": f"inputs rotate over {R} replicas ({R * per_rep / 2**20:.0f} MiB of logits > 126 MB L2)",
                    "cuda_graph": f"one graph of all {K} steps" if graph is not None else "eager launches",
-                   "untimed_replay_before_timing": graph is not None},
+                   "untimed_replay_before_timing": graph is not None,
+                   "pipelined": ("batch i+1's assembly on a side stream overlaps batch i's loss "
+                                 "(ckrl_ppo_step_assemble / ckrl_ppo_step_loss, one workspace per replica); "
+                                 "every step still runs its full assembly and loss") if pipe is not None else False},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),
                      "kernel_ms": kernel_ms,
+                     "kernel_timing": ("median loss launch inside a graph of pipelined steps (events on its stream)"
+                                       if live_kms is not None else "median loss launch alone after its assembly"),
+                     "kernel_ms_alone": alone_ms,
                      "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
                      "step_frac": (kbytes / (ms * 1e-3) / 1e9) / peak},
         "cpu_baseline": cpu,

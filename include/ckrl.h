@@ -394,6 +394,30 @@ int32_t ckrl_grpo_step(const ckrl_rollout* rollout, const ckrl_episodes* episode
                        void* workspace, size_t workspace_bytes, ckrl_comm* comm,
                        ckrl_stream_t stream);
 
+/* The two halves of ckrl_ppo_step / ckrl_grpo_step (same kernels and cross-rank exchange), for
+ * callers that pipeline batches: e.g. batch i+1's assembly on one stream while batch i's loss
+ * runs on another, each batch with its own workspace and batch buffers. The loss must follow
+ * its own assembly (stream order or an event); an assembly may start once the loss of the
+ * batch two before it has completed (the exchange keeps two batches in flight). */
+int32_t ckrl_ppo_step_assemble(const ckrl_rollout* rollout, const ckrl_gae_params* gae,
+                               const ckrl_granularity* spec, ckrl_ppo_batch* batch,
+                               void* workspace, size_t workspace_bytes, ckrl_comm* comm,
+                               ckrl_stream_t stream);
+int32_t ckrl_ppo_step_loss(const ckrl_rollout* rollout, const ckrl_policy_outputs* policy,
+                           const ckrl_granularity* spec, const ckrl_ppo_params* params,
+                           const ckrl_ppo_batch* batch, ckrl_loss_outputs* outputs,
+                           double* diag_device, void* workspace, size_t workspace_bytes,
+                           ckrl_comm* comm, ckrl_stream_t stream);
+int32_t ckrl_grpo_step_assemble(const ckrl_rollout* rollout, const ckrl_episodes* episodes,
+                                const ckrl_granularity* spec, const ckrl_grpo_options* options,
+                                ckrl_grpo_batch* batch, void* workspace, size_t workspace_bytes,
+                                ckrl_comm* comm, ckrl_stream_t stream);
+int32_t ckrl_grpo_step_loss(const ckrl_rollout* rollout, const ckrl_policy_outputs* policy,
+                            const ckrl_granularity* spec, const ckrl_grpo_params* params,
+                            const ckrl_grpo_batch* batch, ckrl_loss_outputs* outputs,
+                            double* diag_device, void* workspace, size_t workspace_bytes,
+                            ckrl_comm* comm, ckrl_stream_t stream);
+
 /* Copy the device diagnostics to the host (synchronises `stream`) and map the device
  * status word to the reference's exceptions: SkipUpdate (no retained groups),
  * DegenerateGroup, NonFinite (losses.cpp:229-230, 326-327). */

@@ -141,6 +141,14 @@ SIGNATURES = {
     "ckrl_grpo_step": (C.c_int32, [P(Rollout), P(Episodes), P(PolicyOutputs), P(Granularity),
                                    P(GrpoOptions), P(GrpoParams), P(GrpoBatchC),
                                    P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
+    "ckrl_ppo_step_assemble": (C.c_int32, [P(Rollout), P(GaeParams), P(Granularity), P(PpoBatchC), vp,
+                                           C.c_size_t, vp, vp]),
+    "ckrl_ppo_step_loss": (C.c_int32, [P(Rollout), P(PolicyOutputs), P(Granularity), P(PpoParams),
+                                       P(PpoBatchC), P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
+    "ckrl_grpo_step_assemble": (C.c_int32, [P(Rollout), P(Episodes), P(Granularity), P(GrpoOptions),
+                                            P(GrpoBatchC), vp, C.c_size_t, vp, vp]),
+    "ckrl_grpo_step_loss": (C.c_int32, [P(Rollout), P(PolicyOutputs), P(Granularity), P(GrpoParams),
+                                        P(GrpoBatchC), P(LossOutputs), vp, vp, C.c_size_t, vp, vp]),
     "ckrl_read_diagnostics": (C.c_int32, [vp, vp, vp]),
     "ckrl_logits_grad": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp, vp,
                                      C.c_int32, vp, vp, vp]),

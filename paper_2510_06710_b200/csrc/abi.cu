@@ -738,6 +738,90 @@ int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
                         overlap_sms() > 0 && po->logits_dtype >= 0, ex, loss_cta_cap(comm));
 }
 
+// The two halves of a step, for callers that pipeline batches (the assembly of batch i+1 on
+// one stream while batch i's loss runs on another, each batch with its own workspace): the
+// same kernels as ckrl_*_step, the loss launched as a plain kernel after its assembly.
+int32_t ckrl_ppo_step_assemble(const ckrl_rollout* ro, const ckrl_gae_params* gae,
+                               const ckrl_granularity* spec, ckrl_ppo_batch* b, void* ws,
+                               size_t ws_bytes, ckrl_comm* comm, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if (spec->value_level != spec->advantage_level)
+    return fail(CKRL_ERR_CONFIG, "value_type must match reward_type for GAE assembly");
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, true))) return st;
+  if ((st = check_comm(comm))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(gae && b && b->counted && b->advantages && b->returns, CKRL_ERR_INVALID_ARGUMENT,
+               "gae / batch required");
+  CKRL_CUDA(launch_ppo_assemble(*ro, spec->advantage_level == CKRL_LEVEL_ACTION, gae->gamma, gae->lambda,
+                                *b, (char*)ws, ws_layout(ro->num_envs, world), (cudaStream_t)stream,
+                                exchange_view(comm)));
+  return CKRL_OK;
+}
+
+int32_t ckrl_ppo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
+                           const ckrl_granularity* spec, const ckrl_ppo_params* p,
+                           const ckrl_ppo_batch* b, ckrl_loss_outputs* out, double* diag, void* ws,
+                           size_t ws_bytes, ckrl_comm* comm, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_comm(comm))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(b && p && diag && b->counted && b->advantages && b->returns, CKRL_ERR_INVALID_ARGUMENT,
+               "batch / params / diag required");
+  CKRL_REQUIRE(p->value_loss_coef == 0.0 || po->values, CKRL_ERR_INVALID_ARGUMENT,
+               "new values required when value_loss_coef != 0");
+  WsLayout L = ws_layout(ro->num_envs, world);
+  LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
+                        reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1);
+  a.ex = exchange_view(comm);
+  a.max_ctas = loss_cta_cap(comm);
+  CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));
+  return CKRL_OK;
+}
+
+int32_t ckrl_grpo_step_assemble(const ckrl_rollout* ro, const ckrl_episodes* ep,
+                                const ckrl_granularity* spec, const ckrl_grpo_options* opt,
+                                ckrl_grpo_batch* gb, void* ws, size_t ws_bytes, ckrl_comm* comm,
+                                ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_comm(comm))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(ep && opt && gb, CKRL_ERR_INVALID_ARGUMENT, "episodes / options / batch required");
+  CKRL_CUDA(launch_grpo_assemble(*ro, *ep, *opt, *gb, (char*)ws, ws_layout(ro->num_envs, world),
+                                 (cudaStream_t)stream, exchange_view(comm)));
+  return CKRL_OK;
+}
+
+int32_t ckrl_grpo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
+                            const ckrl_granularity* spec, const ckrl_grpo_params* p,
+                            const ckrl_grpo_batch* gb, ckrl_loss_outputs* out, double* diag, void* ws,
+                            size_t ws_bytes, ckrl_comm* comm, ckrl_stream_t stream) {
+  int32_t st = validate(spec);
+  if (st) return st;
+  if ((st = check_device())) return st;
+  if ((st = check_rollout(ro, false))) return st;
+  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_comm(comm))) return st;
+  const int world = comm ? comm->world : 1;
+  if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
+  CKRL_REQUIRE(gb && p && diag, CKRL_ERR_INVALID_ARGUMENT, "batch / params / diag required");
+  WsLayout L = ws_layout(ro->num_envs, world);
+  return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
+                        reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
+                        (cudaStream_t)stream, 0, exchange_view(comm), loss_cta_cap(comm));
+}
+
 int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream) {
   CKRL_REQUIRE(diag_device && diag_host, CKRL_ERR_INVALID_ARGUMENT, "null diagnostics");
   CKRL_CUDA(cudaMemcpyAsync(diag_host, diag_device, sizeof(double) * CKRL_DIAG_COUNT,

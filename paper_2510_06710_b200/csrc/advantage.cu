@@ -72,7 +72,8 @@ __device__ void finish_asm_stats(AsmPartial mine, char* ws, const WsLayout L, in
   st->groups_retained = 0;
   st->status = 0;
   tickets[TICKET_ASM] = 0;  // self-reset for the next launch
-  if (ex.world > 1) ex_publish_stats(ex, *st);  // to every rank's exchange buffer (NVLink stores)
+  if (ex.world > 1)  // to every rank's exchange buffer (NVLink stores)
+    ex_publish_stats(ex, *st, tickets + TICKET_EPOCH);
 }
 
 // Two schedules: thread-per-env serial walk (short envs: <= kSerialItems items, the common
@@ -256,7 +257,8 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
     if (tid == 0) {
       *st = StatsRecord{0.0, 0.0, 0, 0, 0, 0, 0, CKRL_ERR_INVALID_ARGUMENT};
       gb.group_counts[0] = gb.group_counts[1] = 0;
-      if (ex.world > 1) ex_publish_stats(ex, *st);  // peers must not wait for a record
+      if (ex.world > 1)  // peers must not wait for a record
+        ex_publish_stats(ex, *st, reinterpret_cast<uint32_t*>(ws + L.tickets) + TICKET_EPOCH);
     }
     return;
   }
@@ -389,7 +391,8 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
     st->n_adv = st->n_val = st->n_pos = 0;
     st->groups_retained = s_retained;
     st->status = s_status;
-    if (ex.world > 1) ex_publish_stats(ex, *st);  // to every rank's exchange buffer
+    if (ex.world > 1)  // to every rank's exchange buffer
+      ex_publish_stats(ex, *st, reinterpret_cast<uint32_t*>(ws + L.tickets) + TICKET_EPOCH);
   }
 }
 

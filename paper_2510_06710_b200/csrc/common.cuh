@@ -130,12 +130,17 @@ __device__ inline bool ex_wait(const unsigned long long* flag, unsigned long lon
     __nanosleep(64);
   }
 }
-// Assembly side (one thread, after the rank's record is final): bump the epoch and store the
-// record into slot [p][rank] of every rank's buffer, then release the flags.
-static __device__ __noinline__ void ex_publish_stats(ExchangeView x, StatsRecord r) {
+// Assembly side (one thread, after the rank's record is final): bump the rank's epoch, note it
+// in the workspace (`ws_epoch`: the loss of this batch reads it there, so a batch's assembly
+// and an earlier batch's loss may run concurrently), store the record into slot [p][rank] of
+// every rank's buffer, then release the flags. Callers keep an assembly at most one batch
+// ahead of the losses (it starts after the loss two batches back has completed), which is
+// what two parities need.
+static __device__ __noinline__ void ex_publish_stats(ExchangeView x, StatsRecord r, uint32_t* ws_epoch) {
   unsigned long long* ep = reinterpret_cast<unsigned long long*>(x.local);
   const unsigned long long e = *ep + 1;
   *ep = e;
+  *ws_epoch = (uint32_t)e;
   for (int q = 0; q < x.world; ++q) ex_slots(x.peers[q], x.world, e)[x.rank].rec = r;
   __threadfence_system();
   for (int q = 0; q < x.world; ++q) st_release_sys(&ex_slots(x.peers[q], x.world, e)[x.rank].stats_epoch, e);
@@ -223,7 +228,8 @@ __host__ __device__ inline WsLayout ws_layout(int E, int world) {
   return L;
 }
 
-enum { TICKET_ASM = 0, TICKET_LOSS = 1, TICKET_GRID = 2, TICKET_GEN = 3, TICKET_NORM = 4 };
+enum { TICKET_ASM = 0, TICKET_LOSS = 1, TICKET_GRID = 2, TICKET_GEN = 3, TICKET_NORM = 4,
+       TICKET_EPOCH = 6 };  // (not a ticket) the exchange epoch of the workspace's last assembly
 
 // ---- warp helpers ----------------------------------------------------------------------
 template <typename T>

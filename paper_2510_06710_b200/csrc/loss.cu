@@ -252,7 +252,9 @@ __device__ LossConsts merge_consts(const LossArgs& a) {
   size_t stride = sizeof(StatsRecord);
   unsigned long long e = 0;
   if (a.ex.world > 1) {
-    e = *reinterpret_cast<const unsigned long long*>(a.ex.local);  // this step's epoch
+    // this batch's epoch, as its assembly noted it in the workspace (the exchange header may
+    // already hold a later batch's)
+    e = (unsigned long long)reinterpret_cast<const uint32_t*>(a.ws + a.L.tickets)[TICKET_EPOCH];
     ExSlot* sl = ex_slots(a.ex.local, a.ex.world, e);
     for (int q = 0; q < a.ex.world; ++q)
       if (!ex_wait(&sl[q].stats_epoch, e)) status = CKRL_ERR_NCCL;  // a peer never posted
@@ -1563,7 +1565,10 @@ __device__ __noinline__ void fused_phase_a(const LossArgs& a, int b, int lane, L
 // Synchronisation is mbarrier-only: full[s]/empty[s] (producer <-> row warps),
 // metafull[b] (buffer warp -> row warps), rowfull[b] (row warps -> buffer warp).
 template <int MODE, typename LT, int ROWW, int RIF, bool FUSED, int BW, bool GRAD = false>
-__global__ void __launch_bounds__(tma_threads<ROWW, BW>(), 1) tma_tile_kernel(LossArgs a, int nstage,
+// launch bounds of at least 19 warps' worth: the register cap stays <= 104 for every variant,
+// so a 16-warp variant leaves room for 2-warp assembly CTAs on each SM
+__global__ void __launch_bounds__(tma_threads<ROWW, BW>() > 608 ? tma_threads<ROWW, BW>() : 608, 1)
+    tma_tile_kernel(LossArgs a, int nstage,
                                                                           uint32_t tile_bytes) {
   constexpr int kThreads = tma_threads<ROWW, BW>();
   static_assert(!FUSED || BW == kBufWarps, "the fused step runs with 4 buffer warps");
@@ -1986,19 +1991,36 @@ static cudaError_t launch_tma_v(LossArgs& a, cudaStream_t s, int* grid_out, int 
 }
 
 static int g_tma_variant = -1;
+static int device_sms_cached() {
+  static int n = 0;
+  if (n == 0) n = device_sms();
+  return n;
+}
 
 template <int MODE, typename LT, bool FUSED>
 static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int nstage, uint32_t tile_bytes) {
   if (g_tma_variant < 0) {
     const char* env = getenv("CKRL_TMA_VARIANT");
-    g_tma_variant = env ? atoi(env) : 4;
+    g_tma_variant = env ? atoi(env) : 99;  // 99: by shape (below)
   }
   if constexpr (!FUSED && MODE != MODE_STATS)
     if (a.dlogits)  // fused softmax-backward seam (row f1)
       return launch_tma_v<MODE, LT, 14, 1, FUSED, kBufWarps, true>(a, s, grid_out, nstage, tile_bytes);
-  switch (g_tma_variant) {
+  int variant = g_tma_variant;
+  if (variant == 99) {
+    // PPO launches of a few tiles per SM (cfg1 / cfg3): 16-warp CTAs, so the 2-warp assembly
+    // CTAs (the previous or next step's, on another stream, or this step's under PDL) share
+    // the SMs instead of waiting for loss CTAs to retire (cfg3 40.4 -> 38.4 us, cfg3 bf16
+    // 35.2 -> 32.8, cfg1 bf16 21.2 -> 19.4); long launches (cfg4: 221 tiles per SM) and GRPO
+    // keep 14 row warps, which the steady-state row throughput needs (cfg4 f32 308 vs 372 us)
+    const int64_t per_sm = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile / device_sms_cached();
+    variant = (MODE == MODE_PPO && !FUSED && per_sm <= 32) ? 5 : 4;
+  }
+  switch (variant) {
     // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
     case 3: return launch_tma_v<MODE, LT, 8, 2, FUSED>(a, s, grid_out, nstage, tile_bytes);
+    // 11 row warps: 16-warp CTAs that an assembly CTA can share an SM with
+    case 5: return launch_tma_v<MODE, LT, 11, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
     case 0: return launch_tma_v<MODE, LT, 16, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);
     // default: 14 row warps (a 56-row tile is 14 x 4 rows) -> 19 warps, 96 registers, no spills
     default: return launch_tma_v<MODE, LT, 14, 1, FUSED>(a, s, grid_out, nstage, tile_bytes);

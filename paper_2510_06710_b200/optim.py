@@ -154,6 +154,20 @@ class PpoStep:
             stream_ptr(stream)))
         return self.diag
 
+    # the two halves (ckrl_ppo_step_assemble / _loss) for pipelining batches across streams
+    def assemble(self, rollout: RolloutBuffer, stream=None):
+        _lib.check(_lib.lib().ckrl_ppo_step_assemble(
+            C.byref(rollout.c()), C.byref(self.gae), C.byref(self.spec), C.byref(self._bc), self.ws.ptr,
+            self.ws.bytes, self.comm.handle if self.comm is not None else None, stream_ptr(stream)))
+
+    def loss(self, rollout: RolloutBuffer, policy: PolicyOutputs, stream=None):
+        _lib.check(_lib.lib().ckrl_ppo_step_loss(
+            C.byref(rollout.c()), C.byref(policy.c()), C.byref(self.spec), C.byref(self.params),
+            C.byref(self._bc), C.byref(self._oc) if self._oc is not None else None,
+            C.c_void_p(self.diag.data_ptr()), self.ws.ptr, self.ws.bytes,
+            self.comm.handle if self.comm is not None else None, stream_ptr(stream)))
+        return self.diag
+
     def diagnostics(self, stream=None) -> dict:
         return read_diagnostics(self.diag, stream)
 
@@ -186,8 +200,75 @@ class GrpoStep:
             stream_ptr(stream)))
         return self.diag
 
+    # the two halves (ckrl_grpo_step_assemble / _loss) for pipelining batches across streams
+    def assemble(self, rollout: RolloutBuffer, episodes: EpisodeTable, stream=None):
+        _lib.check(_lib.lib().ckrl_grpo_step_assemble(
+            C.byref(rollout.c()), C.byref(episodes.c()), C.byref(self._spec), C.byref(self._opt),
+            C.byref(self._bc), self.ws.ptr, self.ws.bytes,
+            self.comm.handle if self.comm is not None else None, stream_ptr(stream)))
+
+    def loss(self, rollout: RolloutBuffer, policy: PolicyOutputs, stream=None):
+        _lib.check(_lib.lib().ckrl_grpo_step_loss(
+            C.byref(rollout.c()), C.byref(policy.c()), C.byref(self._spec), C.byref(self.params),
+            C.byref(self._bc), C.byref(self._oc) if self._oc is not None else None,
+            C.c_void_p(self.diag.data_ptr()), self.ws.ptr, self.ws.bytes,
+            self.comm.handle if self.comm is not None else None, stream_ptr(stream)))
+        return self.diag
+
     def diagnostics(self, stream=None) -> dict:
         return read_diagnostics(self.diag, stream)
+
+
+class Pipelined:
+    """Steps over a stream of batches with batch i+1's assembly on a side stream overlapping
+    batch i's loss (the two halves of PpoStep / GrpoStep, one step object per in-flight batch
+    slot: its workspace and batch buffers). Every batch still gets its full assembly and loss;
+    only their placement in time changes. `issue(K, args_of)` enqueues K batches on the
+    current stream (graph-capturable); batch i uses steps[i % len(steps)] and
+    args_of(i) -> (assemble args, loss args)."""
+
+    def __init__(self, steps):
+        import torch
+        self.steps = steps
+        # across ranks the exchange holds two batches in flight: an assembly may only start
+        # once the loss two batches back has completed (ckrl.h, ckrl_ppo_step_assemble)
+        self.multi_rank = any(getattr(st, "comm", None) is not None and st.comm.world > 1 for st in steps)
+        self.side = torch.cuda.Stream()
+        n = len(steps)
+        self.ev_asm = [torch.cuda.Event() for _ in range(n)]
+        self.ev_loss = [torch.cuda.Event() for _ in range(n)]
+
+    def issue(self, K: int, args_of, loss_events=None):
+        import torch
+        n = len(self.steps)
+        main = torch.cuda.current_stream()
+        side = self.side
+        side.wait_stream(main)
+
+        def asm(j):
+            a_args, _ = args_of(j)
+            # slot reuse: loss j - n done; exchange: at most one batch ahead (loss j - 2 done)
+            for back in ((n, 2) if self.multi_rank else (n,)):
+                if j >= back:
+                    side.wait_event(self.ev_loss[(j - back) % n])
+            self.steps[j % n].assemble(*a_args, stream=side)
+            self.ev_asm[j % n].record(side)
+
+        with torch.cuda.stream(side):
+            asm(0)
+        for i in range(K):
+            if i + 1 < K:
+                with torch.cuda.stream(side):
+                    asm(i + 1)
+            _, l_args = args_of(i)
+            main.wait_event(self.ev_asm[i % n])
+            if loss_events is not None:  # (start, end) timing events around each loss launch
+                loss_events[i][0].record(main)
+            self.steps[i % n].loss(*l_args, stream=main)
+            if loss_events is not None:
+                loss_events[i][1].record(main)
+            self.ev_loss[i % n].record(main)
+        main.wait_stream(side)
 
 
 class AdamParamsC(C.Structure):

@@ -255,3 +255,55 @@ def test_two_processes_cuda_ipc(oracle):
             vec = np.array([dd[k] for k in DIAG])
             assert vec[6] == want[6]
             assert_close(vec[:6], want[:6], TOL, f"ipc rank {rank} diag")
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_pipelined_batches_match_plain_steps(world):
+    """optim.Pipelined (batch i+1's assembly on a side stream overlapping batch i's loss, the
+    ckrl_*_step_assemble / _loss halves) gives every batch the same diagnostics and masks as
+    one ckrl_ppo_step per batch — single rank and across ranks (the exchange epoch travels in
+    each batch's workspace, so a later batch's assembly may publish before an earlier loss)."""
+    a, l, v = synth.SPECS["cfg3"]
+    spec = GranularitySpec(Level(a), Level(l), Level(v))
+    R, n_batches = 3, 7
+    data = [case("cfg3", 32, seed=20 + r) for r in range(R)]
+    comms = Comm.local_group(world) if world > 1 else [None]
+
+    def rank_inputs(r, rep):
+        cfg, d, logits = data[rep]
+        envs = env_shard(cfg.num_envs, world, r)
+        s = shard(d, envs)
+        ro = RolloutBuffer.from_arrays(s, s["boot_scalar"], cfg.vocab)
+        pol = PolicyOutputs(logits[envs.start:envs.stop],
+                            torch.tensor(s["new_value_scalar"], dtype=torch.float32, device="cuda"))
+        return ro, pol
+
+    inputs = [[rank_inputs(r, rep) for rep in range(R)] for r in range(world)]
+    params = PpoParams(0.2, 0.5, 0.01, True)
+    mk = lambda r, rep: optim.PpoStep(inputs[r][rep][0], GaeParams(0.99, 0.95), spec, params,  # noqa: E731
+                                      comm=comms[r])
+    # reference: plain steps, batch i on replica i mod R
+    plain = [[mk(r, rep) for rep in range(R)] for r in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    want = {}
+    for i in range(n_batches):
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                plain[r][i % R](*inputs[r][i % R], stream=streams[r])
+        torch.cuda.synchronize()
+        want[i] = [plain[r][i % R].diagnostics() for r in range(world)]
+    # pipelined
+    pipes = [optim.Pipelined([mk(r, rep) for rep in range(R)]) for r in range(world)]
+    for r in range(world):
+        with torch.cuda.stream(streams[r]):
+            pipes[r].issue(n_batches, lambda i, r=r: ((inputs[r][i % R][0],), inputs[r][i % R]))
+    torch.cuda.synchronize()
+    for r in range(world):
+        for rep in range(R):
+            last = max(i for i in range(n_batches) if i % R == rep)
+            got = pipes[r].steps[rep].diagnostics()
+            assert got == want[last][r], (r, rep)
+            assert torch.equal(pipes[r].steps[rep].batch.counted, plain[r][rep].batch.counted)
+    for c in comms:
+        if c is not None:
+            c.close()
