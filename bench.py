@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--no-pipeline", dest="pipeline", action="store_false",
                    help="PPO: one ckrl_ppo_step per batch instead of overlapping batch i+1's assembly "
                         "with batch i's loss")
+    p.add_argument("--head", type=int, default=0,
+                   help="row N2: feed the step from trunk features of this width H through the "
+                        "tcgen05 policy-head projection (ckrl_project_token_stats) instead of logits")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
@@ -378,6 +381,9 @@ def main():
     if args.config == "adam":
         bench_adam(args, rank, world, local)
         return
+    if args.head:
+        bench_head(args, rank, world, local)
+        return
 
     import numpy as np
     import torch
@@ -444,6 +450,9 @@ def main():
         step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
         run0 = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
         launches_per_step = 3
+        if args.pipeline and args.grad is None:
+            steps = [step] + [optim.GrpoStep(reps[r][0], opts, GrpoParams(0.2), comm=comm) for r in range(1, R)]
+            pipe = optim.Pipelined(steps)
     run = run0
     if args.grad == "fused":  # dlogits written by the loss launch itself (LossOutputs.dlogits)
         step.outputs.dlogits = torch.empty_like(reps[0][1].logits)
@@ -470,8 +479,12 @@ def main():
     torch.cuda.synchronize()
     diag0 = step.diagnostics()
     issue = lambda n: [run(i) for i in range(n)]  # noqa: E731  (K steps, eager order)
+    def pipe_args(i):  # (assembly args, loss args) of batch i
+        ro, pol, ept, _ = reps[i % R]
+        return ((ro,), (ro, pol)) if cfg.algo == "ppo" else ((ro, ept), (ro, pol))
+
     if pipe is not None:
-        issue = lambda n: pipe.issue(n, lambda i: ((reps[i % R][0],), (reps[i % R][0], reps[i % R][1])))  # noqa: E731
+        issue = lambda n: pipe.issue(n, pipe_args)  # noqa: E731
         issue(max(3, args.warmup))
         torch.cuda.synchronize()
 
@@ -524,13 +537,15 @@ def main():
     # so no launch waits on the host); otherwise each launch alone after its assembly
     live_kms = None
     if pipe is not None:
+        # the loss stream's time per launch over a chain of back-to-back launches (events before
+        # the first and after the last, none in between: consecutive losses overlap through
+        # programmatic dependent launch, so a launch's own start-to-end is not its cost)
         n_live = min(K, 50)
-        lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_live)]
+        span = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         torch.cuda._sleep(40_000_000)
-        pipe.issue(n_live, lambda i: ((reps[i % R][0],), (reps[i % R][0], reps[i % R][1])), loss_events=lev)
+        pipe.issue(n_live, pipe_args, span_events=span)
         torch.cuda.synchronize()
-        lt = sorted(e0.elapsed_time(e1) for e0, e1 in lev[2:])
-        live_kms = lt[len(lt) // 2]
+        live_kms = span[0].elapsed_time(span[1]) / n_live
     ws = step.ws
     kms = []
     for i in range(min(K, 50) + 3):  # 3 untimed launches first (first-call attribute setup)
@@ -630,9 +645,12 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),
                      "kernel_ms": kernel_ms,
-                     "kernel_timing": ("median loss launch inside a graph of pipelined steps (events on its stream)"
+                     "kernel_timing": ("loss-stream time per launch over a chain of pipelined steps (events "
+                                       "before the first and after the last launch; consecutive launches "
+                                       "overlap by programmatic dependent launch)"
                                        if live_kms is not None else "median loss launch alone after its assembly"),
                      "kernel_ms_alone": alone_ms,
+                     "frac_alone": kbytes / (alone_ms * 1e-3) / 1e9 / peak,
                      "algorithmic_bytes_per_launch": kbytes, "peak_kind": peak_kind,
                      "step_frac": (kbytes / (ms * 1e-3) / 1e9) / peak},
         "cpu_baseline": cpu,
@@ -649,6 +667,142 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- row N2: policy head
+def bench_head(args, rank, world, local):
+    """The PPO step fed from trunk features instead of logits: per step the tcgen05 projection
+    (ckrl_project_token_stats: [tokens x H] bf16 x W_pol[256 x H] -> per-token {lp, H} rows,
+    the logits never reach HBM), then assembly + loss from the rows. Replicas rotate so the
+    features exceed L2; pipelined like the logits-fed step."""
+    import torch
+    import paper_2510_06710_b200 as ck
+    from paper_2510_06710_b200 import optim, policy, synth
+    from paper_2510_06710_b200.core import GaeParams, GranularitySpec, Level, PolicyOutputs, PpoParams, RolloutBuffer
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    ck.lib()
+    assert args.config in ("cfg1", "cfg3"), "--head runs the PPO workloads"
+    cfg = synth.CONFIGS[args.config]
+    a, l, v = synth.SPECS[args.config]
+    spec = GranularitySpec(Level(a), Level(l), Level(v))
+    H = args.head
+    n_tok = env_steps(cfg) * cfg.tokens_per_action
+    feat_bytes = n_tok * H * 2
+    R = max(2, math.ceil(3 * L2_BYTES / feat_bytes))
+    g = torch.Generator(device=dev).manual_seed(11)
+    W = (torch.randn(256, H, device=dev, generator=g) * (2.0 / H ** 0.5)).to(torch.bfloat16)
+    bias = 0.1 * torch.randn(256, device=dev, generator=g)
+    shape = (cfg.num_envs, cfg.num_chunks, cfg.chunk_len, cfg.tokens_per_action)
+
+    class HeadStep:  # projection + loss in the loss half, so the assembly overlaps both
+        def __init__(self, inner, feat, tokens, rows):
+            self.inner, self.feat, self.tokens, self.rows = inner, feat, tokens, rows
+            self.comm = None
+
+        def assemble(self, *aa, stream=None):
+            self.inner.assemble(*aa, stream=stream)
+
+        def loss(self, ro, pol, stream=None):
+            policy.project_token_stats(self.feat, W, bias, self.tokens, rows_out=self.rows, stream=stream)
+            self.inner.loss(ro, pol, stream=stream)
+
+    reps, steps = [], []
+    for r in range(R):
+        c = synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + 101 * r})
+        d = synth.episodes_numpy(c, env_offset=rank * cfg.num_envs)
+        _, tokens, old = synth.token_tensors(c, dev, torch.float32, env_offset=rank * cfg.num_envs)
+        feat = torch.randn(*shape, H, device=dev, generator=g).to(torch.bfloat16)
+        rows = torch.empty((*shape, 2), dtype=torch.float64, device=dev)
+        pr = policy.project_token_stats(feat, W, bias, tokens, rows_out=rows)
+        d["tokens"], d["old_logprob"] = tokens, pr["token_logprob"].float() + 0.05 * torch.randn_like(old)
+        boot = d["boot_scalar"] if a == 0 else d["boot_vector0"]
+        ro = RolloutBuffer.from_arrays(d, boot, cfg.vocab, dev)
+        nv = d["new_value_scalar"] if v == 0 else d["new_value_vector"]
+        pol = PolicyOutputs(None, torch.tensor(nv, dtype=torch.float32, device=dev), token_rows=rows)
+        inner = optim.PpoStep(ro, GaeParams(0.99, 0.95), spec, PpoParams(0.2, 0.5, 0.01, True))
+        reps.append((ro, pol))
+        steps.append(HeadStep(inner, feat, tokens, rows))
+    pipe = optim.Pipelined(steps)
+    args_of = lambda i: ((reps[i % R][0],), reps[i % R])  # noqa: E731
+    stream = torch.cuda.current_stream()
+    pipe.issue(max(3, args.warmup), args_of)
+    torch.cuda.synchronize()
+    K = args.steps
+    gph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(stream)
+    with torch.cuda.stream(s):
+        pipe.issue(1, args_of)
+    stream.wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(gph):
+        pipe.issue(K, args_of)
+    gph.replay()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        gph.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / K
+    # the projection launch alone (events around each launch; nothing else on the device)
+    pev = []
+    for i in range(min(K, 30) + 3):
+        st = steps[i % R]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)
+        e0.record(stream)
+        policy.project_token_stats(st.feat, W, bias, st.tokens, rows_out=st.rows)
+        e1.record(stream)
+        pev.append((e0, e1))
+    torch.cuda.synchronize()
+    pt = sorted(e0.elapsed_time(e1) for e0, e1 in pev[3:])
+    pms = pt[len(pt) // 2]
+    flops = 2.0 * 256 * H * n_tok
+    pbytes = feat_bytes + 256 * H * 2 + n_tok * (16 + 1)  # features, W_pol, row records, tokens
+    tf = flops / (pms * 1e-3) / 1e12
+    gbs = pbytes / (pms * 1e-3) / 1e9
+    mp = {}
+    mpath = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mpath):
+        with open(mpath) as f:
+            mp = json.load(f)
+    tpeak = mp.get("bf16_tflops", 2250.0)  # burst figure: the projection is timed alone
+    hpeak, hkind = peaks()
+    bound = "tensor" if flops / (tpeak * 1e12) >= pbytes / (hpeak * 1e9) else "hbm"
+    diag = steps[0].inner.diagnostics()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": world * env_steps(cfg) / (ms * 1e-3), "unit": "env-steps/s", "n_gpus": world,
+        "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 features, f32 accumulate",
+        "data": "synthetic trunk features ~N(0,1) and a random-init policy head (no checkpoint)",
+        "config": {**workload(args, cfg, world), "head_hidden": H,
+                   "step_includes": "policy-head projection (tcgen05) + assemble + loss from token rows"},
+        "timing": {"l2": f"features rotate over {R} replicas ({R * feat_bytes / 2**20:.0f} MiB > 126 MB L2)",
+                   "cuda_graph": f"one graph of all {K} steps", "untimed_replay_before_timing": True,
+                   "pipelined": "batch i+1's assembly on a side stream overlaps batch i's projection + loss"},
+        "roofline": {"bound": bound, "achieved": tf if bound == "tensor" else gbs,
+                     "peak": tpeak if bound == "tensor" else hpeak,
+                     "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+                     "frac": tf / tpeak if bound == "tensor" else gbs / hpeak, "traffic": None,
+                     "kernel": "proj_stats_kernel (tcgen05.mma M128 N256 K16, TMEM accumulators, fused log-softmax epilogue)",
+                     "kernel_ms": pms, "kernel_timing": "median projection launch alone",
+                     "tensor_tflops": tf, "tensor_frac": tf / tpeak, "hbm_gbs": gbs, "hbm_frac": gbs / hpeak,
+                     "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": pbytes,
+                     "peak_kind": "measured (MEASURED_PEAKS.json bf16_tflops burst / hbm_gbs)"},
+        "cpu_baseline": {"value": None, "unit": "env-steps/s", "cores": 0, "kind": "unavailable",
+                         "sample": "not timed for the head variant (the headline cfg3 line carries the CPU baseline)"},
+        "e2e": None,
+        "gpu_launches": K * 3,
+        "clocks": clk.summary(),
+        "diagnostics": {k: diag[k] for k in ("loss", "surrogate", "value_loss", "entropy", "clip_frac",
+                                              "approx_kl", "units")},
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- row f4: Adam

@@ -63,7 +63,18 @@ typedef enum {
 
 /* core/granularity.hpp:8 enum class Level { Chunk, Action, Token } */
 enum { CKRL_LEVEL_CHUNK = 0, CKRL_LEVEL_ACTION = 1, CKRL_LEVEL_TOKEN = 2 };
-enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3, CKRL_DTYPE_F64 = 4 };
+enum { CKRL_DTYPE_F32 = 0, CKRL_DTYPE_BF16 = 1, CKRL_DTYPE_U8 = 2, CKRL_DTYPE_I32 = 3, CKRL_DTYPE_F64 = 4,
+       CKRL_DTYPE_TOKEN_ROWS = 5 /* ckrl_token_row per position (ckrl_project_token_stats) */ };
+
+/* One position's finished token statistics: the sampled token's log-prob (fp64) and the
+ * entropy of the position's distribution (evaluate_chunk's token_logprobs / entropy,
+ * policy/policy_net.cpp:333-357). Written by ckrl_project_token_stats; consumed by the losses
+ * in place of logits when ckrl_policy_outputs.logits_dtype == CKRL_DTYPE_TOKEN_ROWS. */
+typedef struct {
+  double logprob;
+  float entropy;
+  uint32_t reserved; /* 0 */
+} ckrl_token_row;
 
 /* Communicator of a multi-rank job: peer-memory exchange buffers (+ optional NCCL), below. */
 typedef struct ckrl_comm ckrl_comm;
@@ -118,7 +129,9 @@ typedef struct {
 /* Current-policy outputs consumed by the loss (what ppo_loss recomputes through
  * PolicyNet::evaluate_chunk / value, losses.cpp:115, 196). Device pointers. */
 typedef struct {
-  int32_t logits_dtype; /* CKRL_DTYPE_F32 | CKRL_DTYPE_BF16 */
+  int32_t logits_dtype; /* CKRL_DTYPE_F32 | CKRL_DTYPE_BF16 | CKRL_DTYPE_TOKEN_ROWS (logits then
+                           points at [E][Tc][C][M] ckrl_token_row: the policy head already
+                           reduced on the tensor cores, ckrl_project_token_stats) */
   const void* logits;
   const float* values;  /* new values at the value level; may be NULL if value_loss_coef == 0 */
 } ckrl_policy_outputs;
@@ -310,6 +323,29 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t chunk_len, int32_t tokens_p
                          const uint8_t* slot_mask, double* action_entropy, double* chunk_entropy,
                          ckrl_stream_t stream);
 
+/* The policy head: PolicyNet::logits_from_feature (policy/policy_net.cpp:265-274),
+ * logits[v] = sum_h W_pol[v][h] * feature[h] + b_pol[v], over the trunk feature of every
+ * position (the hidden state forward_logits feeds it, :276-284). */
+typedef struct {
+  int32_t hidden;        /* H: a multiple of 64, 64 .. 16384 */
+  int32_t vocab;         /* bins: 256 */
+  const void* feature;   /* [rows][H] bf16, 16-byte aligned, row pitch H */
+  const void* w_pol;     /* [vocab][H] bf16 (the reference's row-major W_pol block) */
+  const float* b_pol;    /* [vocab] f32; NULL = zero bias */
+} ckrl_policy_head;
+
+/* Row N2: the hidden -> action-bin projection on the tensor cores (tcgen05.mma, bf16 inputs,
+ * f32 accumulators in TMEM) fused with evaluate_chunk's per-position reduction
+ * (policy_net.cpp:90-102, 333-357): per position the sampled token's log-prob and the
+ * entropy, without the [rows][256] logits ever reaching HBM. Outputs (each nullable):
+ * token_rows ([rows] ckrl_token_row, the losses' CKRL_DTYPE_TOKEN_ROWS input), token_logprob
+ * (f64), token_entropy (f32), and the logits themselves (logits_dtype F32 | BF16, [rows][256])
+ * for callers that still want them. Asynchronous on `stream`. */
+int32_t ckrl_project_token_stats(int64_t rows, const ckrl_policy_head* head, int32_t token_dtype,
+                                 const void* tokens, ckrl_token_row* token_rows,
+                                 double* token_logprob, float* token_entropy, int32_t logits_dtype,
+                                 void* logits, ckrl_stream_t stream);
+
 /* ---- (f1) softmax-backward seam --------------------------------------------------------- */
 
 /* The per-position logits gradient PolicyNet::accumulate_chunk_gradient forms before its
@@ -450,7 +486,21 @@ typedef struct {
   int32_t obs_dim, hidden, trunk_layers, value_hidden, vocab, chunk_len, tokens_per_action;
 } ckrl_policy_desc;
 
-/* RolloutSpec (placement/rollout.hpp:16-22) + pipeline depth k (PlacementPlan::pipeline_stage_num). */
+/* Samplers of StageGen (policy_net.cpp:286-331). REFERENCE sums the 256 exponentials and
+ * walks the inverse CDF serially in the reference's order (bit-exact with sample_chunk);
+ * PARALLEL does both as fixed-order block reductions / scans (warp shuffles), so the draw is
+ * the same for every k and placement but may differ from the reference's in the last ulp of
+ * the log-sum-exp (and, at a CDF boundary within an ulp of u, in the token). */
+enum { CKRL_SAMPLER_REFERENCE = 0, CKRL_SAMPLER_PARALLEL = 1 };
+
+/* RolloutSpec (placement/rollout.hpp:16-22) + pipeline depth k (PlacementPlan::pipeline_stage_num)
+ * + placement. gen_device < 0: colocated (PlacementMode::Colocated, plan.cpp:60-68): env and
+ * generation kernels share the calling device. gen_device >= 0: the generation role runs on
+ * that device (hybrid / disaggregated placement; it may equal the env device, which keeps the
+ * hand-offs): every chunk the stage's observation batch is copied env -> gen and its action
+ * batch (tokens, log-probs, values, optional logits) gen -> env over NVLink peer copies, the
+ * reference's obs / act channels (real_backend.cpp:15-37, 59-138), with per-stage events on
+ * both devices. The slab is bit-identical across k and placement. */
 typedef struct {
   ckrl_env_config env;
   ckrl_policy_desc policy;
@@ -458,7 +508,19 @@ typedef struct {
   int32_t stages;                 /* k: env partitions, must divide num_envs */
   uint64_t sample_seed;
   const int32_t* reset_state_ids; /* [num_envs] device, or NULL */
+  int32_t sampler;                /* CKRL_SAMPLER_* */
+  int32_t gen_device;             /* -1 colocated; else the generation device */
+  void* gen_workspace;            /* gen_device >= 0: ckrl_pipeline_gen_workspace_bytes on gen_device */
+  size_t gen_workspace_bytes;
 } ckrl_pipeline_spec;
+
+/* derive_mode (placement/plan.cpp:60-68) after validate_plan (:49-58) of a PlacementPlan
+ * given as inclusive slot ranges: 0 colocated, 1 disaggregated, 2 hybrid; negative on an
+ * invalid plan (CKRL_ERR_INVALID_PLAN in *status). */
+enum { CKRL_PLACEMENT_COLOCATED = 0, CKRL_PLACEMENT_DISAGGREGATED = 1, CKRL_PLACEMENT_HYBRID = 2 };
+int32_t ckrl_placement_mode(int32_t num_slots, int32_t env_begin, int32_t env_end, int32_t rollout_begin,
+                            int32_t rollout_end, int32_t actor_begin, int32_t actor_end,
+                            int32_t pipeline_stage_num, int32_t* status);
 
 /* The epoch's slab in the ckrl_rollout layout (f32 for the loss, f64 copies for exact
  * comparison with the reference) + the merged episode table. Device pointers. */
@@ -491,6 +553,9 @@ typedef struct {
 
 int64_t ckrl_policy_num_params(const ckrl_policy_desc* desc);
 size_t ckrl_pipeline_workspace_bytes(const ckrl_pipeline_spec* spec);
+/* Generation-side scratch for gen_device >= 0 (policy copy, sampling streams, obs / action
+ * staging), allocated by the caller on gen_device. */
+size_t ckrl_pipeline_gen_workspace_bytes(const ckrl_pipeline_spec* spec);
 /* One rollout epoch (StageSim / StageGen / merge_stages, placement/rollout.cpp:11-109;
  * RealBackend::run_rollout_epoch, real_backend.cpp:59-138): k stage partitions, gen and
  * sim kernels on two streams with per-stage event hand-offs; the slab is identical for

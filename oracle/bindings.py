@@ -114,6 +114,18 @@ class Oracle:
         self.lib.orc_token_stats(C.c_int64(rows), V, _p(lg), _p(tk), _p(lp), _p(ent))
         return lp, ent
 
+    def project_logits(self, feature, w_pol, b_pol=None):
+        """logits_from_feature (policy_net.cpp:265-274) per row: [rows][H] x [V][H] -> [rows][V]."""
+        f = _c64(feature)
+        W = _c64(w_pol)
+        V, H = W.shape
+        f = f.reshape(-1, H)
+        rows = f.shape[0]
+        b = None if b_pol is None else _c64(b_pol).reshape(-1)
+        out = np.zeros((rows, V))
+        self.lib.orc_project_logits(C.c_int64(rows), H, V, _p(f), _p(W), _p(b), _p(out))
+        return out
+
     def entropy_aggregates(self, ent, chunk_len, tokens_per_action, mask=None):
         """Per-token entropies [chunks*C*M] -> (action [chunks][C], chunk [chunks]) entropy in
         canonical order over the `mask` [chunks][C] slots (default all)."""
@@ -300,6 +312,24 @@ def ref_adam(params, grads, lr, max_grad_norm=0.0, beta1=0.9, beta2=0.999, eps=1
     st = lib.refx_adam(C.c_longlong(n), steps, _p(p), _p(g), C.c_double(lr), C.c_double(max_grad_norm),
                        C.c_double(beta1), C.c_double(beta2), C.c_double(eps), _p(norms))
     return st, p, g, norms
+
+
+def ref_project_token_stats(feature, w_pol, b_pol, tokens):
+    """The reference's forward_logits + evaluate_chunk on a head-only PolicyNet whose trunk
+    input is each position's feature (ref_shim.cpp refx_project_token_stats)."""
+    lib = _ref_lib()
+    W = _c64(w_pol)
+    V, H = W.shape
+    f = _c64(feature).reshape(-1, H)
+    rows = f.shape[0]
+    b = None if b_pol is None else _c64(b_pol).reshape(-1)
+    tk = np.ascontiguousarray(tokens, dtype=np.int32).reshape(-1)
+    logits, lp, ent = np.zeros((rows, V)), np.zeros(rows), np.zeros(rows)
+    st = lib.refx_project_token_stats(C.c_longlong(rows), H, V, _p(f), _p(W), _p(b), _p(tk), _p(logits),
+                                      _p(lp), _p(ent))
+    if st:
+        raise RuntimeError(lib.refx_last_error().decode())
+    return logits, lp, ent
 
 
 def ref_load_checkpoint(path: str):

@@ -68,6 +68,22 @@ void orc_log_softmax(int V, const double* x, double* out) {
   for (int v = 0; v < V; ++v) out[v] = x[v] - lse;
 }
 
+/* PolicyNet::logits_from_feature (policy/policy_net.cpp:265-274): per position,
+ * logits[v] = matvec(W_pol, h)[v] + b_pol[v] -- matvec (:13-21) sums row[c] * x[c] in ascending
+ * c from 0.0, then the bias is added. W is [V][H] row-major; b may be NULL (zero bias). */
+void orc_project_logits(int64_t rows, int H, int V, const double* feature, const double* W,
+                        const double* b, double* logits) {
+  for (int64_t k = 0; k < rows; ++k) {
+    const double* h = feature + k * H;
+    for (int v = 0; v < V; ++v) {
+      double s = 0.0;
+      const double* row = W + (int64_t)v * H;
+      for (int c = 0; c < H; ++c) s += row[c] * h[c];
+      logits[k * V + v] = s + (b ? b[v] : 0.0);
+    }
+  }
+}
+
 /* policy/policy_net.cpp:345-355 (evaluate_chunk, per position) */
 void orc_token_stats(int64_t rows, int V, const double* logits, const int32_t* tokens,
                      double* lp, double* ent) {

@@ -136,8 +136,29 @@ def dump_fixture():
     print("wrote", path, len(text), "bytes of dump text")
 
 
+def proj_fixture():
+    """proj_h128.npz: the reference's own policy head (forward_logits + evaluate_chunk on a
+    head-only PolicyNet, ref_shim.cpp refx_project_token_stats) over bf16-representable
+    features / W_pol / b_pol, for tests/test_gpu_projection.py on the GPU box (row N2)."""
+    import torch
+    from oracle.bindings import ref_project_token_stats
+    g = torch.Generator().manual_seed(31)
+    rows, H, V = 200, 128, 256
+    f = torch.randn(rows, H, generator=g).to(torch.bfloat16).double().numpy()
+    W = (torch.randn(V, H, generator=g) * (2.0 / H ** 0.5)).to(torch.bfloat16).double().numpy()
+    b = (0.5 * torch.randn(V, generator=g)).to(torch.bfloat16).double().numpy()
+    tok = torch.randint(0, V, (rows,), generator=g).numpy().astype(np.int32)
+    logits, lp, ent = ref_project_token_stats(f, W, b, tok)
+    path = os.path.join(OUT, "proj_h128.npz")
+    np.savez_compressed(path, feature=f, w_pol=W, b_pol=b, tokens=tok, logits=logits, lp=lp, ent=ent)
+    print("wrote", path)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dump":
         dump_fixture()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "proj":
+        proj_fixture()
         sys.exit(0)
     main()

@@ -217,6 +217,49 @@ int refx_adam(long long n, int steps, double* params, double* grads, double lr, 
   }
 }
 
+// The policy head through the reference's public PolicyNet API, per position: a net with
+// obs_dim 1, no trunk layers and C = M = 1, whose input bias b_in is set to the position's
+// feature h (pos_bias and the embeddings zero, obs = {0}), so trunk_forward's x is exactly h
+// (policy_net.cpp:206-210) and forward_logits returns logits_from_feature(h) = W_pol h + b_pol
+// (:265-284); evaluate_chunk then gives the token's log-prob and entropy (:333-357).
+// Parameter offsets follow PolicyNet::Layout (:114-143). logits [rows][V], lp / ent [rows].
+int refx_project_token_stats(long long rows, int H, int V, const double* feature, const double* W,
+                             const double* b, const int* tokens, double* logits, double* lp, double* ent) {
+  try {
+    policy::PolicyDescriptor d;
+    d.obs_dim = 1;
+    d.hidden = H;
+    d.trunk_layers = 0;
+    d.value_hidden = 1;
+    d.vocab = V;
+    d.C = 1;
+    d.M = 1;
+    policy::PolicyNet net(d);
+    std::vector<double> p(net.num_params(), 0.0);
+    const std::size_t b_in = static_cast<std::size_t>(H), emb = 3 * static_cast<std::size_t>(H);
+    const std::size_t w_pol = emb + static_cast<std::size_t>(V) * H, b_pol = w_pol + static_cast<std::size_t>(V) * H;
+    std::copy(W, W + static_cast<std::size_t>(V) * H, p.begin() + static_cast<std::ptrdiff_t>(w_pol));
+    if (b) std::copy(b, b + V, p.begin() + static_cast<std::ptrdiff_t>(b_pol));
+    const Observation obs{0.0};
+    for (long long k = 0; k < rows; ++k) {
+      std::copy(feature + k * H, feature + (k + 1) * H, p.begin() + static_cast<std::ptrdiff_t>(b_in));
+      net.set_params(p);
+      const std::vector<double> lg = net.forward_logits(obs, {});
+      std::copy(lg.begin(), lg.end(), logits + k * V);
+      ActionChunk ch;
+      ch.actions.resize(1);
+      ch.actions[0].tokens = {tokens[k]};
+      const policy::ChunkEval ev = net.evaluate_chunk(obs, ch);
+      lp[k] = ev.token_logprobs.values[0];
+      ent[k] = ev.entropy[0];
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return status_of(ex);
+  }
+}
+
 // The reference's own dump_slab (core/types.cpp:9-28) of the scenario's slab; *len gets the
 // full length, at most cap bytes are copied.
 int refx_dump_slab(void* h, char* out, size_t cap, size_t* len) {

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CKRL_LIB") or os.path.join(HERE, "libckrl.so")
 
 LEVEL_CHUNK, LEVEL_ACTION, LEVEL_TOKEN = 0, 1, 2
-DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32, DTYPE_F64 = 0, 1, 2, 3, 4
+DTYPE_F32, DTYPE_BF16, DTYPE_U8, DTYPE_I32, DTYPE_F64, DTYPE_TOKEN_ROWS = 0, 1, 2, 3, 4, 5
 FLAG_TERMINATED, FLAG_TRUNCATED, FLAG_VALID = 1, 2, 4
 DIAG_COUNT = 8
 DIAG_NAMES = ("loss", "surrogate", "value_loss", "entropy", "clip_frac", "approx_kl", "units",
@@ -59,6 +59,10 @@ class PolicyOutputs(C.Structure):
     _fields_ = [("logits_dtype", C.c_int32), ("logits", vp), ("values", vp)]
 
 
+class PolicyHead(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("vocab", C.c_int32), ("feature", vp), ("w_pol", vp), ("b_pol", vp)]
+
+
 class Episodes(C.Structure):
     _fields_ = [("count", C.c_int32), ("env_id", vp), ("episode_id", vp), ("start_step", vp),
                 ("length", vp), ("total_reward", vp), ("first_success", vp), ("complete", vp),
@@ -93,9 +97,15 @@ class PolicyDesc(C.Structure):
                                          "vocab", "chunk_len", "tokens_per_action")]
 
 
+SAMPLER_REFERENCE, SAMPLER_PARALLEL = 0, 1
+PLACEMENT_COLOCATED, PLACEMENT_DISAGGREGATED, PLACEMENT_HYBRID = 0, 1, 2
+
+
 class PipelineSpec(C.Structure):
     _fields_ = [("env", EnvConfig), ("policy", PolicyDesc), ("num_chunks", C.c_int32),
-                ("stages", C.c_int32), ("sample_seed", C.c_uint64), ("reset_state_ids", vp)]
+                ("stages", C.c_int32), ("sample_seed", C.c_uint64), ("reset_state_ids", vp),
+                ("sampler", C.c_int32), ("gen_device", C.c_int32), ("gen_workspace", vp),
+                ("gen_workspace_bytes", C.c_size_t)]
 
 
 PIPELINE_OUTPUT_FIELDS = (
@@ -131,6 +141,8 @@ SIGNATURES = {
                                              P(GrpoOptions), P(GrpoBatchC), vp, C.c_size_t, vp]),
     "ckrl_token_stats": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
                                      C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ckrl_project_token_stats": (C.c_int32, [C.c_int64, P(PolicyHead), C.c_int32, vp, vp, vp, vp, C.c_int32,
+                                             vp, vp]),
     "ckrl_ppo_loss": (C.c_int32, [P(Rollout), P(PpoBatchC), P(PolicyOutputs), P(Granularity),
                                   P(PpoParams), P(LossOutputs), vp, vp, C.c_size_t, vp]),
     "ckrl_grpo_loss": (C.c_int32, [P(Rollout), P(GrpoBatchC), P(PolicyOutputs), P(Granularity),
@@ -175,6 +187,8 @@ SIGNATURES = {
     "ckrl_slab_success_rate": (C.c_int32, [P(Episodes), vp, vp]),
     "ckrl_policy_num_params": (C.c_int64, [P(PolicyDesc)]),
     "ckrl_pipeline_workspace_bytes": (C.c_size_t, [P(PipelineSpec)]),
+    "ckrl_pipeline_gen_workspace_bytes": (C.c_size_t, [P(PipelineSpec)]),
+    "ckrl_placement_mode": (C.c_int32, [C.c_int32] * 8 + [P(C.c_int32)]),
     "ckrl_pipeline_run": (C.c_int32, [P(PipelineSpec), vp, P(PipelineOutputs), vp, C.c_size_t,
                                       vp]),
     "ckrl_comm_unique_id": (C.c_int32, [vp]),

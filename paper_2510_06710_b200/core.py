@@ -195,10 +195,15 @@ class EpisodeTable:
 class PolicyOutputs:
     """Current-policy outputs the loss consumes (what ppo_loss recomputes through
     PolicyNet::evaluate_chunk / value, optim/losses.cpp:115, 196)."""
-    logits: torch.Tensor                  # [E][Tc][C][M][V] f32 or bf16
+    logits: Optional[torch.Tensor]        # [E][Tc][C][M][V] f32 or bf16
     values: Optional[torch.Tensor] = None  # [E][Tc] or [E][Tc][C] f32
+    # or, in place of logits, the policy head already reduced on the tensor cores:
+    # [E][Tc][C][M] ckrl_token_row as a [..., 2] f64 tensor (policy.project_token_stats)
+    token_rows: Optional[torch.Tensor] = None
 
     def c(self) -> _lib.PolicyOutputs:
+        if self.token_rows is not None:
+            return _lib.PolicyOutputs(_lib.DTYPE_TOKEN_ROWS, _ptr(self.token_rows), _ptr(self.values))
         dt = _lib.DTYPE_BF16 if self.logits.dtype == torch.bfloat16 else _lib.DTYPE_F32
         return _lib.PolicyOutputs(dt, _ptr(self.logits), _ptr(self.values))
 

@@ -105,6 +105,7 @@ LossArgs base_args(const ckrl_rollout* ro, const ckrl_policy_outputs* po, char* 
   a.logits_bf16 = po->logits_dtype == CKRL_DTYPE_BF16;
   a.tok_i32 = ro->token_dtype == CKRL_DTYPE_I32;
   a.logits = po->logits;
+  if (po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS) a.rows_in = static_cast<const ckrl_token_row*>(po->logits);
   a.tokens = ro->tokens;
   a.old_lp = ro->old_logprob;
   a.ws = ws;
@@ -128,12 +129,13 @@ void set_outputs(LossArgs& a, const ckrl_loss_outputs* o) {
 
 int32_t check_policy(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
   CKRL_REQUIRE(po != nullptr, CKRL_ERR_INVALID_ARGUMENT, "policy outputs are null");
-  CKRL_REQUIRE(po->logits_dtype == CKRL_DTYPE_F32 || po->logits_dtype == CKRL_DTYPE_BF16,
-               CKRL_ERR_INVALID_ARGUMENT, "logits dtype must be f32 or bf16");
+  CKRL_REQUIRE(po->logits_dtype == CKRL_DTYPE_F32 || po->logits_dtype == CKRL_DTYPE_BF16 ||
+                   po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS,
+               CKRL_ERR_INVALID_ARGUMENT, "logits dtype must be f32, bf16 or token rows");
   if ((int64_t)ro->num_envs * ro->num_chunks > 0)
     CKRL_REQUIRE(po->logits && ro->tokens && ro->old_logprob, CKRL_ERR_INVALID_ARGUMENT,
                  "logits, tokens and old_logprob are required");
-  if (ro->vocab == 256) {
+  if (ro->vocab == 256 || po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS) {
     uintptr_t p = reinterpret_cast<uintptr_t>(po->logits);
     CKRL_REQUIRE((p & 15) == 0, CKRL_ERR_INVALID_ARGUMENT, "logits must be 16-byte aligned");
   }
@@ -389,7 +391,44 @@ int32_t ckrl_token_stats(int64_t num_chunks, int32_t C, int32_t M, int32_t V, in
   a.stats_mask = slot_mask;
   a.all_rows = 1;
   a.world = 0;
+  if (logits_dtype == CKRL_DTYPE_TOKEN_ROWS) {
+    CKRL_REQUIRE((reinterpret_cast<uintptr_t>(logits) & 15) == 0, CKRL_ERR_INVALID_ARGUMENT,
+                 "token rows must be 16-byte aligned");
+    a.rows_in = static_cast<const ckrl_token_row*>(logits);
+  } else {
+    CKRL_REQUIRE(logits_dtype == CKRL_DTYPE_F32 || logits_dtype == CKRL_DTYPE_BF16, CKRL_ERR_INVALID_ARGUMENT,
+                 "logits dtype must be f32, bf16 or token rows");
+  }
   CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));
+  return CKRL_OK;
+}
+
+// Row N2: policy head on the tensor cores + per-position reduction (csrc/proj.cu).
+int32_t ckrl_project_token_stats(int64_t rows, const ckrl_policy_head* head, int32_t token_dtype,
+                                 const void* tokens, ckrl_token_row* token_rows, double* token_logprob,
+                                 float* token_entropy, int32_t logits_dtype, void* logits,
+                                 ckrl_stream_t stream) {
+  int32_t st = check_device();
+  if (st) return st;
+  CKRL_REQUIRE(head != nullptr, CKRL_ERR_INVALID_ARGUMENT, "policy head is null");
+  CKRL_REQUIRE(rows >= 0 && rows <= (int64_t)INT32_MAX, CKRL_ERR_LENGTH_MISMATCH, "rows out of range");
+  CKRL_REQUIRE(head->vocab == 256, CKRL_ERR_LENGTH_MISMATCH, "the projection kernel needs vocab == 256");
+  CKRL_REQUIRE(head->hidden >= 64 && head->hidden <= 16384 && head->hidden % 64 == 0,
+               CKRL_ERR_LENGTH_MISMATCH, "hidden must be a multiple of 64 in [64, 16384]");
+  CKRL_REQUIRE(token_dtype == CKRL_DTYPE_U8 || token_dtype == CKRL_DTYPE_I32, CKRL_ERR_INVALID_ARGUMENT,
+               "token dtype must be u8 or i32");
+  CKRL_REQUIRE(!logits || logits_dtype == CKRL_DTYPE_F32 || logits_dtype == CKRL_DTYPE_BF16,
+               CKRL_ERR_INVALID_ARGUMENT, "logits output dtype must be f32 or bf16");
+  if (rows == 0) return CKRL_OK;
+  CKRL_REQUIRE(head->feature && head->w_pol && tokens, CKRL_ERR_INVALID_ARGUMENT,
+               "feature, w_pol and tokens are required");
+  CKRL_REQUIRE(((reinterpret_cast<uintptr_t>(head->feature) | reinterpret_cast<uintptr_t>(head->w_pol)) & 15) == 0,
+               CKRL_ERR_INVALID_ARGUMENT, "feature / w_pol must be 16-byte aligned");
+  CKRL_REQUIRE((reinterpret_cast<uintptr_t>(token_rows) & 15) == 0, CKRL_ERR_INVALID_ARGUMENT,
+               "token rows must be 16-byte aligned");
+  CKRL_CUDA(launch_proj_stats(rows, head->hidden, head->feature, head->w_pol, head->b_pol, tokens,
+                              token_dtype == CKRL_DTYPE_I32, token_rows, token_logprob, token_entropy, logits,
+                              logits_dtype == CKRL_DTYPE_BF16, 0, (cudaStream_t)stream));
   return CKRL_OK;
 }
 
@@ -518,6 +557,20 @@ static int overlap_sms() {
   static int n = -1;
   if (n < 0) {
     const char* env = getenv("CKRL_ASM_SMS");
+    n = env ? atoi(env) : 1;
+  }
+  return n;
+}
+
+// Pipelined steps: each batch's loss launched as a programmatic dependent of the previous
+// launch on its stream (the previous batch's loss), so its logits stream while that loss's
+// tail runs; the unit phase still waits for the predecessor (griddepcontrol.wait), so a
+// same-stream assembly or any producer that does not trigger early stays a full dependency.
+// CKRL_CHAIN=0 disables (A/B).
+static int chain_enabled() {
+  static int n = -1;
+  if (n < 0) {
+    const char* env = getenv("CKRL_CHAIN");
     n = env ? atoi(env) : 1;
   }
   return n;
@@ -782,6 +835,10 @@ int32_t ckrl_ppo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1);
   a.ex = exchange_view(comm);
   a.max_ctas = loss_cta_cap(comm);
+  if (chain_enabled() && po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS) {
+    a.pdl = 1;
+    a.ro = *ro;
+  }
   CKRL_CUDA(launch_tile(a, (cudaStream_t)stream, nullptr));
   return CKRL_OK;
 }
@@ -819,7 +876,8 @@ int32_t ckrl_grpo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* p
   WsLayout L = ws_layout(ro->num_envs, world);
   return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
-                        (cudaStream_t)stream, 0, exchange_view(comm), loss_cta_cap(comm));
+                        (cudaStream_t)stream, chain_enabled() && po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS,
+                        exchange_view(comm), loss_cta_cap(comm));
 }
 
 int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream) {
@@ -965,7 +1023,38 @@ static int32_t check_pipeline(const ckrl_pipeline_spec* sp) {
                CKRL_ERR_CONFIG, "bad pipeline dimensions");
   CKRL_REQUIRE(!e.use_fixed_reset_state_ids || sp->reset_state_ids, CKRL_ERR_BAD_RESET_ID,
                "use_fixed_reset_state_ids requires reset_state_ids");
+  CKRL_REQUIRE(sp->sampler == CKRL_SAMPLER_REFERENCE || sp->sampler == CKRL_SAMPLER_PARALLEL,
+               CKRL_ERR_CONFIG, "unknown sampler");
   return CKRL_OK;
+}
+
+int32_t ckrl_placement_mode(int32_t num_slots, int32_t env_begin, int32_t env_end, int32_t rollout_begin,
+                            int32_t rollout_end, int32_t actor_begin, int32_t actor_end,
+                            int32_t pipeline_stage_num, int32_t* status) {
+  auto bad = [&](const std::string& msg) {
+    if (status) *status = CKRL_ERR_INVALID_PLAN;
+    fail(CKRL_ERR_INVALID_PLAN, msg);
+    return -1;
+  };
+  if (status) *status = CKRL_OK;
+  // validate_plan (placement/plan.cpp:49-58) + SlotRange::parse's end >= begin (:27-28)
+  if (num_slots < 1) return bad("cluster needs at least one slot");
+  const int32_t r[3][2] = {{env_begin, env_end}, {rollout_begin, rollout_end}, {actor_begin, actor_end}};
+  for (const auto& q : r) {
+    if (q[1] < q[0]) return bad("bad slot range");
+    if (q[0] < 0 || q[1] >= num_slots) return bad("slot range outside cluster");
+  }
+  if (pipeline_stage_num < 1) return bad("pipeline_stage_num must be >= 1");
+  // derive_mode (:60-68)
+  auto same = [](const int32_t* a, const int32_t* b) { return a[0] == b[0] && a[1] == b[1]; };
+  auto overlaps = [](const int32_t* a, const int32_t* b) { return a[0] <= b[1] && b[0] <= a[1]; };
+  if (same(r[0], r[1]) && same(r[1], r[2])) return CKRL_PLACEMENT_COLOCATED;
+  const bool disjoint = !overlaps(r[0], r[1]) && !overlaps(r[0], r[2]) && !overlaps(r[1], r[2]);
+  return disjoint ? CKRL_PLACEMENT_DISAGGREGATED : CKRL_PLACEMENT_HYBRID;
+}
+
+size_t ckrl_pipeline_gen_workspace_bytes(const ckrl_pipeline_spec* sp) {
+  return check_pipeline(sp) == CKRL_OK ? pipeline_gen_ws_bytes(*sp) : 0;
 }
 
 size_t ckrl_pipeline_workspace_bytes(const ckrl_pipeline_spec* sp) {
@@ -980,6 +1069,13 @@ int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* sp, const double* params,
   if ((st = check_device())) return st;
   CKRL_REQUIRE(params && out && ws, CKRL_ERR_INVALID_ARGUMENT, "params / outputs / workspace required");
   CKRL_REQUIRE(ws_bytes >= pipeline_ws_bytes(*sp), CKRL_ERR_INVALID_ARGUMENT, "pipeline workspace too small");
+  if (sp->gen_device >= 0) {
+    int n = 0;
+    cudaGetDeviceCount(&n);
+    CKRL_REQUIRE(sp->gen_device < n, CKRL_ERR_INVALID_ARGUMENT, "gen_device out of range");
+    CKRL_REQUIRE(sp->gen_workspace && sp->gen_workspace_bytes >= pipeline_gen_ws_bytes(*sp),
+                 CKRL_ERR_INVALID_ARGUMENT, "generation workspace missing or too small");
+  }
   CKRL_CUDA(pipeline_run(*sp, params, *out, (char*)ws, (cudaStream_t)stream));
   return CKRL_OK;
 }

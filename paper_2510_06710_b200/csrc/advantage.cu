@@ -565,7 +565,9 @@ __device__ void copy_bytes(void* dst, const void* src, int64_t bytes) {
 __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
   const int C = a.src.chunk_len, M = a.src.tokens_per_action, V = a.src.vocab;
   const int tb = a.src.token_dtype == CKRL_DTYPE_I32 ? 4 : 1;
-  const int lb = a.sp.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4;
+  // bytes per position: a V-bin logits row, or one finished token row (row N2)
+  const int64_t pb = a.sp.logits_dtype == CKRL_DTYPE_TOKEN_ROWS ? (int64_t)sizeof(ckrl_token_row)
+                     : (int64_t)V * (a.sp.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
   const int U = a.action_level ? C : 1;
   const int NV = a.value_action ? C : 1;
   AsmPartial mine{{0.0, 0.0, 0.0}, 0.0};
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(128) select_records_kernel(SelectArgs a) {
     const int64_t r = a.idx[i];
     const int64_t P = (int64_t)C * M;
     if (a.sp.logits)
-      copy_bytes((char*)a.dp.logits + i * P * V * lb, (const char*)a.sp.logits + r * P * V * lb, P * V * lb);
+      copy_bytes((char*)a.dp.logits + i * P * pb, (const char*)a.sp.logits + r * P * pb, P * pb);
     const int t = threadIdx.x;
     for (int k = t; k < P; k += blockDim.x) {
       if (a.src.tokens) {

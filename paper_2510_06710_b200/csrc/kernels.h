@@ -65,6 +65,7 @@ struct LossArgs {
   int rows_cap;  // TMA kernel: rows per buffer (rec_per_tile * C * M, rounded up to 8)
   int slots_cap; // TMA kernel: slots per buffer (rec_per_tile * C, rounded up to 8)
   void* dlogits; // optional fused softmax-backward output [positions][V] (logits dtype)
+  const ckrl_token_row* rows_in;  // finished per-position {lp, H} instead of logits (row N2)
 };
 
 cudaError_t launch_ppo_assemble(const ckrl_rollout& ro, int action_level, double gamma,
@@ -98,8 +99,12 @@ cudaError_t launch_logits_grad(const void* logits, int logits_bf16, const void* 
                                const float* coeff_lp, const float* coeff_ent, int64_t rows, int V,
                                void* out, int out_bf16, int32_t* status, cudaStream_t s);
 cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t launch_proj_stats(int64_t rows, int H, const void* feature, const void* w_pol, const float* b_pol,
+                              const void* tokens, int tok_i32, ckrl_token_row* out, double* lp, float* ent,
+                              void* logits, int logits_bf16, int max_ctas, cudaStream_t s);
 cudaError_t read_timeline(uint64_t* out, int n);
 size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp);
+size_t pipeline_gen_ws_bytes(const ckrl_pipeline_spec& sp);
 cudaError_t launch_select_records(const ckrl_rollout& src, const ckrl_ppo_batch& sb, const ckrl_policy_outputs& sp,
                                   int action_level, int value_action, int64_t n, const int64_t* idx,
                                   const ckrl_rollout& dst, const ckrl_ppo_batch& db,

@@ -390,10 +390,18 @@ __device__ __forceinline__ void unit_phase(const LossArgs& a, const LossConsts& 
     const int64_t kk = k0 + row;
     const int64_t slot = kk / M;
     const int64_t rec = kk / P;
-    const double s = (double)sm.s[row];
-    const double ls = log(s);
-    const double lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
-    const float ent = (float)(ls - kLN2 * (double)sm.t2[row] / s);
+    double lp;
+    float ent;
+    if (a.rows_in) {  // finished on the tensor cores (ckrl_project_token_stats, row N2)
+      const ckrl_token_row tr = a.rows_in[kk];
+      lp = tr.logprob;
+      ent = tr.entropy;
+    } else {
+      const double s = (double)sm.s[row];
+      const double ls = log(s);
+      lp = ((double)sm.xt[row] - (double)sm.c[row] * kLN2) - ls;
+      ent = (float)(ls - kLN2 * (double)sm.t2[row] / s);
+    }
     const float old = MODE == MODE_STATS ? 0.0f : __ldg(a.old_lp + kk);
     sm.lp[row] = lp;
     sm.old[row] = old;
@@ -730,7 +738,7 @@ __global__ void __launch_bounds__(kLossThreads, 2) tile_kernel(LossArgs a) {
     const int nrec = (int)(rem < a.rec_per_tile ? rem : a.rec_per_tile);
     const int rows = nrec * P;
     const int64_t k0 = r0 * P;
-    for (int rg = warp * 4; rg < rows; rg += (kLossThreads / 32) * 4) {
+    for (int rg = warp * 4; rg < rows && !a.rows_in; rg += (kLossThreads / 32) * 4) {
       const int row = rg + sub;
       bool need = row < rows && row_needed(a, MODE, (k0 + row) / M);
       const int64_t kk = k0 + (row < rows ? row : 0);
@@ -1592,6 +1600,11 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>() > 608 ? tma_threads<RO
 
   if (tid == 0) {
     tl_mark(0);
+    // A loss launched right after this one on the stream as a programmatic dependent (the
+    // pipelined step's next batch) may start now: its CTAs take SMs as these retire, stream
+    // their logits and finish rows, and wait (griddepcontrol.wait) for this grid's completion
+    // before their first unit phase.
+    asm volatile("griddepcontrol.launch_dependents;");
     CKRL_PROBE(if (blockIdx.x < 1184) g_cta_times[0][blockIdx.x] = gtimer());
     for (int s = 0; s < nstage; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -2035,6 +2048,10 @@ static cudaError_t launch_mode(LossArgs& a, cudaStream_t s, int* g) {
     const char* env = getenv("CKRL_LOSS_KERNEL");
     g_force_direct = (env && env[0] == 'd') ? 1 : 0;
   }
+  if (a.rows_in) {  // per-position rows already finished: only the unit phase is left
+    if (a.dlogits) return cudaErrorInvalidValue;
+    return launch_direct<MODE, float, true>(a, s, g);
+  }
   const bool fast = a.V == 256;
   const int dbytes = a.logits_bf16 ? 2 : 4;
   int rpt, nstage;
@@ -2068,7 +2085,7 @@ cudaError_t launch_ppo_fused(LossArgs& a, cudaStream_t s, int* g) {
   int rpt, nstage;
   uint32_t tile_bytes;
   const uintptr_t align = reinterpret_cast<uintptr_t>(a.logits) & 15;
-  if (a.V != 256 || g_force_direct || align != 0 || !tma_plan(a, dbytes, rpt, nstage, tile_bytes))
+  if (a.rows_in || a.V != 256 || g_force_direct || align != 0 || !tma_plan(a, dbytes, rpt, nstage, tile_bytes))
     return cudaErrorNotSupported;
   a.rec_per_tile = rpt;
   return a.logits_bf16 ? launch_tma<MODE_PPO, __nv_bfloat16, true>(a, s, g, nstage, tile_bytes)

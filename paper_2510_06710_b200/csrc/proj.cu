@@ -1,0 +1,383 @@
+// Row N2 — the hidden -> action-bin projection on the 5th-generation tensor cores, fused with
+// the per-token statistics of the action-token kernel.
+//
+// The reference forms every position's logits as logits = W_pol . h + b_pol
+// (PolicyNet::logits_from_feature, policy/policy_net.cpp:265-274: `matvec` over the trunk
+// feature h of width H, then the bias) and reduces them with log_softmax
+// (policy_net.cpp:90-102) to the sampled token's log-prob and the entropy
+// (evaluate_chunk, policy_net.cpp:333-357). Here that is one persistent sm_100a kernel:
+//
+//   [rows x H] bf16 features  x  [256 x H] bf16 W_pol  ->  [128 x 256] f32 tiles in TMEM
+//
+//   warp 0 (one lane)  TMA producer: 2-D tensor copies (128-byte swizzle) of a 128-row
+//                      feature slab and the 256-row W_pol slab per 64-wide K step into a
+//                      4-stage shared-memory ring (mbarrier complete_tx).
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16, into
+//                      one of two 256-column TMEM accumulators (512 columns: the epilogue of
+//                      tile i overlaps the MMAs of tile i+1); tcgen05.commit frees the smem
+//                      stage and, after the last K step, hands the accumulator to the epilogue.
+//   warps 2-5          epilogue: TMEM lane = tile row, so each thread owns one position's
+//                      whole 256-bin row (tcgen05.ld 32x32b.x32, 8 column chunks). Bias, max,
+//                      sum of exp2, the entropy sum and the sampled token's logit in
+//                      registers; log-prob and entropy finished in fp64; the row record
+//                      {lp, H} (and optionally the logits) written straight to HBM.
+//
+// Nothing of the 256-bin row is ever written unless asked for: the loss consumes the
+// 16-byte row records (CKRL_DTYPE_TOKEN_ROWS), so the step's HBM traffic is the features
+// (2H bytes per position) plus 16 bytes, against 2H + 1 KB + 1 KB for projection -> logits
+// in HBM -> token kernel.
+#include <cuda.h>
+
+#include "kernels.h"
+
+namespace ckrl {
+namespace {
+
+constexpr int kPM = 128;  // positions per tile (UMMA M; TMEM lanes)
+constexpr int kPN = 256;  // bins (UMMA N; TMEM columns per accumulator)
+constexpr int kPK = 64;   // K per stage: one 128-byte swizzle atom of bf16
+constexpr int kPStages = 4;
+constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
+constexpr uint32_t kBBytes = kPN * kPK * 2;  // 32 KB
+constexpr int kProjThreads = 192;            // producer, MMA, 4 epilogue warps
+constexpr uint32_t kTmemCols = 512;          // two 256-column accumulators
+constexpr size_t kProjSmem = 1024 /*align slack*/ + kPStages * (size_t)(kABytes + kBBytes) + 1024 /*bias*/ +
+                             256 /*barriers*/;
+
+// Instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = 256, M = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kPN >> 3) << 17) |
+                            ((uint32_t)(kPM >> 4) << 24);
+
+struct ProjArgs {
+  int64_t rows;
+  int64_t n_tiles;
+  int n_kb;              // H / 64
+  const float* b_pol;    // [256]
+  const void* tokens;    // [rows] u8 / i32
+  int tok_i32;
+  ckrl_token_row* out;   // [rows] {lp, H} (nullable)
+  double* lp;            // [rows] (nullable)
+  float* ent;            // [rows] (nullable)
+  void* logits;          // [rows][256] (nullable)
+  int logits_bf16;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                       uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar)), "l"(policy)
+      : "memory");
+}
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart
+// (SBO), LBO unused (1), sm_100 descriptor version 1, layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 consecutive TMEM columns of this warp's 32 lanes (one f32 per lane per column).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float fast_ex2(float y) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y));
+  return r;
+}
+
+constexpr double kLn2 = 0.6931471805599453094;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__global__ void __launch_bounds__(kProjThreads, 1)
+    proj_stats_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                      ProjArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle atoms
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sa = base;                                   // kPStages x 16 KB
+  unsigned char* sb = base + kPStages * kABytes;              // kPStages x 32 KB
+  float* s_bias = reinterpret_cast<float*>(sb + kPStages * kBBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_bias + kPN);
+  uint64_t* empty = full + kPStages;
+  uint64_t* tfull = empty + kPStages;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kPN; i += kProjThreads) s_bias[i] = a.b_pol ? a.b_pol[i] : 0.0f;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&tfull[i], 1);
+      bar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      uint64_t pol_a, pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < a.n_kb; ++kb) {
+          bar_wait(&empty[stage], phase ^ 1);
+          bar_expect(&full[stage], kABytes + kBBytes);
+          tma_2d(su32(sa + stage * kABytes), &map_a, kb * kPK, (int)(tile * kPM), &full[stage], pol_a);
+          tma_2d(su32(sb + stage * kBBytes), &map_b, kb * kPK, 0, &full[stage], pol_b);
+          if (++stage == kPStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++i) {
+        const int acc = i & 1;
+        const uint32_t acc_phase = (uint32_t)(i >> 1) & 1u;
+        bar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * kPN);
+        for (int kb = 0; kb < a.n_kb; ++kb) {
+          bar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = su32(sa + stage * kABytes), b0 = su32(sb + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < kPK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
+            umma(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == kPStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---- epilogue: warps 2..5 own TMEM lanes 32*(warp%4) ..
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    int i = 0;
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const uint32_t acc_phase = (uint32_t)(i >> 1) & 1u;
+      const int64_t row = tile * kPM + row_in_tile;
+      const bool live = row < a.rows;
+      int tok = 0;
+      if (live)
+        tok = a.tok_i32 ? reinterpret_cast<const int32_t*>(a.tokens)[row]
+                        : (int)reinterpret_cast<const uint8_t*>(a.tokens)[row];
+      tok &= kPN - 1;
+      bar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kPN);
+      // pass 1: max and the sampled token's logit
+      float m = -INFINITY, xt = 0.0f;
+#pragma unroll 1
+      for (int c = 0; c < kPN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = v[j] + s_bias[c * 32 + j];
+          m = fmaxf(m, x);
+          xt = (c * 32 + j == tok) ? x : xt;
+        }
+      }
+      // pass 2: s = sum 2^y, t = sum 2^y * y, y = (x - m) log2 e
+      const float mb = m * kLog2e;
+      float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < kPN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float x0 = v[j] + s_bias[c * 32 + j], x1 = v[j + 1] + s_bias[c * 32 + j + 1];
+          const float y0 = fmaf(x0, kLog2e, -mb), y1 = fmaf(x1, kLog2e, -mb);
+          const float e0 = fast_ex2(y0), e1 = fast_ex2(y1);
+          s0 += e0;
+          s1 += e1;
+          t0 = fmaf(e0, y0, t0);
+          t1 = fmaf(e1, y1, t1);
+          if (a.logits && live) {
+            if (a.logits_bf16) {
+              __nv_bfloat162 p = __floats2bfloat162_rn(x0, x1);
+              reinterpret_cast<__nv_bfloat162*>(a.logits)[(row * kPN + c * 32 + j) >> 1] = p;
+            } else {
+              reinterpret_cast<float2*>(a.logits)[(row * kPN + c * 32 + j) >> 1] = make_float2(x0, x1);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      bar_arrive(&tempty[acc]);  // accumulator drained: the MMA warp may overwrite it
+      if (live) {
+        const float s = s0 + s1, t = t0 + t1;
+        // y = fma(x, log2e, -mb) with mb = fl(m log2e): every y carries the same shift
+        // r = m log2e - mb (exact by fma), so ln sum 2^((x-m) log2e) = ln s - r ln2; the
+        // entropy ln S - ln2 E[(x-m) log2e] is shift-free
+        const double r = (double)fmaf(m, kLog2e, -mb);
+        const double ls = log((double)s);
+        const double ey = (double)t / (double)s;  // E[y]
+        const double lp = ((double)xt - (double)m) - (ls - r * kLn2);
+        const double h = ls - kLn2 * ey;
+        if (a.out) {
+          ckrl_token_row r;
+          r.logprob = lp;
+          r.entropy = (float)h;
+          r.reserved = 0;
+          a.out[row] = r;
+        }
+        if (a.lp) a.lp[row] = lp;
+        if (a.ent) a.ent[row] = (float)h;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// [outer][H] bf16, row pitch H * 2 bytes, box {64, box_rows}, 128-byte swizzle, OOB rows zero.
+bool make_map(CUtensorMap* m, const void* ptr, int64_t outer, int H, int box_rows) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)H * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kPK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+size_t proj_smem_bytes() { return kProjSmem; }
+
+cudaError_t launch_proj_stats(int64_t rows, int H, const void* feature, const void* w_pol, const float* b_pol,
+                              const void* tokens, int tok_i32, ckrl_token_row* out, double* lp, float* ent,
+                              void* logits, int logits_bf16, int max_ctas, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, feature, rows, H, kPM) || !make_map(&mb, w_pol, kPN, H, kPN)) return cudaErrorInvalidValue;
+  ProjArgs a;
+  a.rows = rows;
+  a.n_tiles = (rows + kPM - 1) / kPM;
+  a.n_kb = H / kPK;
+  a.b_pol = b_pol;
+  a.tokens = tokens;
+  a.tok_i32 = tok_i32;
+  a.out = out;
+  a.lp = lp;
+  a.ent = ent;
+  a.logits = logits;
+  a.logits_bf16 = logits_bf16;
+  cudaError_t e = cudaFuncSetAttribute(proj_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kProjSmem);
+  if (e != cudaSuccess) return e;
+  int64_t grid = sm_count();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid > a.n_tiles) grid = a.n_tiles;
+  proj_stats_kernel<<<(unsigned)grid, kProjThreads, kProjSmem, s>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
+}  // namespace ckrl

@@ -113,6 +113,24 @@ struct EnvState {
   uint8_t* ep_complete;
 };
 
+// Where generation writes a chunk's action batch: the slab itself (colocated, record
+// e * T + t) or the generation side's staging rows (placed, row e, T = 1, t ignored).
+struct GenOut {
+  int32_t* tokens;
+  float* lp;
+  double* lp64;
+  float* vs;
+  double* vs64;
+  float* vv;
+  double* vv64;
+  float* logits;
+  int T;       // records per env in this view
+  int staged;  // 1: one record per env (the chunk index is not part of the row)
+};
+__host__ __device__ inline int64_t gen_rec(const GenOut& g, int e, int t) {
+  return (int64_t)e * g.T + (g.staged ? 0 : t);
+}
+
 struct PipeArgs {
   ckrl_env_config env;
   PolicyLayout pl;
@@ -128,6 +146,10 @@ struct PipeArgs {
   struct {
     int64_t win, trunk, wpol, v1, v2, c1, c2, c3;
   } pk;
+  int sampler;          // CKRL_SAMPLER_*
+  const double* gobs;   // generation's view of the observations [E][D]
+  uint64_t* gsamp;      // generation's per-env sampling streams [E]
+  GenOut gout;          // generation's action-batch destination
 };
 
 __device__ void observe(const PipeArgs& a, int e, double* o) {
@@ -450,6 +472,72 @@ __device__ void value_heads(const PipeArgs& a, const double* pk, const double* f
 
 constexpr int kGenThreads = 128;
 
+// CKRL_SAMPLER_PARALLEL: log_softmax's sum of exp(l_v - max) and the inverse-CDF walk of
+// sample_chunk (policy_net.cpp:90-102, 306-316) as block-wide fixed-order reductions: thread i
+// owns the contiguous bins [i*q, (i+1)*q) (q = ceil(V / 128)), sums them in bin order, then a
+// shuffle tree per warp and the 4 warp totals in warp order (the LSE); the CDF is the same
+// partition's inclusive scan (own bins serially, warp Kogge-Stone, warp offsets), and the
+// token is the smallest v with u < cdf[v] (V - 1 if none, as the reference). Every thread
+// returns the token; w.red[4] = lse. Deterministic and independent of scheduling.
+__device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int q = (V + kGenThreads - 1) / kGenThreads;
+  const int v0 = tid * q, v1 = min(V, v0 + q);
+  double part = 0.0;
+  for (int v = v0; v < v1; ++v) {
+    const double ex = exp(__dsub_rn(w.lg[v], mx));
+    part = __dadd_rn(part, ex);
+  }
+  double tot = part;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, o));
+  __syncthreads();  // w.red[] is free (the max has been read)
+  if (lane == 0) w.red[warp] = tot;
+  __syncthreads();
+  const double sum = __dadd_rn(__dadd_rn(w.red[0], w.red[1]), __dadd_rn(w.red[2], w.red[3]));
+  const double lse = __dadd_rn(mx, log(sum));
+  // probabilities and this thread's inclusive partial sums
+  double acc = 0.0;
+  for (int v = v0; v < v1; ++v) {
+    const double pv = exp(__dsub_rn(w.lg[v], lse));
+    w.ex[v] = pv;
+    acc = __dadd_rn(acc, pv);
+  }
+  // exclusive prefix of the thread totals: warp inclusive scan + preceding warps' totals
+  double inc = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc = __dadd_rn(inc, y);
+  }
+  __syncthreads();
+  if (lane == 31) w.red[warp] = inc;
+  __syncthreads();
+  // this thread's exclusive prefix inside its warp: the previous lane's inclusive value
+  double base = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) base = 0.0;
+  double woff = 0.0;
+  for (int q2 = 0; q2 < warp; ++q2) woff = __dadd_rn(woff, w.red[q2]);
+  double c = __dadd_rn(woff, base);
+  int hit = V;
+  for (int v = v0; v < v1; ++v) {
+    c = __dadd_rn(c, w.ex[v]);
+    if (u < c && hit == V) hit = v;
+  }
+  // smallest hit over the block
+  int m = hit;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int* sred = reinterpret_cast<int*>(w.red + 6);
+  __syncthreads();
+  if (lane == 0) sred[warp] = m;
+  __syncthreads();
+  m = min(min(sred[0], sred[1]), min(sred[2], sred[3]));
+  if (tid == 0) w.red[4] = lse;
+  __syncthreads();
+  return m < V ? m : V - 1;
+}
+
 // StageGen::generate (rollout.cpp:68-83) for one env per CTA: sample_chunk
 // (policy_net.cpp:286-331) token by token, then the scalar and vector values of the obs.
 __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first, int count, int t) {
@@ -461,9 +549,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
   const PolScratch w = carve(reinterpret_cast<double*>(smem), L, true);
   const double* p = a.params;
   const double* pk = a.packed;
-  const double* obs = a.st.obs + (int64_t)e * L.D;
-  const int64_t rec = (int64_t)e * a.T + t;
-  uint64_t rng = tid == 0 ? a.st.samp[e] : 0;
+  const double* obs = a.gobs + (int64_t)e * L.D;
+  const GenOut& go = a.gout;
+  const int64_t rec = gen_rec(go, e, t);
+  const bool par = a.sampler == CKRL_SAMPLER_PARALLEL;
+  uint64_t rng = (tid == 0 || par) ? a.gsamp[e] : 0;  // parallel: every thread draws the same u
   for (int pos = 0; pos < L.P; ++pos) {
     // trunk input (policy_net.cpp:197-212): W_in obs + (b_in + pos_bias) + sum_k emb[k][tok_k]
     for (int hh = tid; hh < L.H; hh += kGenThreads) {
@@ -487,12 +577,28 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
     if (lane == 0) w.red[warp] = mx;
     __syncthreads();
     mx = fmax(fmax(w.red[0], w.red[1]), fmax(w.red[2], w.red[3]));
-    // log_softmax (policy_net.cpp:90-102): exps in parallel, the sum in v order on thread 0
-    for (int v = tid; v < L.V; v += kGenThreads) w.ex[v] = exp(__dsub_rn(w.lg[v], mx));
-    if (a.out.logits) {
-      float* dst = a.out.logits + (rec * L.P + pos) * (int64_t)L.V;
+    if (go.logits) {
+      float* dst = go.logits + (rec * L.P + pos) * (int64_t)L.V;
       for (int v = tid; v < L.V; v += kGenThreads) dst[v] = (float)w.lg[v];
     }
+    if (par) {  // fixed-order block reductions / scan (identical for every k and placement)
+      const int tok = sample_parallel(w, L.V, mx, rng_double(rng), tid);
+      const double lse = w.red[4];
+      if (tid == 0) {
+        const double lp = __dsub_rn(w.lg[tok], lse);
+        const int64_t k = rec * L.P + pos;
+        go.tokens[k] = tok;
+        go.lp[k] = (float)lp;
+        go.lp64[k] = lp;
+        w.prefix[pos] = tok;
+      }
+      __syncthreads();
+      for (int hh = tid; hh < L.H; hh += kGenThreads)
+        w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
+      continue;
+    }
+    // log_softmax (policy_net.cpp:90-102): exps in parallel, the sum in v order on thread 0
+    for (int v = tid; v < L.V; v += kGenThreads) w.ex[v] = exp(__dsub_rn(w.lg[v], mx));
     __syncthreads();
     if (tid == 0) {
       double sum = 0.0;
@@ -540,9 +646,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
       }
       const double lp = __dsub_rn(w.lg[tok], lse);
       const int64_t k = rec * L.P + pos;
-      a.out.tokens[k] = tok;
-      a.out.old_logprob[k] = (float)lp;
-      a.out.old_logprob_f64[k] = lp;
+      go.tokens[k] = tok;
+      go.lp[k] = (float)lp;
+      go.lp64[k] = lp;
       w.prefix[pos] = tok;
     }
     __syncthreads();
@@ -551,17 +657,54 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
       w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
     // the next position's trunk input reads embc[pos][hh] from the same thread
   }
-  if (tid == 0) a.st.samp[e] = rng;
+  if (tid == 0) a.gsamp[e] = rng;
   __syncthreads();
   // StageGen's value calls re-run the trunk on the obs with an empty prefix: f0
   value_heads<true>(a, pk, w.f0, w, tid, kGenThreads, w.vs, w.vs + 1);
   if (tid == 0) {
-    a.out.value_scalar[rec] = (float)w.vs[0];
-    a.out.value_scalar_f64[rec] = w.vs[0];
+    go.vs[rec] = (float)w.vs[0];
+    go.vs64[rec] = w.vs[0];
   }
   for (int c = tid; c < L.C; c += kGenThreads) {
-    a.out.value_vector[rec * L.C + c] = (float)w.vs[1 + c];
-    a.out.value_vector_f64[rec * L.C + c] = w.vs[1 + c];
+    go.vv[rec * L.C + c] = (float)w.vs[1 + c];
+    go.vv64[rec * L.C + c] = w.vs[1 + c];
+  }
+}
+
+// Placed generation: the sampling streams live with the generation role (StageGen owns
+// them, rollout.cpp:61-66), seeded by global env id exactly as env_reset_kernel does.
+__global__ void gen_init_kernel(PipeArgs a, int first, int count) {
+  const int e = first + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < first + count) a.gsamp[e] = rng_make(mix_seed(a.sample_seed, 0xac7100full + (uint64_t)e));
+}
+
+// The env side's receive of a stage's action batch (the act channel's recv,
+// real_backend.cpp:82-84): staging row e -> slab record e * T + t, one CTA per env.
+__global__ void act_scatter_kernel(PipeArgs a, GenOut src, int first, int t) {
+  const int e = first + blockIdx.x;
+  const PolicyLayout& L = a.pl;
+  const int64_t rec = (int64_t)e * a.T + t, row = e;
+  for (int i = threadIdx.x; i < L.P; i += blockDim.x) {
+    a.out.tokens[rec * L.P + i] = src.tokens[row * L.P + i];
+    a.out.old_logprob[rec * L.P + i] = src.lp[row * L.P + i];
+    a.out.old_logprob_f64[rec * L.P + i] = src.lp64[row * L.P + i];
+  }
+  for (int c = threadIdx.x; c < L.C; c += blockDim.x) {
+    a.out.value_vector[rec * L.C + c] = src.vv[row * L.C + c];
+    a.out.value_vector_f64[rec * L.C + c] = src.vv64[row * L.C + c];
+  }
+  if (threadIdx.x == 0) {
+    a.out.value_scalar[rec] = src.vs[row];
+    a.out.value_scalar_f64[rec] = src.vs64[row];
+  }
+  if (a.out.logits && src.logits) {
+    const int64_t n = (int64_t)L.P * L.V;
+    const float4* s4 = reinterpret_cast<const float4*>(src.logits + row * n);
+    float4* d4 = reinterpret_cast<float4*>(a.out.logits + rec * n);
+    if ((n & 3) == 0)
+      for (int64_t i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = s4[i];
+    else
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a.out.logits[rec * n + i] = src.logits[row * n + i];
   }
 }
 
@@ -682,38 +825,136 @@ size_t pipeline_ws_layout(const ckrl_pipeline_spec& sp, EnvState* st, double** p
   return off;
 }
 
-size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp) { return pipeline_ws_layout(sp, nullptr, nullptr, nullptr); }
+size_t staging_bytes(const ckrl_pipeline_spec& sp);
+size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp) {
+  size_t n = pipeline_ws_layout(sp, nullptr, nullptr, nullptr);
+  if (sp.gen_device >= 0) n += staging_bytes(sp);  // the env side's receive buffers
+  return n;
+}
 int64_t policy_num_params(const ckrl_policy_desc& d) { return make_layout(d).total; }
 
-struct PipeStreams {
-  std::vector<cudaStream_t> stage;
-  std::vector<cudaEvent_t> done;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  size_t gen_smem_set = 0, boot_smem_set = 0;
-};
+// One action batch's staging rows ([E] rows: tokens, log-probs, values, optional logits),
+// contiguous so a stage's rows [first, first + per) of each field move with one copy.
+size_t staging_layout(const ckrl_pipeline_spec& sp, GenOut* g, char* base, bool logits) {
+  const int64_t E = sp.env.num_envs, P = (int64_t)sp.policy.chunk_len * sp.policy.tokens_per_action,
+                C = sp.policy.chunk_len, V = sp.policy.vocab;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = off;
+    off = align256(off + bytes);
+    return base ? base + at : nullptr;
+  };
+  GenOut o;
+  o.tokens = (int32_t*)take(4 * E * P);
+  o.lp = (float*)take(4 * E * P);
+  o.lp64 = (double*)take(8 * E * P);
+  o.vs = (float*)take(4 * E);
+  o.vs64 = (double*)take(8 * E);
+  o.vv = (float*)take(4 * E * C);
+  o.vv64 = (double*)take(8 * E * C);
+  o.logits = logits ? (float*)take(4 * E * P * V) : nullptr;
+  o.T = 1;
+  o.staged = 1;
+  if (g) *g = o;
+  return off;
+}
+size_t staging_bytes(const ckrl_pipeline_spec& sp) { return staging_layout(sp, nullptr, nullptr, true); }
 
-PipeStreams& pipe_streams(int k) {
-  static PipeStreams ps;
-  if (!ps.fork) {
-    cudaEventCreateWithFlags(&ps.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ps.join, cudaEventDisableTiming);
-  }
-  while ((int)ps.stage.size() < k) {
+// Generation side of a placed pipeline: the policy copy (+ its transposed weights), the
+// sampling streams, the observation batch it receives and the action batch it sends.
+struct GenWs {
+  double *params, *packed, *obs;
+  uint64_t* samp;
+  GenOut stage;
+};
+size_t gen_ws_layout(const ckrl_pipeline_spec& sp, GenWs* g, char* base) {
+  const PolicyLayout L = make_layout(sp.policy);
+  const int64_t E = sp.env.num_envs;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = off;
+    off = align256(off + bytes);
+    return base ? base + at : nullptr;
+  };
+  GenWs w;
+  w.params = (double*)take(8 * (size_t)L.total);
+  w.packed = (double*)take(8 * (size_t)packed_layout(L, nullptr).total);
+  w.obs = (double*)take(8 * (size_t)E * L.D);
+  w.samp = (uint64_t*)take(8 * (size_t)E);
+  char* st = (char*)take(staging_bytes(sp));
+  staging_layout(sp, &w.stage, st, true);
+  if (g) *g = w;
+  return off;
+}
+size_t pipeline_gen_ws_bytes(const ckrl_pipeline_spec& sp) { return gen_ws_layout(sp, nullptr, nullptr); }
+
+// Streams and events of one device's role (created on that device).
+struct RoleStreams {
+  std::vector<cudaStream_t> stage;
+  std::vector<cudaEvent_t> done;  // per stage: last work of the stage on this role
+  cudaEvent_t fork = nullptr;
+};
+RoleStreams& role_streams(int device, int k) {
+  static std::vector<RoleStreams> per_dev;
+  if ((int)per_dev.size() <= device) per_dev.resize(device + 1);
+  RoleStreams& r = per_dev[device];
+  if (!r.fork) cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+  while ((int)r.stage.size() < k) {
     cudaStream_t st;
     cudaEvent_t ev;
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    ps.stage.push_back(st);
-    ps.done.push_back(ev);
+    r.stage.push_back(st);
+    r.done.push_back(ev);
   }
-  return ps;
+  return r;
 }
 
-// RealBackend::run_rollout_epoch (real_backend.cpp:59-138) on one GPU: stage s owns envs
-// [s*E/k, (s+1)*E/k) (rollout.cpp:11-17) and its own stream, on which it runs
-// Reset -> (Gen(t) -> Sim(t)) x T; the k stage streams run concurrently, so stage s's env
-// step overlaps stage s'’s policy inference. Bootstrap values and the merged episode table
-// follow once every stage has finished.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static cudaError_t set_kernel_smem(size_t gen_smem, size_t boot_smem) {
+  static thread_local size_t gen_set[64] = {0}, boot_set[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t err;
+  if (gen_smem > gen_set[dev & 63]) {
+    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_smem)))
+      return err;
+    // the transposed weights are re-read every position: leave most of the SM's 256 KB to L1
+    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    gen_smem * 3 <= 64 * 1024 ? 25 : 100)))
+      return err;
+    gen_set[dev & 63] = gen_smem;
+  }
+  if (boot_smem > boot_set[dev & 63]) {
+    if ((err = cudaFuncSetAttribute(boot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)boot_smem)))
+      return err;
+    boot_set[dev & 63] = boot_smem;
+  }
+  return cudaSuccess;
+}
+
+// RealBackend::run_rollout_epoch (real_backend.cpp:59-138): stage s owns envs
+// [s*E/k, (s+1)*E/k) (rollout.cpp:11-17) and runs Reset -> (Gen(t) -> Sim(t)) x T.
+//   colocated: stage s on its own stream of the calling device; the k stage streams run
+//     concurrently, so stage s's env step overlaps stage s'’s policy inference.
+//   placed (gen_device >= 0): the generation role on gen_device with its own policy copy and
+//     sampling streams; per chunk the env stream sends the stage's obs rows (peer copy) and
+//     records obs_ev[s], the gen stream waits it, samples, sends the action rows back and
+//     records done(gen)[s], which the env stream waits before scattering them into the slab
+//     and stepping the envs. Bootstrap values and the merged episode table follow on
+//     `stream` once every stage has finished.
 cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckrl_pipeline_outputs& out,
                          char* ws, cudaStream_t stream) {
   static std::mutex mu;
@@ -728,8 +969,9 @@ cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckr
   a.sample_seed = sp.sample_seed;
   a.reset_ids = sp.reset_state_ids;
   a.out = out;
+  a.sampler = sp.sampler;
   double* packed = nullptr;
-  pipeline_ws_layout(sp, &a.st, &a.post_obs, ws, &packed);
+  const size_t env_ws = pipeline_ws_layout(sp, &a.st, &a.post_obs, ws, &packed);
   a.packed = packed;
   PackTable tab;
   std::memset(&tab, 0, sizeof(tab));
@@ -743,39 +985,125 @@ cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckr
   a.pk.c1 = pk.c1;
   a.pk.c2 = pk.c2;
   a.pk.c3 = pk.c3;
+  // colocated generation reads the env state's observations and writes the slab directly
+  a.gobs = a.st.obs;
+  a.gsamp = a.st.samp;
+  a.gout = GenOut{out.tokens, out.old_logprob, out.old_logprob_f64, out.value_scalar, out.value_scalar_f64,
+                  out.value_vector, out.value_vector_f64, out.logits, a.T, 0};
   const int E = sp.env.num_envs, k = sp.stages, per = E / k, T = sp.num_chunks;
   const size_t gen_smem = 8 * pol_scratch_doubles(a.pl, true);
   const size_t boot_smem = 8 * (size_t)kBootWarps * pol_scratch_doubles(a.pl, false);
   if (gen_smem > 227 * 1024 || boot_smem > 227 * 1024) return cudaErrorInvalidValue;
-  PipeStreams& ps = pipe_streams(k);
-  cudaError_t err;
-  if (gen_smem > ps.gen_smem_set) {
-    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_smem)))
-      return err;
-    // the transposed weights are re-read every position: leave most of the SM's 256 KB to L1
-    if ((err = cudaFuncSetAttribute(gen_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    gen_smem * 3 <= 64 * 1024 ? 25 : 100)))
-      return err;
-    ps.gen_smem_set = gen_smem;
-  }
-  if (boot_smem > ps.boot_smem_set) {
-    if ((err = cudaFuncSetAttribute(boot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)boot_smem)))
-      return err;
-    ps.boot_smem_set = boot_smem;
-  }
+  int env_dev = 0;
+  cudaError_t err = cudaGetDevice(&env_dev);
+  if (err) return err;
+  const bool placed = sp.gen_device >= 0;
+  const int gen_dev = placed ? sp.gen_device : env_dev;
+  if ((err = set_kernel_smem(gen_smem, boot_smem))) return err;
   cudaMemsetAsync(out.status, 0, sizeof(int32_t), stream);
   pack_kernel<<<(unsigned)std::min<int64_t>((tab.total + 255) / 256, 592), 256, 0, stream>>>(params, packed, tab);
-  cudaEventRecord(ps.fork, stream);
-  for (int s = 0; s < k; ++s) {
-    cudaStream_t st = ps.stage[s];
-    cudaStreamWaitEvent(st, ps.fork, 0);
-    env_reset_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per);
-    for (int t = 0; t < T; ++t) {
-      gen_kernel<<<per, kGenThreads, gen_smem, st>>>(a, s * per, per, t);
-      env_chunk_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per, t);
+  RoleStreams& es = role_streams(env_dev, k);
+  cudaEventRecord(es.fork, stream);
+
+  if (!placed) {
+    for (int s = 0; s < k; ++s) {
+      cudaStream_t st = es.stage[s];
+      cudaStreamWaitEvent(st, es.fork, 0);
+      env_reset_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per);
+      for (int t = 0; t < T; ++t) {
+        gen_kernel<<<per, kGenThreads, gen_smem, st>>>(a, s * per, per, t);
+        env_chunk_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per, t);
+      }
+      cudaEventRecord(es.done[s], st);
+      cudaStreamWaitEvent(stream, es.done[s], 0);
     }
-    cudaEventRecord(ps.done[s], st);
-    cudaStreamWaitEvent(stream, ps.done[s], 0);
+  } else {
+    // the env side's receive buffers follow its workspace; the gen side's live in gen_workspace
+    GenOut recv;
+    staging_layout(sp, &recv, ws + env_ws, true);
+    if (!out.logits) recv.logits = nullptr;
+    GenWs gw;
+    gen_ws_layout(sp, &gw, reinterpret_cast<char*>(sp.gen_workspace));
+    if (!out.logits) gw.stage.logits = nullptr;
+    PipeArgs ag = a;  // generation's view: its own policy copy, streams and staging
+    ag.params = gw.params;
+    ag.packed = gw.packed;
+    ag.gobs = gw.obs;
+    ag.gsamp = gw.samp;
+    ag.gout = gw.stage;
+    const int D = a.pl.D, P = a.pl.P, C = a.pl.C, V = a.pl.V;
+    if (gen_dev != env_dev) {  // NVLink peer access both ways (no-op when already enabled)
+      cudaDeviceEnablePeerAccess(gen_dev, 0);
+      DeviceGuard g(gen_dev);
+      cudaDeviceEnablePeerAccess(env_dev, 0);
+      cudaGetLastError();
+    }
+    RoleStreams* gs;
+    {
+      DeviceGuard g(gen_dev);
+      if ((err = set_kernel_smem(gen_smem, boot_smem))) return err;
+      gs = &role_streams(gen_dev, k);
+      // the policy snapshot moves to the generation role once per epoch
+      cudaStream_t g0 = gs->stage[0];
+      cudaStreamWaitEvent(g0, es.fork, 0);
+      cudaMemcpyPeerAsync(gw.params, gen_dev, params, env_dev, sizeof(double) * (size_t)a.pl.total, g0);
+      pack_kernel<<<(unsigned)std::min<int64_t>((tab.total + 255) / 256, 592), 256, 0, g0>>>(gw.params, gw.packed,
+                                                                                              tab);
+      cudaEventRecord(gs->fork, g0);
+    }
+    std::vector<cudaEvent_t>& obs_ev = es.done;  // env -> gen: "obs batch of stage s sent"
+    auto send_obs = [&](int s) {
+      cudaStream_t st = es.stage[s];
+      cudaMemcpyPeerAsync(gw.obs + (size_t)s * per * D, gen_dev, a.st.obs + (size_t)s * per * D, env_dev,
+                          sizeof(double) * (size_t)per * D, st);
+      cudaEventRecord(obs_ev[s], st);
+    };
+    auto send_act = [&](int s, cudaStream_t st) {  // gen -> env, the stage's rows of every field
+      const size_t r0 = (size_t)s * per;
+      auto cp = [&](void* dst, const void* src, size_t row_bytes) {
+        cudaMemcpyPeerAsync((char*)dst + r0 * row_bytes, env_dev, (const char*)src + r0 * row_bytes, gen_dev,
+                            row_bytes * per, st);
+      };
+      cp(recv.tokens, gw.stage.tokens, 4 * (size_t)P);
+      cp(recv.lp, gw.stage.lp, 4 * (size_t)P);
+      cp(recv.lp64, gw.stage.lp64, 8 * (size_t)P);
+      cp(recv.vs, gw.stage.vs, 4);
+      cp(recv.vs64, gw.stage.vs64, 8);
+      cp(recv.vv, gw.stage.vv, 4 * (size_t)C);
+      cp(recv.vv64, gw.stage.vv64, 8 * (size_t)C);
+      if (recv.logits) cp(recv.logits, gw.stage.logits, 4 * (size_t)P * V);
+    };
+    for (int s = 0; s < k; ++s) {
+      cudaStream_t st = es.stage[s];
+      cudaStreamWaitEvent(st, es.fork, 0);
+      env_reset_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per);
+      send_obs(s);
+      DeviceGuard g(gen_dev);
+      cudaStream_t gst = gs->stage[s];
+      cudaStreamWaitEvent(gst, gs->fork, 0);
+      gen_init_kernel<<<(per + 127) / 128, 128, 0, gst>>>(ag, s * per, per);
+    }
+    for (int t = 0; t < T; ++t) {
+      for (int s = 0; s < k; ++s) {
+        {
+          DeviceGuard g(gen_dev);
+          cudaStream_t gst = gs->stage[s];
+          cudaStreamWaitEvent(gst, obs_ev[s], 0);
+          gen_kernel<<<per, kGenThreads, gen_smem, gst>>>(ag, s * per, per, t);
+          send_act(s, gst);
+          cudaEventRecord(gs->done[s], gst);
+        }
+        cudaStream_t st = es.stage[s];
+        cudaStreamWaitEvent(st, gs->done[s], 0);
+        act_scatter_kernel<<<per, 128, 0, st>>>(a, recv, s * per, t);
+        env_chunk_kernel<<<(per + 127) / 128, 128, 0, st>>>(a, s * per, per, t);
+        if (t + 1 < T) send_obs(s);
+      }
+    }
+    for (int s = 0; s < k; ++s) {
+      cudaEventRecord(es.done[s], es.stage[s]);
+      cudaStreamWaitEvent(stream, es.done[s], 0);
+    }
   }
   const int64_t nslots = (int64_t)E * T * sp.env.chunk_len;
   boot_kernel<<<(unsigned)((nslots + kBootWarps - 1) / kBootWarps), 32 * kBootWarps, boot_smem, stream>>>(a, nslots);

@@ -95,24 +95,57 @@ class RolloutEpoch:
                              bootstrap=boot, vocab=self.vocab)
 
 
+SAMPLER_REFERENCE, SAMPLER_PARALLEL = _lib.SAMPLER_REFERENCE, _lib.SAMPLER_PARALLEL
+COLOCATED, DISAGGREGATED, HYBRID = (_lib.PLACEMENT_COLOCATED, _lib.PLACEMENT_DISAGGREGATED,
+                                    _lib.PLACEMENT_HYBRID)
+
+
+def derive_mode(num_slots: int, env_slots, rollout_slots, actor_slots, pipeline_stage_num: int = 1) -> int:
+    """placement::derive_mode after validate_plan (placement/plan.cpp:49-68) on inclusive slot
+    ranges ("0-3" strings or (begin, end) pairs): COLOCATED / DISAGGREGATED / HYBRID; raises
+    InvalidPlan like the reference."""
+    def rng(r):
+        if isinstance(r, str):
+            b, _, e = r.partition("-")
+            return int(b), int(e or b)
+        return int(r[0]), int(r[1])
+    (eb, ee), (rb, re_), (ab, ae) = rng(env_slots), rng(rollout_slots), rng(actor_slots)
+    st = C.c_int32(0)
+    m = _lib.lib().ckrl_placement_mode(num_slots, eb, ee, rb, re_, ab, ae, pipeline_stage_num, C.byref(st))
+    _lib.check(st.value)
+    return int(m)
+
+
 class RolloutPipeline:
-    """RealBackend::run_rollout_epoch on one GPU with `stages` pipeline partitions."""
+    """RealBackend::run_rollout_epoch with `stages` pipeline partitions. gen_device=None is
+    the colocated placement (env and generation kernels on `device`); an int places the
+    generation role on that device (hybrid / disaggregated: obs and action batches cross
+    between the devices every chunk; it may equal `device`). `sampler` picks the reference-
+    order serial sampler (bit-exact with sample_chunk) or the warp-parallel one."""
 
     def __init__(self, env: EnvConfig, policy: PolicyDescriptor, num_chunks: int,
                  stages: int = 1, sample_seed: int = 0,
                  reset_state_ids: Optional[torch.Tensor] = None, device="cuda",
-                 keep_logits: bool = False):
+                 keep_logits: bool = False, sampler: int = SAMPLER_REFERENCE,
+                 gen_device: Optional[int] = None):
         self.env, self.policy, self.num_chunks, self.stages = env, policy, num_chunks, stages
         self.sample_seed = sample_seed
         self.device = torch.device(device)
         self.reset_ids = (None if reset_state_ids is None else
                           torch.as_tensor(reset_state_ids, dtype=torch.int32).to(self.device))
         self.spec = _lib.PipelineSpec(env.c(), policy.c(), num_chunks, stages, sample_seed,
-                                      _ptr(self.reset_ids))
+                                      _ptr(self.reset_ids), int(sampler),
+                                      -1 if gen_device is None else int(gen_device), None, 0)
         self._lib = _lib.lib()
         nbytes = int(self._lib.ckrl_pipeline_workspace_bytes(C.byref(self.spec)))
         if nbytes == 0:  # invalid spec: re-run validation to raise the reference's exception
             _lib.check(self._lib.ckrl_pipeline_run(C.byref(self.spec), None, None, None, 0, None))
+        self.gen_ws = None
+        if gen_device is not None:
+            gb = int(self._lib.ckrl_pipeline_gen_workspace_bytes(C.byref(self.spec)))
+            self.gen_ws = torch.empty(gb, dtype=torch.uint8, device=torch.device("cuda", int(gen_device)))
+            self.spec.gen_workspace = _ptr(self.gen_ws)
+            self.spec.gen_workspace_bytes = gb
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.keep_logits = keep_logits
         self.out = self._alloc()

@@ -40,6 +40,43 @@ def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, valid=None, stre
             "action_entropy": aent, "chunk_entropy": cent}
 
 
+def project_token_stats(feature: torch.Tensor, w_pol: torch.Tensor, b_pol, tokens: torch.Tensor,
+                        rows_out=None, want_logits=None, stream=None):
+    """Row N2: the policy head PolicyNet::logits_from_feature (policy/policy_net.cpp:265-274,
+    logits = W_pol h + b_pol) on the tensor cores, fused with evaluate_chunk's per-position
+    log-prob / entropy (:333-357). feature [..., H] bf16 (H a multiple of 64), w_pol [256, H]
+    bf16, b_pol [256] f32 or None, tokens [...]. Returns {"token_rows": [..., 2] f64 (the
+    16-byte ckrl_token_row per position: PolicyOutputs(token_rows=...) feeds the losses),
+    "token_logprob": [...] f64, "token_entropy": [...] f32, "logits": [..., 256] (only with
+    want_logits = torch.float32 / torch.bfloat16)}."""
+    *lead, H = feature.shape
+    rows = 1
+    for d in lead:
+        rows *= d
+    dev = feature.device
+    feature = feature.contiguous()
+    w_pol = w_pol.contiguous()
+    if feature.dtype != torch.bfloat16 or w_pol.dtype != torch.bfloat16:
+        raise TypeError("feature and w_pol must be bfloat16")
+    V = w_pol.shape[0]
+    b = None if b_pol is None else b_pol.to(device=dev, dtype=torch.float32).contiguous()
+    if rows_out is None:
+        rows_out = torch.empty((*lead, 2), dtype=torch.float64, device=dev)
+    lp = torch.empty(tuple(lead), dtype=torch.float64, device=dev)
+    ent = torch.empty(tuple(lead), dtype=torch.float32, device=dev)
+    logits = None
+    ld = _lib.DTYPE_F32
+    if want_logits is not None:
+        logits = torch.empty((*lead, V), dtype=want_logits, device=dev)
+        ld = _lib.DTYPE_BF16 if want_logits == torch.bfloat16 else _lib.DTYPE_F32
+    td = _lib.DTYPE_U8 if tokens.dtype == torch.uint8 else _lib.DTYPE_I32
+    tokens = tokens.contiguous() if tokens.dtype in (torch.uint8, torch.int32) else tokens.to(torch.int32).contiguous()
+    head = _lib.PolicyHead(H, V, _ptr(feature), _ptr(w_pol), _ptr(b))
+    _lib.check(_lib.lib().ckrl_project_token_stats(rows, C.byref(head), td, _ptr(tokens), _ptr(rows_out),
+                                                   _ptr(lp), _ptr(ent), ld, _ptr(logits), stream_ptr(stream)))
+    return {"token_rows": rows_out, "token_logprob": lp, "token_entropy": ent, "logits": logits}
+
+
 def logits_grad(logits: torch.Tensor, tokens: torch.Tensor, coeff_logprob: torch.Tensor,
                 coeff_entropy=None, out=None, out_dtype=None, status=None, stream=None,
                 check: bool = True) -> torch.Tensor:

@@ -89,3 +89,22 @@ def test_compute_entry_points_fail_loudly_without_device():
                               None, None, None)
     assert st == 14  # CKRL_ERR_CUDA: no CPU fallback
     assert b"no CPU fallback" in lib.ckrl_last_error()
+
+
+def test_placement_mode_known_answers():
+    """placement::derive_mode / validate_plan (placement/plan.cpp:49-68), the reference's own
+    cases (tests/test_placement.cpp:71-74) plus validation errors."""
+    from paper_2510_06710_b200 import errors
+    from paper_2510_06710_b200.pipeline import COLOCATED, DISAGGREGATED, HYBRID, derive_mode
+    assert derive_mode(8, "0-7", "0-7", "0-7") == COLOCATED
+    assert derive_mode(8, "0-1", "2-3", "4-7") == DISAGGREGATED
+    assert derive_mode(8, "0-3", "4-7", "0-7") == HYBRID
+    assert derive_mode(1, "0", "0", "0") == COLOCATED
+    with pytest.raises(errors.InvalidPlan):
+        derive_mode(8, "0-8", "0-7", "0-7")
+    with pytest.raises(errors.InvalidPlan):
+        derive_mode(8, "3-2", "0-7", "0-7")
+    with pytest.raises(errors.InvalidPlan):
+        derive_mode(0, "0", "0", "0")
+    with pytest.raises(errors.InvalidPlan):
+        derive_mode(8, "0-7", "0-7", "0-7", pipeline_stage_num=0)

@@ -27,8 +27,8 @@ from paper_2510_06710_b200.core import (EpisodeTable, FilterBounds, GaeParams,  
                                         GranularitySpec, GrpoAssemblyOptions, GrpoParams,
                                         Level, LossOutputs, PolicyOutputs, PpoAssemblyOptions,
                                         PpoParams, read_diagnostics)
-from paper_2510_06710_b200.pipeline import (EnvConfig, PolicyDescriptor,  # noqa: E402
-                                            RolloutPipeline)
+from paper_2510_06710_b200.pipeline import (SAMPLER_PARALLEL, SAMPLER_REFERENCE,  # noqa: E402
+                                            EnvConfig, PolicyDescriptor, RolloutPipeline)
 
 bindings = pytest.importorskip("oracle.bindings")
 if not bindings.ref_available():
@@ -86,12 +86,13 @@ def ref_cache():
     return get
 
 
-def run_pipeline(name, stages, p, ids):
+def run_pipeline(name, stages, p, ids, sampler=SAMPLER_REFERENCE, gen_device=None, keep_logits=False):
     cfg, env, pol = specs_of(SCENARIOS[name])
     assert pol.num_params() == p.size
     pipe = RolloutPipeline(env, pol, cfg["num_chunks"], stages=stages,
                            sample_seed=cfg["sample_seed"],
-                           reset_state_ids=None if ids is None else torch.tensor(ids))
+                           reset_state_ids=None if ids is None else torch.tensor(ids),
+                           sampler=sampler, gen_device=gen_device, keep_logits=keep_logits)
     ep = pipe.run(torch.tensor(p, dtype=torch.float64, device="cuda"))
     torch.cuda.synchronize()
     host = {k: v.cpu().numpy() for k, v in ep.t.items() if v is not None}
@@ -160,6 +161,45 @@ def test_pipeline_scheduling_invariance(name, ref_cache):
         _, g = run_pipeline(name, k, p, ids)
         for key in base:
             np.testing.assert_array_equal(g[key], base[key], err_msg=f"k={k} {key}")
+
+
+@pytest.mark.parametrize("name", sorted(SCENARIOS))
+def test_pipeline_placement_invariance(name, ref_cache):
+    """a13 placements: the generation role placed on its own device (here the same B200, so
+    the obs / action hand-offs run as device copies through the generation side's staging)
+    gives the colocated slab bit-for-bit for every k, for both samplers, and with the
+    reference sampler it is the reference's own rollout (tests/acceptance.cpp:245-311,
+    real_backend.cpp:59-138)."""
+    _, d, p, ids = ref_cache(name)
+    E = specs_of(SCENARIOS[name])[0]["num_envs"]
+    for sampler in (SAMPLER_REFERENCE, SAMPLER_PARALLEL):
+        _, base = run_pipeline(name, 1, p, ids, sampler=sampler, keep_logits=True)
+        for k in (1, 2, 4):
+            if E % k:
+                continue
+            _, g = run_pipeline(name, k, p, ids, sampler=sampler, gen_device=0, keep_logits=True)
+            for key in base:
+                np.testing.assert_array_equal(g[key], base[key], err_msg=f"placed k={k} sampler={sampler} {key}")
+        if sampler == SAMPLER_REFERENCE:
+            np.testing.assert_array_equal(base["tokens"], d["tokens"])
+
+
+@pytest.mark.parametrize("name", ["v256_m7", "toyreach_shaped_long", "deep_trunk_l0"])
+def test_parallel_sampler_vs_reference(name, ref_cache):
+    """The warp-parallel sampler reorders only the log-sum-exp and CDF sums: its tokens are
+    the reference's (a differing draw needs u within an ulp of a CDF boundary) and its old
+    log-probs match the reference's to 1e-12; invariance across k holds exactly."""
+    _, d, p, ids = ref_cache(name)
+    _, g = run_pipeline(name, 1, p, ids, sampler=SAMPLER_PARALLEL)
+    np.testing.assert_array_equal(g["tokens"], d["tokens"], err_msg="tokens")
+    np.testing.assert_array_equal(g["flags"], d["flags"], err_msg="flags")
+    np.testing.assert_allclose(g["old_logprob_f64"], d["old_logprob"], rtol=1e-12, atol=1e-12)
+    E = specs_of(SCENARIOS[name])[0]["num_envs"]
+    for k in (2, 4):
+        if E % k == 0:
+            _, h = run_pipeline(name, k, p, ids, sampler=SAMPLER_PARALLEL)
+            for key in g:
+                np.testing.assert_array_equal(h[key], g[key], err_msg=f"k={k} {key}")
 
 
 def test_pipeline_config_errors():
