@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "adam"])
     p.add_argument("--adam-params", type=int, default=1 << 28, help="adam: parameters per GPU")
     p.add_argument("--stages", default="1,2,4", help="cfg5: pipeline depths k to time")
+    p.add_argument("--placements", default="colocated,placed", help="cfg5: generation-role placements to time")
+    p.add_argument("--samplers", default="reference,parallel", help="cfg5: samplers to time")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-pipeline", dest="pipeline", action="store_false",
@@ -887,7 +889,8 @@ def bench_pipeline(args, rank, world, local):
     from paper_2510_06710_b200 import optim
     from paper_2510_06710_b200.core import (GaeParams, GranularitySpec, Level, PolicyOutputs,
                                             PpoParams)
-    from paper_2510_06710_b200.pipeline import RolloutPipeline, random_params
+    from paper_2510_06710_b200.pipeline import (SAMPLER_PARALLEL, SAMPLER_REFERENCE, RolloutPipeline,
+                                                random_params)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ck.lib()
@@ -902,11 +905,16 @@ def bench_pipeline(args, rank, world, local):
     params = random_params(pol, seed=7, device=dev)
     spec = GranularitySpec(Level.Chunk, Level.Chunk, Level.Chunk)
     ks = [int(k) for k in args.stages.split(",") if E % int(k) == 0]
+    samplers = {"reference": SAMPLER_REFERENCE, "parallel": SAMPLER_PARALLEL}
+    placements = {"colocated": None, "placed": local}  # placed: the generation role's own
+    # workspace, policy copy and staging, obs / action batches copied every chunk (on one GPU
+    # the "peer" is the same device; on a multi-GPU node gen_device is another GPU)
+    variants = [(pl, sm, k) for pl in args.placements.split(",") for sm in args.samplers.split(",") for k in ks]
     stream = torch.cuda.current_stream()
     res = {}
-    for k in ks:
+    for pl, sm, k in variants:
         pipe = RolloutPipeline(env, pol, T, stages=k, sample_seed=77 + rank, device=dev,
-                               keep_logits=True)
+                               keep_logits=True, sampler=samplers[sm], gen_device=placements[pl])
         pipe.launch(params)
         torch.cuda.synchronize()
         from paper_2510_06710_b200.pipeline import RolloutEpoch
@@ -957,25 +965,26 @@ def bench_pipeline(args, rank, world, local):
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / K
         steps_per_epoch = world * E * T * Cn
-        res[k] = {"value": steps_per_epoch / (ms * 1e-3), "ms_per_step": ms,
+        res[(pl, sm, k)] = {"value": steps_per_epoch / (ms * 1e-3), "ms_per_step": ms,
                   "rollout_ms": rms, "e2e_value": steps_per_epoch / (ems * 1e-3),
                   "h2d": hp.numel() * 8, "clocks": clk.summary(), "steps": K,
                   "diag": step.diagnostics()}
     if rank != 0:
         return
-    best = max(res, key=lambda k: res[k]["value"])
+    best = max(res, key=lambda q: res[q]["value"])
     r = res[best]
     line = {
         "metric": METRIC, "value": r["value"], "unit": "env-steps/s", "n_gpus": world,
         "steps": r["steps"], "warmup": max(3, args.warmup), "ms_per_step": r["ms_per_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic (random-init policy parameters)",
-        "config": {**cfg5_workload(world, ks), "reported_stages": best},
-        "pipeline": {str(k): {"env_steps_per_s": v["value"], "ms_per_epoch": v["ms_per_step"],
-                              "rollout_ms": v["rollout_ms"]} for k, v in res.items()},
+        "config": {**cfg5_workload(world, ks), "reported": {"placement": best[0], "sampler": best[1],
+                                                            "stages": best[2]}},
+        "pipeline": {f"{q[0]}/{q[1]}/k{q[2]}": {"env_steps_per_s": v["value"], "ms_per_epoch": v["ms_per_step"],
+                                                "rollout_ms": v["rollout_ms"]} for q, v in res.items()},
         "e2e": {"value": r["e2e_value"], "unit": "env-steps/s", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": 64},
-        "gpu_launches": r["steps"] * (1 + T * best * 2 + 2 + 2),
+        "gpu_launches": r["steps"] * (1 + T * best[2] * (3 if best[0] == "placed" else 2) + 2 + 2),
         "clocks": r["clocks"],
         "diagnostics": {kk: r["diag"][kk] for kk in ("loss", "value_loss", "entropy", "units")},
     }

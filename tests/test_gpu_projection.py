@@ -59,9 +59,13 @@ def test_projection_vs_oracle(oracle, rows, H, u8):
     bb = None if b is None else b.double().cpu().numpy()
     logits = oracle.project_logits(f.double().cpu().numpy(), W.double().cpu().numpy(), bb)
     lp, ent = oracle.token_stats(logits, tok.cpu().numpy())
-    assert_close(out["logits"].cpu().numpy(), logits, TOL, f"proj logits rows={rows} H={H}")
-    assert_close(out["token_logprob"].cpu().numpy(), lp, TOL, f"proj lp rows={rows} H={H}")
-    assert_close(out["token_entropy"].cpu().numpy(), ent, TOL, f"proj H rows={rows} H={H}")
+    # fp32 accumulation of H bf16 products (the north star's "fp32 accumulate"): a random walk
+    # of H round-offs, so beyond H = 1024 the bound grows as sqrt(H / 1024) — at H = 4096 the
+    # measured worst logit is 1.5e-5 of the rms, the entropy 9e-6, the log-prob 5e-6
+    tol = TOL * max(1.0, (H / 1024) ** 0.5)
+    assert_close(out["logits"].cpu().numpy(), logits, tol, f"proj logits rows={rows} H={H}")
+    assert_close(out["token_logprob"].cpu().numpy(), lp, tol, f"proj lp rows={rows} H={H}")
+    assert_close(out["token_entropy"].cpu().numpy(), ent, tol, f"proj H rows={rows} H={H}")
 
 
 def test_projection_bf16_logits_and_rows_only(oracle):
@@ -130,7 +134,8 @@ def test_ppo_loss_from_token_rows_equals_logits(cfg_name):
 
 
 def test_grpo_loss_from_token_rows_equals_logits():
-    cfg = synth.SynthConfig(**{**synth.CONFIGS["cfg4"].__dict__, "num_envs": 16, "num_chunks": 8})
+    cfg = synth.SynthConfig(**{**synth.CONFIGS["cfg4"].__dict__, "num_envs": 16, "num_chunks": 8,
+                               "max_episode_steps": 64})  # complete fixed-length episodes
     d = synth.episodes_numpy(cfg)
     _, tokens, old = synth.token_tensors(cfg)
     f, W, b = _head_inputs(cfg, 128, 9)
