@@ -537,17 +537,30 @@ def main():
     # pipelined steps (events around every loss launch on its stream while the next batch's
     # assembly runs beside it; the device is held in a sleep while the host enqueues them all,
     # so no launch waits on the host); otherwise each launch alone after its assembly
-    live_kms = None
+    live_kms, live_how = None, None
     if pipe is not None:
         # the loss stream's time per launch over a chain of back-to-back launches (events before
         # the first and after the last, none in between: consecutive losses overlap through
         # programmatic dependent launch, so a launch's own start-to-end is not its cost)
         n_live = min(K, 50)
         span = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        torch.cuda._sleep(40_000_000)
-        pipe.issue(n_live, pipe_args, span_events=span)
-        torch.cuda.synchronize()
-        live_kms = span[0].elapsed_time(span[1]) / n_live
+        try:  # inside a graph, like the timed region (event-record nodes around the loss chain)
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2):
+                pipe.issue(n_live, pipe_args, span_events=span)
+            g2.replay()
+            torch.cuda.synchronize()
+            g2.replay()
+            torch.cuda.synchronize()
+            live_kms = span[0].elapsed_time(span[1]) / n_live
+            live_how = "graph"
+        except Exception:  # eager launches, the device held asleep while the host enqueues
+            torch.cuda.synchronize()
+            torch.cuda._sleep(40_000_000)
+            pipe.issue(n_live, pipe_args, span_events=span)
+            torch.cuda.synchronize()
+            live_kms = span[0].elapsed_time(span[1]) / n_live
+            live_how = "eager"
     ws = step.ws
     kms = []
     for i in range(min(K, 50) + 3):  # 3 untimed launches first (first-call attribute setup)
@@ -647,9 +660,9 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),
                      "kernel_ms": kernel_ms,
-                     "kernel_timing": ("loss-stream time per launch over a chain of pipelined steps (events "
-                                       "before the first and after the last launch; consecutive launches "
-                                       "overlap by programmatic dependent launch)"
+                     "kernel_timing": (f"loss-stream time per launch over a chain of {min(K, 50)} pipelined "
+                                       f"steps ({live_how}; events before the first and after the last launch; "
+                                       "consecutive launches overlap by programmatic dependent launch)"
                                        if live_kms is not None else "median loss launch alone after its assembly"),
                      "kernel_ms_alone": alone_ms,
                      "frac_alone": kbytes / (alone_ms * 1e-3) / 1e9 / peak,
@@ -697,16 +710,18 @@ def bench_head(args, rank, world, local):
     bias = 0.1 * torch.randn(256, device=dev, generator=g)
     shape = (cfg.num_envs, cfg.num_chunks, cfg.chunk_len, cfg.tokens_per_action)
 
-    class HeadStep:  # projection + loss in the loss half, so the assembly overlaps both
+    class HeadStep:  # assembly + projection on the side stream, the loss on the main one: batch
+        # i+1's projection overlaps batch i's loss (the loss waits for both through the pipeline's event)
         def __init__(self, inner, feat, tokens, rows):
             self.inner, self.feat, self.tokens, self.rows = inner, feat, tokens, rows
             self.comm = None
 
         def assemble(self, *aa, stream=None):
             self.inner.assemble(*aa, stream=stream)
+            policy.project_token_stats(self.feat, W, bias, self.tokens, rows_out=self.rows, stream=stream,
+                                       rows_only=True)
 
         def loss(self, ro, pol, stream=None):
-            policy.project_token_stats(self.feat, W, bias, self.tokens, rows_out=self.rows, stream=stream)
             self.inner.loss(ro, pol, stream=stream)
 
     reps, steps = [], []
@@ -756,7 +771,7 @@ def bench_head(args, rank, world, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda._sleep(200_000)
         e0.record(stream)
-        policy.project_token_stats(st.feat, W, bias, st.tokens, rows_out=st.rows)
+        policy.project_token_stats(st.feat, W, bias, st.tokens, rows_out=st.rows, rows_only=True)
         e1.record(stream)
         pev.append((e0, e1))
     torch.cuda.synchronize()
@@ -786,7 +801,7 @@ def bench_head(args, rank, world, local):
                    "step_includes": "policy-head projection (tcgen05) + assemble + loss from token rows"},
         "timing": {"l2": f"features rotate over {R} replicas ({R * feat_bytes / 2**20:.0f} MiB > 126 MB L2)",
                    "cuda_graph": f"one graph of all {K} steps", "untimed_replay_before_timing": True,
-                   "pipelined": "batch i+1's assembly on a side stream overlaps batch i's projection + loss"},
+                   "pipelined": "batch i+1's assembly + projection on a side stream overlap batch i's loss"},
         "roofline": {"bound": bound, "achieved": tf if bound == "tensor" else gbs,
                      "peak": tpeak if bound == "tensor" else hpeak,
                      "unit": "TFLOP/s" if bound == "tensor" else "GB/s",

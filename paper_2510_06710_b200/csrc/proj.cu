@@ -39,10 +39,10 @@ constexpr int kPK = 64;   // K per stage: one 128-byte swizzle atom of bf16
 constexpr int kPStages = 4;
 constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kPN * kPK * 2;  // 32 KB
-constexpr int kProjThreads = 192;            // producer, MMA, 4 epilogue warps
+constexpr int kProjThreads = 320;            // producer, MMA, 8 epilogue warps
 constexpr uint32_t kTmemCols = 512;          // two 256-column accumulators
 constexpr size_t kProjSmem = 1024 /*align slack*/ + kPStages * (size_t)(kABytes + kBBytes) + 1024 /*bias*/ +
-                             256 /*barriers*/;
+                             256 /*barriers*/ + 5 * 128 * 4 /*half exchange*/;
 
 // Instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = 256, M = 128.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kPN >> 3) << 17) |
@@ -107,20 +107,33 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-// 32 consecutive TMEM columns of this warp's 32 lanes (one f32 per lane per column).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+// 32 consecutive TMEM columns of this warp's 32 lanes (one f32 per lane per column), issued
+// asynchronously: the registers are valid after tmem_wait() (tcgen05.wait::ld waits for every
+// load this thread has issued).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]),
+        "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]),
+        "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// tcgen05.wait::ld with the just-loaded registers as in/out operands, so no use of them can be
+// scheduled above the wait
+__device__ __forceinline__ void tmem_wait(float (&v)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+        "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]),
+        "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]), "+f"(v[22]), "+f"(v[23]),
+        "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]), "+f"(v[29]), "+f"(v[30]), "+f"(v[31])
+      :
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ float fast_ex2(float y) {
@@ -146,6 +159,8 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   uint64_t* tfull = empty + kPStages;  // [2]
   uint64_t* tempty = tfull + 2;        // [2]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  float (*s_m)[kPM] = reinterpret_cast<float (*)[kPM]>(s_bias + kPN + 64);   // [2][128] half maxima
+  float (*s_st)[kPM] = reinterpret_cast<float (*)[kPM]>(s_bias + kPN + 64 + 2 * kPM);  // [3][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kPN; i += kProjThreads) s_bias[i] = a.b_pol ? a.b_pol[i] : 0.0f;
@@ -156,7 +171,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(&tfull[i], 1);
-      bar_init(&tempty[i], 128);
+      bar_init(&tempty[i], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -219,9 +234,14 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else {  // ---- epilogue: warps 2..5 own TMEM lanes 32*(warp%4) ..
-    const int q = warp & 3;
+  } else {
+    // ---- epilogue: 8 warps. Warp w (2..9) reads TMEM lane quarter q = w % 4 (the hardware
+    // rule: a warp reaches lanes 32*(w%4) .. +31) and column half h = (w-2)/4, so every tile
+    // row is split between two threads, 128 bins each; the halves trade their max and their
+    // sums through shared memory under a 64-thread named barrier per quarter.
+    const int q = warp & 3, half = (warp - 2) >> 2;
     const int row_in_tile = q * 32 + lane;
+    const uint32_t bar_id = 1 + q;
     int i = 0;
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++i) {
       const int acc = i & 1;
@@ -235,30 +255,40 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       tok &= kPN - 1;
       bar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kPN);
-      // pass 1: max and the sampled token's logit
+      const int c0 = half * (kPN / 2);
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kPN + c0);
+      const float* bias = s_bias + c0;
+      // pass 1: this half's max and (if it holds it) the sampled token's logit; the next
+      // 32-column load is in flight while the current one is reduced
+      float v[2][32];
       float m = -INFINITY, xt = 0.0f;
-#pragma unroll 1
-      for (int c = 0; c < kPN / 32; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
+      tmem_ld32_issue(taddr, v[0]);
+      tmem_wait(v[0]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < 3) tmem_ld32_issue(taddr + (c + 1) * 32, v[(c + 1) & 1]);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float x = v[j] + s_bias[c * 32 + j];
+          const float x = v[c & 1][j] + bias[c * 32 + j];
           m = fmaxf(m, x);
-          xt = (c * 32 + j == tok) ? x : xt;
+          xt = (c0 + c * 32 + j == tok) ? x : xt;
         }
+        if (c < 3) tmem_wait(v[(c + 1) & 1]);
       }
-      // pass 2: s = sum 2^y, t = sum 2^y * y, y = (x - m) log2 e
+      s_m[half][row_in_tile] = m;
+      named_bar(bar_id, 64);
+      m = fmaxf(m, s_m[half ^ 1][row_in_tile]);
+      // pass 2: s = sum 2^y, t = sum 2^y * y over this half, y = (x - m) log2 e
       const float mb = m * kLog2e;
       float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < kPN / 32; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
+      tmem_ld32_issue(taddr, v[0]);
+      tmem_wait(v[0]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < 3) tmem_ld32_issue(taddr + (c + 1) * 32, v[(c + 1) & 1]);
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          const float x0 = v[j] + s_bias[c * 32 + j], x1 = v[j + 1] + s_bias[c * 32 + j + 1];
+          const float x0 = v[c & 1][j] + bias[c * 32 + j], x1 = v[c & 1][j + 1] + bias[c * 32 + j + 1];
           const float y0 = fmaf(x0, kLog2e, -mb), y1 = fmaf(x1, kLog2e, -mb);
           const float e0 = fast_ex2(y0), e1 = fast_ex2(y1);
           s0 += e0;
@@ -266,19 +296,27 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           t0 = fmaf(e0, y0, t0);
           t1 = fmaf(e1, y1, t1);
           if (a.logits && live) {
-            if (a.logits_bf16) {
-              __nv_bfloat162 p = __floats2bfloat162_rn(x0, x1);
-              reinterpret_cast<__nv_bfloat162*>(a.logits)[(row * kPN + c * 32 + j) >> 1] = p;
-            } else {
-              reinterpret_cast<float2*>(a.logits)[(row * kPN + c * 32 + j) >> 1] = make_float2(x0, x1);
-            }
+            const int64_t at = row * kPN + c0 + c * 32 + j;
+            if (a.logits_bf16)
+              reinterpret_cast<__nv_bfloat162*>(a.logits)[at >> 1] = __floats2bfloat162_rn(x0, x1);
+            else
+              reinterpret_cast<float2*>(a.logits)[at >> 1] = make_float2(x0, x1);
           }
         }
+        if (c < 3) tmem_wait(v[(c + 1) & 1]);
       }
       tc_fence_before();
-      bar_arrive(&tempty[acc]);  // accumulator drained: the MMA warp may overwrite it
-      if (live) {
-        const float s = s0 + s1, t = t0 + t1;
+      bar_arrive(&tempty[acc]);  // this half of the accumulator drained
+      if (half == 1) {
+        s_st[0][row_in_tile] = s0 + s1;
+        s_st[1][row_in_tile] = t0 + t1;
+        s_st[2][row_in_tile] = xt;
+      }
+      named_bar(bar_id, 64);
+      if (half == 0 && live) {
+        // bins 0..127 then 128..255: a fixed order, identical run to run
+        const float s = (s0 + s1) + s_st[0][row_in_tile], t = (t0 + t1) + s_st[1][row_in_tile];
+        if (tok >= kPN / 2) xt = s_st[2][row_in_tile];
         // y = fma(x, log2e, -mb) with mb = fl(m log2e): every y carries the same shift
         // r = m log2e - mb (exact by fma), so ln sum 2^((x-m) log2e) = ln s - r ln2; the
         // entropy ln S - ln2 E[(x-m) log2e] is shift-free
@@ -288,11 +326,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         const double lp = ((double)xt - (double)m) - (ls - r * kLn2);
         const double h = ls - kLn2 * ey;
         if (a.out) {
-          ckrl_token_row r;
-          r.logprob = lp;
-          r.entropy = (float)h;
-          r.reserved = 0;
-          a.out[row] = r;
+          ckrl_token_row rr;
+          rr.logprob = lp;
+          rr.entropy = (float)h;
+          rr.reserved = 0;
+          a.out[row] = rr;
         }
         if (a.lp) a.lp[row] = lp;
         if (a.ent) a.ent[row] = (float)h;

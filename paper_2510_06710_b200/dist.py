@@ -33,6 +33,29 @@ def env_shard(num_envs: int, world: int, rank: int, group_size: int = 1) -> rang
     return range(g0 * group_size, g1 * group_size)
 
 
+def key_shard(env_keys, world: int):
+    """Shard envs by GRPO GroupKey (task_id, reset_state_id; assembler.cpp:207-226): every key's
+    envs land on one rank, so each rank's std::map grouping is the global grouping restricted
+    to its keys and only the retained-group count crosses ranks. `env_keys` is one key per env
+    (its grouped episode's key; envs drawing reset ids with replacement share keys across
+    non-adjacent envs, train.cpp:92-101). Keys are placed largest first on the least-loaded
+    rank (ties: lower rank, then key order), deterministic. Returns one ascending env-index
+    array per rank."""
+    if world < 1:
+        raise ConfigError("bad world")
+    keys = [tuple(np.atleast_1d(k).tolist()) for k in env_keys]
+    members = {}
+    for e, k in enumerate(keys):
+        members.setdefault(k, []).append(e)
+    load = [0] * world
+    parts = [[] for _ in range(world)]
+    for k in sorted(members, key=lambda q: (-len(members[q]), q)):
+        r = min(range(world), key=lambda i: (load[i], i))
+        parts[r].extend(members[k])
+        load[r] += len(members[k])
+    return [np.array(sorted(p), dtype=np.int64) for p in parts]
+
+
 def check_group_sharding(env_of_episode, key_of_episode, world: int, shard_of_env) -> None:
     """Raises ConfigError if any GroupKey (task, reset id) has members on two ranks: the
     rank-local grouping would then differ from the reference's global std::map grouping."""

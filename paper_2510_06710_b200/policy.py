@@ -41,14 +41,15 @@ def evaluate_chunks(logits: torch.Tensor, tokens: torch.Tensor, valid=None, stre
 
 
 def project_token_stats(feature: torch.Tensor, w_pol: torch.Tensor, b_pol, tokens: torch.Tensor,
-                        rows_out=None, want_logits=None, stream=None):
+                        rows_out=None, want_logits=None, stream=None, rows_only: bool = False):
     """Row N2: the policy head PolicyNet::logits_from_feature (policy/policy_net.cpp:265-274,
     logits = W_pol h + b_pol) on the tensor cores, fused with evaluate_chunk's per-position
     log-prob / entropy (:333-357). feature [..., H] bf16 (H a multiple of 64), w_pol [256, H]
     bf16, b_pol [256] f32 or None, tokens [...]. Returns {"token_rows": [..., 2] f64 (the
     16-byte ckrl_token_row per position: PolicyOutputs(token_rows=...) feeds the losses),
     "token_logprob": [...] f64, "token_entropy": [...] f32, "logits": [..., 256] (only with
-    want_logits = torch.float32 / torch.bfloat16)}."""
+    want_logits = torch.float32 / torch.bfloat16)}; rows_only skips the separate lp / entropy
+    arrays (the rows carry both)."""
     *lead, H = feature.shape
     rows = 1
     for d in lead:
@@ -62,8 +63,8 @@ def project_token_stats(feature: torch.Tensor, w_pol: torch.Tensor, b_pol, token
     b = None if b_pol is None else b_pol.to(device=dev, dtype=torch.float32).contiguous()
     if rows_out is None:
         rows_out = torch.empty((*lead, 2), dtype=torch.float64, device=dev)
-    lp = torch.empty(tuple(lead), dtype=torch.float64, device=dev)
-    ent = torch.empty(tuple(lead), dtype=torch.float32, device=dev)
+    lp = None if rows_only else torch.empty(tuple(lead), dtype=torch.float64, device=dev)
+    ent = None if rows_only else torch.empty(tuple(lead), dtype=torch.float32, device=dev)
     logits = None
     ld = _lib.DTYPE_F32
     if want_logits is not None:

@@ -205,3 +205,103 @@ def test_env_shard_keeps_groups_whole():
         check_group_sharding(envs, np.stack([np.zeros(512), envs % 8], 1), 8, owner)
     with pytest.raises(ConfigError):
         env_shard(10, 2, 0, group_size=4)
+
+
+def gather_envs(d, envs):
+    """The shard of envs `envs` (ascending, any subset): slab rows and their episodes, env ids
+    renumbered 0..len-1 in the same order."""
+    envs = np.asarray(envs)
+    out = {}
+    for k, v in d.items():
+        if k == "V":
+            out[k] = v
+        elif not k.startswith("ep_"):
+            out[k] = v[envs]
+    m = np.isin(d["ep_env_id"], envs)
+    for k in d:
+        if k.startswith("ep_"):
+            out[k] = d[k][m]
+    remap = {int(e): i for i, e in enumerate(envs)}
+    out["ep_env_id"] = np.array([remap[int(e)] for e in out["ep_env_id"]], dtype=d["ep_env_id"].dtype)
+    return out
+
+
+def make_grpo_merged(E=16, seed=9):
+    """Reset ids drawn with replacement (train.cpp:92-101): equal GroupKeys on non-adjacent envs."""
+    d = make_grpo(E=E, G=4, seed=seed)
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(0, 5, E).astype(d["ep_reset_id"].dtype)
+    d["ep_reset_id"] = ids[d["ep_env_id"]]
+    return d
+
+
+def key_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.bindings import Oracle
+    from paper_2510_06710_b200.dist import key_shard
+    orc = Oracle()
+    d = make_grpo_merged()
+    first = {}
+    for e, t, r in zip(d["ep_env_id"], d["ep_task"], d["ep_reset_id"]):
+        first.setdefault(int(e), (int(t), int(r)))
+    parts = key_shard([first[e] for e in range(16)], world)
+    s = gather_envs(d, parts[rank])
+    out = {}
+    for spec in [(0, 0, 0), (0, 2, 0)]:
+        st, a = orc.assemble_grpo(s, spec)
+        groups = torch.tensor([a["groups_retained"]], dtype=torch.int64)
+        dist.all_reduce(groups)
+        if a["groups_retained"]:
+            st, diag, _ = orc.grpo_loss(s, spec[1], a, s["logits"], 0.2)
+            raw = torch.tensor([-diag[1] * a["groups_retained"], diag[5] * diag[6], diag[4] * diag[6], diag[6]],
+                               dtype=torch.float64)
+        else:
+            raw = torch.zeros(4, dtype=torch.float64)
+        dist.all_reduce(raw)
+        out[spec] = dict(loss=-raw[0].item() / groups.item(), clip_frac=raw[2].item() / raw[3].item(),
+                         approx_kl=raw[1].item() / raw[3].item(), units=raw[3].item(), groups=groups.item())
+    if rank == 0:
+        q.put((out, [p.tolist() for p in parts]))
+    dist.destroy_process_group()
+
+
+def test_grpo_key_sharded_two_ranks_match_full_batch(oracle):
+    """Merged GroupKeys on non-adjacent envs: key_shard keeps every key on one rank, and the
+    two ranks' losses (retained-group count exchanged) equal the full batch's."""
+    world, port = 2, free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=key_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got, parts = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sorted(sum(parts, [])) == list(range(16)) and all(parts)
+    assert any(np.any(np.diff(p) > 1) for p in parts), "the shards should be non-contiguous here"
+    d = make_grpo_merged()
+    for spec, g in got.items():
+        st, a = oracle.assemble_grpo(d, spec)
+        st, diag, _ = oracle.grpo_loss(d, spec[1], a, d["logits"], 0.2)
+        assert g["groups"] == a["groups_retained"]
+        assert g["loss"] == pytest.approx(diag[0], rel=1e-10, abs=1e-12)
+        assert g["clip_frac"] == pytest.approx(diag[4], rel=1e-12)
+        assert g["approx_kl"] == pytest.approx(diag[5], rel=1e-10)
+        assert g["units"] == diag[6]
+
+
+def test_key_shard_balanced_and_whole():
+    from paper_2510_06710_b200.dist import key_shard
+    keys = [(0, i % 5) for i in range(37)]
+    parts = key_shard(keys, 3)
+    assert sorted(np.concatenate(parts).tolist()) == list(range(37))
+    owner = {}
+    for r, p in enumerate(parts):
+        for e in p:
+            assert owner.setdefault(keys[e], r) == r
+    sizes = sorted(len(p) for p in parts)
+    assert sizes[-1] - sizes[0] <= 8
