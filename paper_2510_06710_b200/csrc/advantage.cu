@@ -253,7 +253,10 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   if (tid == 0) s_n = scan_scratch[kGrpoThreads / 32];
   __syncthreads();
   const int n = s_n;
-  if (n > kGrpoMaxEligible) {
+  // up to kGrpoMaxEligible eligible episodes sort in shared memory; beyond, in the workspace's
+  // sort region (one eligible episode per env at most: the one starting at step 0)
+  const bool big = n > kGrpoMaxEligible;
+  if (big && n > num_envs) {
     if (tid == 0) {
       *st = StatsRecord{0.0, 0.0, 0, 0, 0, 0, 0, CKRL_ERR_INVALID_ARGUMENT};
       gb.group_counts[0] = gb.group_counts[1] = 0;
@@ -263,9 +266,11 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
     return;
   }
   while (cap < n) cap <<= 1;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
-  int32_t* idx = reinterpret_cast<int32_t*>(keys + kGrpoMaxEligible);
-  int32_t* gid = idx + kGrpoMaxEligible;  // reused: group id per sorted position
+  const int capacity = big ? pow2_at_least(num_envs) : kGrpoMaxEligible;
+  unsigned char* sort_base = big ? reinterpret_cast<unsigned char*>(ws + L.grpo_sort) : smem;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sort_base);
+  int32_t* idx = reinterpret_cast<int32_t*>(keys + capacity);
+  int32_t* gid = idx + capacity;  // reused: group id per sorted position
   for (int i = i0, k = base; i < i1; ++i)
     if (ep.complete[i] && ep.start_step[i] == 0) {
       keys[k] = group_key(ep.task_id[i], ep.reset_state_id[i]);
@@ -321,7 +326,7 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   __syncthreads();
   const int G = s_groups;
   // group start positions live in the (now free) tail of the key array
-  int32_t* gstart = reinterpret_cast<int32_t*>(smem + (size_t)kGrpoMaxEligible * 16);
+  int32_t* gstart = reinterpret_cast<int32_t*>(sort_base + (size_t)capacity * 16);
   for (int k = tid; k < n; k += kGrpoThreads)
     if (k == 0 || gid[k] != gid[k - 1]) gstart[gid[k]] = k;
   if (tid == 0) gstart[G] = n;

@@ -195,6 +195,8 @@ struct WsLayout {
   size_t asm_partials;  // AsmPartial per assembly CTA
   size_t loss_partials; // double[RAW_COUNT] per loss CTA
   size_t grpo_env;      // per-env int32 len, fs (GRPO assembly scratch)
+  size_t grpo_sort;     // GroupKey sort scratch when more episodes are eligible than fit in
+                        // shared memory: keys u64 / index / group id [pow2 >= E], starts [E+1]
   size_t total;
 };
 
@@ -204,6 +206,15 @@ struct AsmPartial {
   Moments m;
   double n_pos;  // counted slots
 };
+
+__host__ __device__ inline int pow2_at_least(int n) {
+  int c = 1;
+  while (c < n) c <<= 1;
+  return c;
+}
+__host__ __device__ inline size_t grpo_sort_bytes(int E) {
+  return (size_t)pow2_at_least(E) * 16 + sizeof(int32_t) * ((size_t)E + 1);
+}
 
 __host__ __device__ inline WsLayout ws_layout(int E, int world) {
   WsLayout L;
@@ -224,6 +235,7 @@ __host__ __device__ inline WsLayout ws_layout(int E, int world) {
   L.asm_partials = take(sizeof(AsmPartial) * (size_t)asm_ctas);
   L.loss_partials = take(sizeof(double) * RAW_COUNT * kMaxLossCtas);
   L.grpo_env = take(sizeof(int32_t) * 2 * (size_t)(E < 1 ? 1 : E));
+  L.grpo_sort = take(E > kGrpoMaxEligible ? grpo_sort_bytes(E) : 0);
   L.total = off;
   return L;
 }

@@ -150,6 +150,7 @@ struct PipeArgs {
   const double* gobs;   // generation's view of the observations [E][D]
   uint64_t* gsamp;      // generation's per-env sampling streams [E]
   GenOut gout;          // generation's action-batch destination
+  int gen_split;        // parallel sampler: bit 0 split trunk matvecs, bit 1 split logits matvec
 };
 
 __device__ void observe(const PipeArgs& a, int e, double* o) {
@@ -339,6 +340,31 @@ __device__ void matvec_t(const double* WT, const double* bias, int rows, int col
   }
 }
 
+// CKRL_SAMPLER_PARALLEL's matvec: four consecutive threads share a row, each summing a quarter
+// of the columns in order, combined as (p0 + p1) + (p2 + p3) by xor shuffles — a fixed order
+// (identical for every k and placement) with a dependency chain a quarter as long. nth must be
+// a multiple of 32 and every thread must call it (the shuffles span the warp).
+__device__ void matvec_split(const double* WT, const double* bias, int rows, int cols, const double* in,
+                             double* out, bool tanh_act, int tid, int nth) {
+  constexpr int G = 4;
+  const int g = tid & (G - 1), per = (cols + G - 1) / G;
+  const int c0 = g * per, c1 = min(cols, c0 + per);
+  for (int rb = 0; rb < rows; rb += nth / G) {
+    const int r = rb + tid / G;
+    double s = 0.0;
+    if (r < rows) {
+#pragma unroll 4
+      for (int c = c0; c < c1; ++c) s = madd(s, __ldg(WT + (int64_t)c * rows + r), in[c]);
+    }
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    if (g == 0 && r < rows) {
+      const double v = bias ? __dadd_rn(s, __ldg(bias + r)) : s;
+      out[r] = tanh_act ? tanh(v) : v;
+    }
+  }
+}
+
 // Transposed copies of every weight matrix (W[rows][cols] -> WT[cols][rows]), built once per
 // run into the workspace; biases and embeddings are read in place.
 struct PackSeg {
@@ -431,13 +457,16 @@ __device__ PolScratch carve(double* base, const PolicyLayout& L, bool emb_cache)
 // trunk layers (policy_net.cpp:214-226) on x -> feature pointer; block- or warp-synchronous
 template <bool BLOCK>
 __device__ const double* trunk_layers(const PipeArgs& a, const double* pk, const PolScratch& w, int tid,
-                                      int nth) {
+                                      int nth, bool split = false) {
   const PolicyLayout& L = a.pl;
   const double* in = w.x;
   double* out = w.h;
   for (int l = 0; l < L.L; ++l) {
     const int64_t bias = L.trunk + (int64_t)l * ((int64_t)L.H * L.H + L.H) + (int64_t)L.H * L.H;
-    matvec_t(pk + a.pk.trunk + (int64_t)l * L.H * L.H, a.params + bias, L.H, L.H, in, out, true, tid, nth);
+    if (split)
+      matvec_split(pk + a.pk.trunk + (int64_t)l * L.H * L.H, a.params + bias, L.H, L.H, in, out, true, tid, nth);
+    else
+      matvec_t(pk + a.pk.trunk + (int64_t)l * L.H * L.H, a.params + bias, L.H, L.H, in, out, true, tid, nth);
     if (BLOCK) __syncthreads(); else __syncwarp();
     double* t = const_cast<double*>(in);
     in = out;
@@ -479,29 +508,32 @@ constexpr int kGenThreads = 128;
 // partition's inclusive scan (own bins serially, warp Kogge-Stone, warp offsets), and the
 // token is the smallest v with u < cdf[v] (V - 1 if none, as the reference). Every thread
 // returns the token; w.red[4] = lse. Deterministic and independent of scheduling.
-__device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, int tid) {
+__device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, int tid, double& lse_out) {
   const int lane = tid & 31, warp = tid >> 5;
   const int q = (V + kGenThreads - 1) / kGenThreads;
   const int v0 = tid * q, v1 = min(V, v0 + q);
+  // block scratch in w.ex (unused by this sampler): warp sums, warp scan totals, warp minima —
+  // distinct slots, so only the three hand-off barriers below are needed
+  double* s_sum = w.ex;
+  double* s_scan = w.ex + 4;
+  int* s_min = reinterpret_cast<int*>(w.ex + 8);
   double part = 0.0;
-  for (int v = v0; v < v1; ++v) {
-    const double ex = exp(__dsub_rn(w.lg[v], mx));
-    part = __dadd_rn(part, ex);
-  }
+  for (int v = v0; v < v1; ++v) part = __dadd_rn(part, exp(__dsub_rn(w.lg[v], mx)));
   double tot = part;
 #pragma unroll
   for (int o = 16; o; o >>= 1) tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, o));
-  __syncthreads();  // w.red[] is free (the max has been read)
-  if (lane == 0) w.red[warp] = tot;
+  if (lane == 0) s_sum[warp] = tot;
   __syncthreads();
-  const double sum = __dadd_rn(__dadd_rn(w.red[0], w.red[1]), __dadd_rn(w.red[2], w.red[3]));
+  const double sum = __dadd_rn(__dadd_rn(s_sum[0], s_sum[1]), __dadd_rn(s_sum[2], s_sum[3]));
   const double lse = __dadd_rn(mx, log(sum));
-  // probabilities and this thread's inclusive partial sums
+  // probabilities (kept in registers for up to 8 bins per thread) and this thread's inclusive sum
+  constexpr int kQ = 8;
+  double pv[kQ];
   double acc = 0.0;
   for (int v = v0; v < v1; ++v) {
-    const double pv = exp(__dsub_rn(w.lg[v], lse));
-    w.ex[v] = pv;
-    acc = __dadd_rn(acc, pv);
+    const double p = exp(__dsub_rn(w.lg[v], lse));
+    if (v - v0 < kQ) pv[v - v0] = p;
+    acc = __dadd_rn(acc, p);
   }
   // exclusive prefix of the thread totals: warp inclusive scan + preceding warps' totals
   double inc = acc;
@@ -510,31 +542,25 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
     const double y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc = __dadd_rn(inc, y);
   }
+  if (lane == 31) s_scan[warp] = inc;
   __syncthreads();
-  if (lane == 31) w.red[warp] = inc;
-  __syncthreads();
-  // this thread's exclusive prefix inside its warp: the previous lane's inclusive value
-  double base = __shfl_up_sync(0xffffffffu, inc, 1);
+  double base = __shfl_up_sync(0xffffffffu, inc, 1);  // the previous lane's inclusive value
   if (lane == 0) base = 0.0;
   double woff = 0.0;
-  for (int q2 = 0; q2 < warp; ++q2) woff = __dadd_rn(woff, w.red[q2]);
+  for (int q2 = 0; q2 < warp; ++q2) woff = __dadd_rn(woff, s_scan[q2]);
   double c = __dadd_rn(woff, base);
   int hit = V;
   for (int v = v0; v < v1; ++v) {
-    c = __dadd_rn(c, w.ex[v]);
+    c = __dadd_rn(c, v - v0 < kQ ? pv[v - v0] : exp(__dsub_rn(w.lg[v], lse)));
     if (u < c && hit == V) hit = v;
   }
-  // smallest hit over the block
   int m = hit;
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-  int* sred = reinterpret_cast<int*>(w.red + 6);
+  if (lane == 0) s_min[warp] = m;
   __syncthreads();
-  if (lane == 0) sred[warp] = m;
-  __syncthreads();
-  m = min(min(sred[0], sred[1]), min(sred[2], sred[3]));
-  if (tid == 0) w.red[4] = lse;
-  __syncthreads();
+  m = min(min(s_min[0], s_min[1]), min(s_min[2], s_min[3]));
+  lse_out = lse;
   return m < V ? m : V - 1;
 }
 
@@ -560,17 +586,26 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
       double s = 0.0;
       for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
       s = __dadd_rn(s, __dadd_rn(__ldg(p + L.b_in + hh), __ldg(p + L.pos_bias + (int64_t)pos * L.H + hh)));
+      if (par) {  // the prefix's embeddings as one running sum
+        if (pos > 0) s = __dadd_rn(s, w.embc[hh]);
+      } else {
 #pragma unroll 8
-      for (int k = 0; k < pos; ++k) s = __dadd_rn(s, w.embc[k * L.H + hh]);
+        for (int k = 0; k < pos; ++k) s = __dadd_rn(s, w.embc[k * L.H + hh]);
+      }
       w.x[hh] = s;
     }
     __syncthreads();
-    const double* f = trunk_layers<true>(a, pk, w, tid, kGenThreads);
+    const double* f = trunk_layers<true>(a, pk, w, tid, kGenThreads, par && (a.gen_split & 1));
     if (pos == 0)
       for (int hh = tid; hh < L.H; hh += kGenThreads) w.f0[hh] = f[hh];
     // logits (logits_from_feature) + block max
-    matvec_t(pk + a.pk.wpol, p + L.b_pol, L.V, L.H, f, w.lg, false, tid, kGenThreads);
     double mx = -INFINITY;
+    if (par && (a.gen_split & 2)) {
+      matvec_split(pk + a.pk.wpol, p + L.b_pol, L.V, L.H, f, w.lg, false, tid, kGenThreads);
+      __syncthreads();  // rows were written by other threads
+    } else {
+      matvec_t(pk + a.pk.wpol, p + L.b_pol, L.V, L.H, f, w.lg, false, tid, kGenThreads);
+    }
     for (int v = tid; v < L.V; v += kGenThreads) mx = fmax(mx, w.lg[v]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -582,19 +617,19 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
       for (int v = tid; v < L.V; v += kGenThreads) dst[v] = (float)w.lg[v];
     }
     if (par) {  // fixed-order block reductions / scan (identical for every k and placement)
-      const int tok = sample_parallel(w, L.V, mx, rng_double(rng), tid);
-      const double lse = w.red[4];
+      double lse;
+      const int tok = sample_parallel(w, L.V, mx, rng_double(rng), tid, lse);
       if (tid == 0) {
         const double lp = __dsub_rn(w.lg[tok], lse);
         const int64_t k = rec * L.P + pos;
         go.tokens[k] = tok;
         go.lp[k] = (float)lp;
         go.lp64[k] = lp;
-        w.prefix[pos] = tok;
       }
-      __syncthreads();
+      // every thread holds the token: the running embedding sum of the prefix (row 0 of the
+      // cache) is updated by the thread that reads it in the next trunk input
       for (int hh = tid; hh < L.H; hh += kGenThreads)
-        w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
+        w.embc[hh] = __dadd_rn(pos == 0 ? 0.0 : w.embc[hh], __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh));
       continue;
     }
     // log_softmax (policy_net.cpp:90-102): exps in parallel, the sum in v order on thread 0
@@ -970,6 +1005,14 @@ cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckr
   a.reset_ids = sp.reset_state_ids;
   a.out = out;
   a.sampler = sp.sampler;
+  {  // CKRL_GEN_SPLIT (A/B): which matvecs the parallel sampler splits across 4 threads per row
+    static int split = -1;
+    if (split < 0) {
+      const char* env = getenv("CKRL_GEN_SPLIT");
+      split = env ? atoi(env) : 1;
+    }
+    a.gen_split = split;
+  }
   double* packed = nullptr;
   const size_t env_ws = pipeline_ws_layout(sp, &a.st, &a.post_obs, ws, &packed);
   a.packed = packed;

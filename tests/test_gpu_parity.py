@@ -300,3 +300,36 @@ def test_compute_gae_random_vs_oracle(oracle):
         oa, orr = oracle.compute_gae(r, v, b, te, tr, 0.97, 0.9)
         np.testing.assert_allclose(adv.cpu().numpy(), oa, rtol=1e-12, atol=1e-12)
         np.testing.assert_allclose(ret.cpu().numpy(), orr, rtol=1e-12, atol=1e-12)
+
+
+def test_grpo_beyond_shared_memory_sort(oracle):
+    """More eligible episodes than the group kernel's shared-memory sort holds (8192): the
+    GroupKey sort runs in the workspace's sort region. Reset ids drawn with replacement
+    (train.cpp:92-101) leave the keys unordered, so the bitonic sort really runs; group
+    assignment, membership and the fp64 advantages must equal the oracle's bit-for-bit."""
+    from paper_2510_06710_b200 import synth
+    E = 9216
+    cfg = synth.SynthConfig(num_envs=E, num_chunks=6, chunk_len=1, tokens_per_action=2, vocab=16,
+                            algo="grpo", mode="mask", max_episode_steps=6, group_size=8, seed=21)
+    d = synth.episodes_numpy(cfg)
+    rng = np.random.default_rng(21)
+    ids = rng.integers(0, E // 6, E).astype(d["ep_reset_id"].dtype)
+    d["ep_reset_id"] = ids[d["ep_env_id"]]
+    logits, tokens, old = synth.token_tensors(cfg)
+    d["tokens"], d["old_logprob"] = tokens.cpu().numpy(), old.cpu().numpy()
+    spec = GranularitySpec(Level(0), Level(1), Level(0))
+    ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], cfg.vocab)
+    ept = EpisodeTable.from_arrays(d)
+    step = optim.GrpoStep(ro, GrpoAssemblyOptions(spec), GrpoParams(0.2))
+    step(ro, ept, PolicyOutputs(logits))
+    got = diag_vec(step.diagnostics())
+    r = rounded({**d, "logits": logits.cpu().numpy()})
+    st, asm = oracle.assemble_grpo(r, (0, 1, 0))
+    assert st == 0 and int((np.asarray(d["ep_complete"]) != 0).sum()) > 8192
+    assert (step.batch.groups_total, step.batch.groups_retained) == (asm["groups_total"], asm["groups_retained"])
+    np.testing.assert_array_equal(step.batch.env_group.cpu().numpy(), asm["env_group"])
+    np.testing.assert_array_equal(step.batch.env_advantage.cpu().numpy(), asm["env_adv"])
+    np.testing.assert_array_equal(step.batch.slot_member.cpu().numpy(), asm["slot_member"])
+    st, want, _ = oracle.grpo_loss(r, 1, asm, r["logits"], 0.2)
+    assert got[6] == want[6]
+    assert_close(got[:6], want[:6], TOL, "grpo 9216 envs diag")

@@ -151,6 +151,11 @@ def test_grpo_loss_from_token_rows_equals_logits():
         step(ro, ept, pol)
         res.append((step.diagnostics(), step.outputs.coeff_logprob.clone()))
     (d0, k0), (d1, k1) = res
-    for key in ("loss", "surrogate", "approx_kl", "clip_frac"):
+    # the GRPO loss is a signed sum whose terms cancel (group-relative advantages sum to ~0):
+    # its error scales with the terms' L1 mass, which at token level is sum |coeff_lp|
+    mass = float(k0.abs().sum())
+    for key in ("loss", "surrogate"):
+        assert_close([d1[key]], [d0[key]], TOL, f"grpo token-rows {key}", floor=mass)
+    for key in ("approx_kl", "clip_frac"):
         assert_close([d1[key]], [d0[key]], TOL, f"grpo token-rows {key}")
     assert_close(k1.cpu().numpy(), k0.cpu().numpy(), TOL, "grpo token-rows coeff_lp")
