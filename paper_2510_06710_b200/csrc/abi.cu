@@ -127,8 +127,10 @@ void set_outputs(LossArgs& a, const ckrl_loss_outputs* o) {
   a.all_rows = (o->token_logprob || o->token_entropy) ? 1 : 0;
 }
 
-int32_t check_policy(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
+int32_t check_policy(const ckrl_rollout* ro, const ckrl_policy_outputs* po, const ckrl_loss_outputs* out) {
   CKRL_REQUIRE(po != nullptr, CKRL_ERR_INVALID_ARGUMENT, "policy outputs are null");
+  CKRL_REQUIRE(!(po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS && out && out->dlogits), CKRL_ERR_INVALID_ARGUMENT,
+               "dlogits need the logits (token rows carry only the finished log-prob / entropy)");
   CKRL_REQUIRE(po->logits_dtype == CKRL_DTYPE_F32 || po->logits_dtype == CKRL_DTYPE_BF16 ||
                    po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS,
                CKRL_ERR_INVALID_ARGUMENT, "logits dtype must be f32, bf16 or token rows");
@@ -634,7 +636,7 @@ int32_t ckrl_ppo_loss(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
   if (st) return st;
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, 1))) return st;
   CKRL_REQUIRE(b && p && diag && b->counted && b->advantages && b->returns,
                CKRL_ERR_INVALID_ARGUMENT, "batch / params / diag required");
@@ -690,7 +692,7 @@ int32_t ckrl_grpo_loss(const ckrl_rollout* ro, const ckrl_grpo_batch* gb,
   if (st) return st;
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, 1))) return st;
   CKRL_REQUIRE(gb && p && diag, CKRL_ERR_INVALID_ARGUMENT, "batch / params / diag required");
   WsLayout L = ws_layout(ro->num_envs, 1);
@@ -727,7 +729,7 @@ int32_t ckrl_ppo_step(const ckrl_rollout* ro, const ckrl_policy_outputs* po,
     return fail(CKRL_ERR_CONFIG, "value_type must match reward_type for GAE assembly");
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, true))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
@@ -775,7 +777,7 @@ int32_t ckrl_grpo_step(const ckrl_rollout* ro, const ckrl_episodes* ep,
   if (st) return st;
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
@@ -822,7 +824,7 @@ int32_t ckrl_ppo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po
   if (st) return st;
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;
@@ -868,7 +870,7 @@ int32_t ckrl_grpo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* p
   if (st) return st;
   if ((st = check_device())) return st;
   if ((st = check_rollout(ro, false))) return st;
-  if ((st = check_policy(ro, po))) return st;
+  if ((st = check_policy(ro, po, out))) return st;
   if ((st = check_comm(comm))) return st;
   const int world = comm ? comm->world : 1;
   if ((st = check_ws(ws, ws_bytes, ro->num_envs, world))) return st;

@@ -9,18 +9,20 @@
 //
 //   [rows x H] bf16 features  x  [256 x H] bf16 W_pol  ->  [128 x 256] f32 tiles in TMEM
 //
-//   warp 0 (one lane)  TMA producer: 2-D tensor copies (128-byte swizzle) of a 128-row
-//                      feature slab and the 256-row W_pol slab per 64-wide K step into a
-//                      4-stage shared-memory ring (mbarrier complete_tx).
+//   warps 0 / 10       TMA producers (one lane each): 2-D tensor copies (128-byte swizzle) per
+//                      64-wide K step — warp 0 the 128-row feature slabs into a 7-stage ring
+//                      (the HBM stream, 112 KB in flight), warp 10 the 256-row W_pol slabs
+//                      (L2-resident) into a 3-stage ring; mbarrier complete_tx.
 //   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16, into
 //                      one of two 256-column TMEM accumulators (512 columns: the epilogue of
 //                      tile i overlaps the MMAs of tile i+1); tcgen05.commit frees the smem
 //                      stage and, after the last K step, hands the accumulator to the epilogue.
-//   warps 2-5          epilogue: TMEM lane = tile row, so each thread owns one position's
-//                      whole 256-bin row (tcgen05.ld 32x32b.x32, 8 column chunks). Bias, max,
-//                      sum of exp2, the entropy sum and the sampled token's logit in
-//                      registers; log-prob and entropy finished in fp64; the row record
-//                      {lp, H} (and optionally the logits) written straight to HBM.
+//   warps 2-9          epilogue: TMEM lane = tile row; warp w reads lane quarter w % 4 and one
+//                      128-bin column half (tcgen05.ld 32x32b.x32, the next load in flight);
+//                      bias, max, sum of exp2, the entropy sum and the sampled token's logit in
+//                      registers, the two halves combined through shared memory; log-prob and
+//                      entropy finished in fp64; the row record {lp, H} (and optionally the
+//                      logits) written straight to HBM.
 //
 // Nothing of the 256-bin row is ever written unless asked for: the loss consumes the
 // 16-byte row records (CKRL_DTYPE_TOKEN_ROWS), so the step's HBM traffic is the features
@@ -36,12 +38,13 @@ namespace {
 constexpr int kPM = 128;  // positions per tile (UMMA M; TMEM lanes)
 constexpr int kPN = 256;  // bins (UMMA N; TMEM columns per accumulator)
 constexpr int kPK = 64;   // K per stage: one 128-byte swizzle atom of bf16
-constexpr int kPStages = 4;
+constexpr int kStA = 7;  // feature stages (16 KB): the HBM stream, deeper in flight
+constexpr int kStB = 3;  // W_pol stages (32 KB): served from L2
 constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kPN * kPK * 2;  // 32 KB
-constexpr int kProjThreads = 320;            // producer, MMA, 8 epilogue warps
+constexpr int kProjThreads = 352;            // A producer, MMA, 8 epilogue warps, B producer
 constexpr uint32_t kTmemCols = 512;          // two 256-column accumulators
-constexpr size_t kProjSmem = 1024 /*align slack*/ + kPStages * (size_t)(kABytes + kBBytes) + 1024 /*bias*/ +
+constexpr size_t kProjSmem = 1024 /*align slack*/ + kStA * (size_t)kABytes + kStB * (size_t)kBBytes + 1024 /*bias*/ +
                              256 /*barriers*/ + 5 * 128 * 4 /*half exchange*/;
 
 // Instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = 256, M = 128.
@@ -151,12 +154,14 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  unsigned char* sa = base;                                   // kPStages x 16 KB
-  unsigned char* sb = base + kPStages * kABytes;              // kPStages x 32 KB
-  float* s_bias = reinterpret_cast<float*>(sb + kPStages * kBBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_bias + kPN);
-  uint64_t* empty = full + kPStages;
-  uint64_t* tfull = empty + kPStages;  // [2]
+  unsigned char* sa = base;                                   // kStA x 16 KB
+  unsigned char* sb = base + kStA * kABytes;                  // kStB x 32 KB
+  float* s_bias = reinterpret_cast<float*>(sb + kStB * kBBytes);
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(s_bias + kPN);
+  uint64_t* empty_a = full_a + kStA;
+  uint64_t* full_b = empty_a + kStA;
+  uint64_t* empty_b = full_b + kStB;
+  uint64_t* tfull = empty_b + kStB;  // [2]
   uint64_t* tempty = tfull + 2;        // [2]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
   float (*s_m)[kPM] = reinterpret_cast<float (*)[kPM]>(s_bias + kPN + 64);   // [2][128] half maxima
@@ -165,9 +170,13 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kPN; i += kProjThreads) s_bias[i] = a.b_pol ? a.b_pol[i] : 0.0f;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kPStages; ++s) {
-      bar_init(&full[s], 1);
-      bar_init(&empty[s], 1);
+    for (int s = 0; s < kStA; ++s) {
+      bar_init(&full_a[s], 1);
+      bar_init(&empty_a[s], 1);
+    }
+    for (int s = 0; s < kStB; ++s) {
+      bar_init(&full_b[s], 1);
+      bar_init(&empty_b[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(&tfull[i], 1);
@@ -187,20 +196,30 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      uint64_t pol_a, pol_b;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
+  if (warp == 0 || warp == 10) {
+    if (lane == 0) {  // ---- TMA producers: warp 0 the feature slabs, warp 10 the W_pol slabs
+      const bool is_a = warp == 0;
+      uint64_t pol;
+      if (is_a)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      const int nst = is_a ? kStA : kStB;
+      uint64_t* fullx = is_a ? full_a : full_b;
+      uint64_t* emptyx = is_a ? empty_a : empty_b;
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         for (int kb = 0; kb < a.n_kb; ++kb) {
-          bar_wait(&empty[stage], phase ^ 1);
-          bar_expect(&full[stage], kABytes + kBBytes);
-          tma_2d(su32(sa + stage * kABytes), &map_a, kb * kPK, (int)(tile * kPM), &full[stage], pol_a);
-          tma_2d(su32(sb + stage * kBBytes), &map_b, kb * kPK, 0, &full[stage], pol_b);
-          if (++stage == kPStages) {
+          bar_wait(&emptyx[stage], phase ^ 1);
+          if (is_a) {
+            bar_expect(&fullx[stage], kABytes);
+            tma_2d(su32(sa + stage * kABytes), &map_a, kb * kPK, (int)(tile * kPM), &fullx[stage], pol);
+          } else {
+            bar_expect(&fullx[stage], kBBytes);
+            tma_2d(su32(sb + stage * kBBytes), &map_b, kb * kPK, 0, &fullx[stage], pol);
+          }
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -209,8 +228,8 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
-      int stage = 0;
-      uint32_t phase = 0;
+      int sa_i = 0, sb_i = 0;
+      uint32_t pa = 0, pb = 0;
       int i = 0;
       for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++i) {
         const int acc = i & 1;
@@ -219,22 +238,28 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * kPN);
         for (int kb = 0; kb < a.n_kb; ++kb) {
-          bar_wait(&full[stage], phase);
+          bar_wait(&full_a[sa_i], pa);
+          bar_wait(&full_b[sb_i], pb);
           tc_fence_after();
-          const uint32_t a0 = su32(sa + stage * kABytes), b0 = su32(sb + stage * kBBytes);
+          const uint32_t a0 = su32(sa + sa_i * kABytes), b0 = su32(sb + sb_i * kBBytes);
 #pragma unroll
           for (int k = 0; k < kPK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
             umma(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), (kb | k) != 0);
-          umma_commit(&empty[stage]);
-          if (++stage == kPStages) {
-            stage = 0;
-            phase ^= 1;
+          umma_commit(&empty_a[sa_i]);  // both slots free once these MMAs have read them
+          umma_commit(&empty_b[sb_i]);
+          if (++sa_i == kStA) {
+            sa_i = 0;
+            pa ^= 1;
+          }
+          if (++sb_i == kStB) {
+            sb_i = 0;
+            pb ^= 1;
           }
         }
         umma_commit(&tfull[acc]);
       }
     }
-  } else {
+  } else if (warp >= 2 && warp < 10) {
     // ---- epilogue: 8 warps. Warp w (2..9) reads TMEM lane quarter q = w % 4 (the hardware
     // rule: a warp reaches lanes 32*(w%4) .. +31) and column half h = (w-2)/4, so every tile
     // row is split between two threads, 128 bins each; the halves trade their max and their

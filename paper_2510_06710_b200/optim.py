@@ -238,7 +238,7 @@ class Pipelined:
         self.ev_asm = [torch.cuda.Event() for _ in range(n)]
         self.ev_loss = [torch.cuda.Event() for _ in range(n)]
 
-    def issue(self, K: int, args_of, loss_events=None, span_events=None):
+    def issue(self, K: int, args_of, loss_events=None):
         import torch
         n = len(self.steps)
         main = torch.cuda.current_stream()
@@ -264,13 +264,9 @@ class Pipelined:
             main.wait_event(self.ev_asm[i % n])
             if loss_events is not None:  # (start, end) timing events around each loss launch
                 loss_events[i][0].record(main)
-            if span_events is not None and i == 0:  # (start, end) around the whole loss chain
-                span_events[0].record(main)
             self.steps[i % n].loss(*l_args, stream=main)
             if loss_events is not None:
                 loss_events[i][1].record(main)
-            if span_events is not None and i == K - 1:
-                span_events[1].record(main)
             self.ev_loss[i % n].record(main)
         main.wait_stream(side)
 

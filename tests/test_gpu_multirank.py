@@ -307,3 +307,60 @@ def test_pipelined_batches_match_plain_steps(world):
     for c in comms:
         if c is not None:
             c.close()
+
+
+@pytest.mark.parametrize("algo", ["ppo", "grpo"])
+def test_pipelined_graph_matches_plain_steps(algo):
+    """The bench's form of the pipelined step: optim.Pipelined captured in one CUDA graph (the
+    losses chained as programmatic dependents, the assemblies on a side stream) and replayed;
+    every batch's diagnostics and masks equal one plain step per batch (single rank, PPO cfg3
+    and GRPO cfg2 shapes)."""
+    cfg_name = "cfg3" if algo == "ppo" else "cfg2"
+    a, l, v = synth.SPECS[cfg_name]
+    spec = GranularitySpec(Level(a), Level(l), Level(v))
+    R, n_batches = 3, 8
+    data = [case(cfg_name, 64, seed=40 + r) for r in range(R)]
+    inputs = []
+    for cfg, d, logits in data:
+        ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], cfg.vocab)
+        nv = torch.tensor(d["new_value_scalar"], dtype=torch.float32, device="cuda")
+        ept = EpisodeTable.from_arrays(d) if algo == "grpo" else None
+        inputs.append((ro, PolicyOutputs(logits, nv), ept))
+
+    def mk(rep):
+        ro = inputs[rep][0]
+        if algo == "ppo":
+            return optim.PpoStep(ro, GaeParams(0.99, 0.95), spec, PpoParams(0.2, 0.5, 0.01, True))
+        return optim.GrpoStep(ro, GrpoAssemblyOptions(spec), GrpoParams(0.2))
+
+    def args_of(i):
+        ro, pol, ept = inputs[i % R]
+        return ((ro,), (ro, pol)) if algo == "ppo" else ((ro, ept), (ro, pol))
+
+    plain = [mk(rep) for rep in range(R)]
+    want = {}
+    for i in range(n_batches):
+        ro, pol, ept = inputs[i % R]
+        plain[i % R](ro, pol) if algo == "ppo" else plain[i % R](ro, ept, pol)
+        torch.cuda.synchronize()
+        want[i] = plain[i % R].diagnostics()
+    pipe = optim.Pipelined([mk(rep) for rep in range(R)])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        pipe.issue(1, args_of)  # warm-up outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pipe.issue(n_batches, args_of)
+    for _ in range(2):  # replays are idempotent: every batch recomputes from its inputs
+        g.replay()
+        torch.cuda.synchronize()
+        for rep in range(R):
+            last = max(i for i in range(n_batches) if i % R == rep)
+            assert pipe.steps[rep].diagnostics() == want[last], rep
+            if algo == "ppo":
+                assert torch.equal(pipe.steps[rep].batch.counted, plain[rep].batch.counted)
+            else:
+                assert torch.equal(pipe.steps[rep].batch.env_group, plain[rep].batch.env_group)

@@ -159,3 +159,20 @@ def test_grpo_loss_from_token_rows_equals_logits():
     for key in ("approx_kl", "clip_frac"):
         assert_close([d1[key]], [d0[key]], TOL, f"grpo token-rows {key}")
     assert_close(k1.cpu().numpy(), k0.cpu().numpy(), TOL, "grpo token-rows coeff_lp")
+
+
+def test_token_rows_reject_dlogits():
+    """The softmax-backward seam needs the logits; with token rows the loss refuses it up front."""
+    cfg = synth.SynthConfig(**{**synth.CONFIGS["cfg3"].__dict__, "num_envs": 4})
+    d = synth.episodes_numpy(cfg)
+    _, tokens, old = synth.token_tensors(cfg)
+    d["tokens"], d["old_logprob"] = tokens, old
+    ro = RolloutBuffer.from_arrays(d, d["boot_scalar"], cfg.vocab)
+    rows = torch.zeros((*tokens.shape, 2), dtype=torch.float64, device="cuda")
+    nv = torch.tensor(d["new_value_scalar"], dtype=torch.float32, device="cuda")
+    step = optim.PpoStep(ro, GaeParams(0.99, 0.95), GranularitySpec(Level(0), Level(0), Level(0)),
+                         PpoParams(0.2, 0.5, 0.01, True))
+    step.outputs.dlogits = torch.empty((*tokens.shape, 256), dtype=torch.float32, device="cuda")
+    step._oc = step.outputs.c()
+    with pytest.raises(errors.InvalidArgument):
+        step(ro, PolicyOutputs(None, nv, token_rows=rows))
