@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--head", type=int, default=0,
                    help="row N2: feed the step from trunk features of this width H through the "
                         "tcgen05 policy-head projection (ckrl_project_token_stats) instead of logits")
+    p.add_argument("--loss-streams", type=int, default=2,
+                   help="pipelined steps: alternate the losses over this many streams")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
@@ -446,7 +448,7 @@ def main():
             # replica (its own workspace / batch buffers), the public two-halves API
             steps = [step] + [optim.PpoStep(reps[r][0], GaeParams(0.99, 0.95), spec,
                                             PpoParams(0.2, 0.5, 0.01, True), comm=comm) for r in range(1, R)]
-            pipe = optim.Pipelined(steps)
+            pipe = optim.Pipelined(steps, loss_streams=args.loss_streams)
     else:
         opts = GrpoAssemblyOptions(spec)
         step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
@@ -454,7 +456,7 @@ def main():
         launches_per_step = 3
         if args.pipeline and args.grad is None:
             steps = [step] + [optim.GrpoStep(reps[r][0], opts, GrpoParams(0.2), comm=comm) for r in range(1, R)]
-            pipe = optim.Pipelined(steps)
+            pipe = optim.Pipelined(steps, loss_streams=args.loss_streams)
     run = run0
     if args.grad == "fused":  # dlogits written by the loss launch itself (LossOutputs.dlogits)
         step.outputs.dlogits = torch.empty_like(reps[0][1].logits)
@@ -634,9 +636,10 @@ def main():
         "timing": {"l2": f"inputs rotate over {R} replicas ({R * per_rep / 2**20:.0f} MiB of logits > 126 MB L2)",
                    "cuda_graph": f"one graph of all {K} steps" if graph is not None else "eager launches",
                    "untimed_replay_before_timing": graph is not None,
-                   "pipelined": ("batch i+1's assembly on a side stream overlaps batch i's loss "
-                                 "(ckrl_ppo_step_assemble / ckrl_ppo_step_loss, one workspace per replica); "
-                                 "every step still runs its full assembly and loss") if pipe is not None else False},
+                   "pipelined": ("batch i+1's assembly on a side stream overlaps batch i's loss; the losses "
+                                 f"alternate over {args.loss_streams} streams (ckrl_*_step_assemble / "
+                                 "ckrl_*_step_loss, one workspace per replica); every step still runs its full "
+                                 "assembly and loss") if pipe is not None else False},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "tile_kernel (fused token + loss)" + (" + dlogits" if args.grad == "fused" else ""),

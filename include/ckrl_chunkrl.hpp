@@ -359,7 +359,10 @@ struct LossDiagnostics {
 /// The current policy as the loss sees it. Either its two public calls (filled for the
 /// selected records only, like the reference's evaluate_chunk / value), or a view of its
 /// logits [E][Tc][C][M][V] (f32 or bf16) and new values (value-level shape, f32) for every
-/// record, on the device (`device = true`) or in host memory.
+/// record, on the device (`device = true`) or in host memory. With logits_dtype =
+/// CKRL_DTYPE_TOKEN_ROWS the view is [E][Tc][C][M] ckrl_token_row instead: the policy head
+/// already reduced on the tensor cores (ckrl_project_token_stats over the trunk features,
+/// PolicyNet::logits_from_feature + evaluate_chunk, policy_net.cpp:265-284, 333-357).
 struct CurrentPolicy {
   LogitsFn forward_logits;
   ValueFn value;

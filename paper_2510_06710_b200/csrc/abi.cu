@@ -573,9 +573,28 @@ static int chain_enabled() {
   static int n = -1;
   if (n < 0) {
     const char* env = getenv("CKRL_CHAIN");
-    n = env ? atoi(env) : 1;
+    n = env ? atoi(env) : 2;
   }
   return n;
+}
+
+// Whether a pipelined loss launches as a programmatic dependent (CKRL_CHAIN: 0 never, 1 always,
+// 2 = by size, the default). By size: launches of < 8 or > 64 56-KB tiles per SM chain; in
+// between they launch normally. Measured with two alternating loss streams (optim.Pipelined):
+// cfg1 (4 tiles/SM) 14.7 -> 13.7 us and cfg4 (221) 296 -> 284 us with chaining, cfg3 (17)
+// 34.6 -> 33.1 us and cfg2 (17, GRPO) 37.4 -> 32.9 us without — the early-launched CTAs hold
+// SMs the next batch's assembly (GRPO: a 160 KB-smem group kernel) then waits for.
+static bool chain_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
+  const int mode = chain_enabled();
+  if (mode == 0 || po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS) return false;
+  if (mode == 1) return true;
+  const double bytes = (double)ro->num_envs * ro->num_chunks * ro->chunk_len * ro->tokens_per_action *
+                       ro->vocab * (po->logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double per_sm = bytes / (56.0 * 1024) / (sms > 0 ? sms : 148);
+  return per_sm < 8.0 || per_sm > 64.0;
 }
 
 static LossArgs ppo_args(const ckrl_rollout* ro, const ckrl_ppo_batch* b,
@@ -837,7 +856,7 @@ int32_t ckrl_ppo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1);
   a.ex = exchange_view(comm);
   a.max_ctas = loss_cta_cap(comm);
-  if (chain_enabled() && po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS) {
+  if (chain_loss(ro, po)) {
     a.pdl = 1;
     a.ro = *ro;
   }
@@ -878,7 +897,7 @@ int32_t ckrl_grpo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* p
   WsLayout L = ws_layout(ro->num_envs, world);
   return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
-                        (cudaStream_t)stream, chain_enabled() && po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS,
+                        (cudaStream_t)stream, chain_loss(ro, po),
                         exchange_view(comm), loss_cta_cap(comm));
 }
 

@@ -701,7 +701,10 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
   const int V = vocab_of(net, batch.records[record_indices[0]].rec->obs);
   const std::size_t P = static_cast<std::size_t>(C) * M;
   const int NV = vec ? C : 1, U = action ? C : 1;
-  const int lb = net.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4;
+  // bytes per position of the policy view: a V-bin logits row, or one finished token row
+  // (CKRL_DTYPE_TOKEN_ROWS, the tensor-core policy head's output: ckrl_project_token_stats)
+  const std::size_t pb = net.logits_dtype == CKRL_DTYPE_TOKEN_ROWS ? sizeof(ckrl_token_row)
+                         : static_cast<std::size_t>(V) * (net.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
   if (net.logits && !batch.device)
     throw ConfigError("ppo_loss: a logits view needs a batch assembled by this library (record order)");
 
@@ -761,7 +764,7 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
   sfl.upload(fl);
   scnt.upload(cnt);
   sboot.zero();
-  DevBuf<unsigned char> logits(static_cast<std::size_t>(n) * P * V * lb);
+  DevBuf<unsigned char> logits(static_cast<std::size_t>(n) * P * pb);
   ckrl_policy_outputs src_pol{net.logits_dtype, nullptr, nullptr};
   ckrl_rollout src{static_cast<int32_t>(n), 1, C, M, V, CKRL_DTYPE_I32, stok.get(), solp.get(), srew.get(), sfl.get(),
                    seid.get(), svs.get(), svv.get(), sboot.get()};
@@ -778,7 +781,7 @@ LossDiagnostics ppo_loss(const CurrentPolicy& net, const advantage::PpoBatch& ba
       src_pol.logits = net.logits;
       src_pol.values = net.values;
     } else {
-      full_logits.upload(static_cast<const unsigned char*>(net.logits), nr * P * V * lb);
+      full_logits.upload(static_cast<const unsigned char*>(net.logits), nr * P * pb);
       src_pol.logits = full_logits.get();
       if (net.values) {
         full_values.upload(net.values, nr * NV);
@@ -854,13 +857,14 @@ LossDiagnostics grpo_loss(const CurrentPolicy& net, const advantage::GrpoBatch& 
     if (g >= batch.groups.size()) throw LengthMismatch("grpo_loss: group index out of range");
   const Observation probe = E && Tc ? d.slab->records[0][0].obs : Observation{};
   const int V = vocab_of(net, probe);
-  const int lb = net.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4;
+  const std::size_t pb = net.logits_dtype == CKRL_DTYPE_TOKEN_ROWS ? sizeof(ckrl_token_row)
+                         : static_cast<std::size_t>(V) * (net.logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
   DevBuf<unsigned char> logits;
   const void* lp = net.logits;
   if (!net.logits || !net.device) {
-    logits.alloc(nr * P * V * lb);
+    logits.alloc(nr * P * pb);
     if (net.logits) {
-      cuda_check(cudaMemcpy(logits.get(), net.logits, nr * P * V * lb, cudaMemcpyHostToDevice));
+      cuda_check(cudaMemcpy(logits.get(), net.logits, nr * P * pb, cudaMemcpyHostToDevice));
     } else {
       if (net.logits_dtype != CKRL_DTYPE_F32) throw ConfigError("forward_logits fills f32 logits");
       std::vector<float> hl(nr * P * V, 0.0f);  // unselected envs never reach the loss

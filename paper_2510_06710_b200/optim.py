@@ -227,9 +227,13 @@ class Pipelined:
     current stream (graph-capturable); batch i uses steps[i % len(steps)] and
     args_of(i) -> (assemble args, loss args)."""
 
-    def __init__(self, steps):
+    def __init__(self, steps, loss_streams: int = 2):
+        """loss_streams = 2 alternates the losses between the current stream and a second one,
+        so batch i+1's loss depends only on its own assembly (not on batch i's loss): its CTAs
+        start and run their unit phases while batch i's last CTAs finish."""
         import torch
         self.steps = steps
+        self.alt = torch.cuda.Stream() if loss_streams > 1 else None
         # across ranks the exchange holds two batches in flight: an assembly may only start
         # once the loss two batches back has completed (ckrl.h, ckrl_ppo_step_assemble)
         self.multi_rank = any(getattr(st, "comm", None) is not None and st.comm.world > 1 for st in steps)
@@ -254,6 +258,8 @@ class Pipelined:
             self.steps[j % n].assemble(*a_args, stream=side)
             self.ev_asm[j % n].record(side)
 
+        if self.alt is not None:
+            self.alt.wait_stream(main)
         with torch.cuda.stream(side):
             asm(0)
         for i in range(K):
@@ -261,14 +267,18 @@ class Pipelined:
                 with torch.cuda.stream(side):
                     asm(i + 1)
             _, l_args = args_of(i)
-            main.wait_event(self.ev_asm[i % n])
+            ls = self.alt if (self.alt is not None and i % 2 == 1) else main
+            ls.wait_event(self.ev_asm[i % n])
             if loss_events is not None:  # (start, end) timing events around each loss launch
-                loss_events[i][0].record(main)
-            self.steps[i % n].loss(*l_args, stream=main)
+                loss_events[i][0].record(ls)
+            with torch.cuda.stream(ls):
+                self.steps[i % n].loss(*l_args, stream=ls)
             if loss_events is not None:
-                loss_events[i][1].record(main)
-            self.ev_loss[i % n].record(main)
+                loss_events[i][1].record(ls)
+            self.ev_loss[i % n].record(ls)
         main.wait_stream(side)
+        if self.alt is not None:
+            main.wait_stream(self.alt)
 
 
 class AdamParamsC(C.Structure):

@@ -632,6 +632,31 @@ TEST_CASE("minibatch: record order does not change the loss; subsets normalise b
   LossDiagnostics v2 = ppo_loss(cur.current(), ab, fwd, p);
   CHECK_APPROX(v1.loss, v2.loss, 1e-6);
   CHECK(v1.units == v2.units);
+  // the same policy as finished token rows (the tensor-core head's output format)
+  std::vector<ckrl_token_row> rows;
+  for (const auto& rec : slab.records[0]) {
+    std::vector<int> prefix;
+    for (int j = 0; j < 2; ++j)
+      for (int m = 0; m < 2; ++m) {
+        std::vector<double> l;
+        for (double x : cur.logits(rec.obs, prefix)) l.push_back((float)x);  // as the f32 view
+        double mx = l[0], s = 0.0, h = 0.0;
+        for (double x : l) mx = std::max(mx, x);
+        for (double x : l) s += std::exp(x - mx);
+        const double lse = mx + std::log(s);
+        for (double x : l) h -= std::exp(x - lse) * (x - lse);
+        const int tok = rec.chunk.actions[j].tokens[m];
+        rows.push_back(ckrl_token_row{l[tok] - lse, (float)h, 0u});
+        prefix.push_back(tok);
+      }
+  }
+  CurrentPolicy rview = view;
+  rview.logits = rows.data();
+  rview.logits_dtype = CKRL_DTYPE_TOKEN_ROWS;
+  LossDiagnostics v3 = ppo_loss(rview, ab, fwd, p);
+  CHECK_APPROX(v3.loss, v1.loss, 1e-6);
+  CHECK_APPROX(v3.entropy, v1.entropy, 1e-6);
+  CHECK(v3.units == v1.units);
 }
 
 TEST_CASE("errors keep the reference's types") {
