@@ -443,7 +443,7 @@ def main():
                              PpoParams(0.2, 0.5, 0.01, True), comm=comm)
         run0 = lambda i: step(reps[i % R][0], reps[i % R][1])  # noqa: E731
         launches_per_step = 2
-        if args.pipeline and args.grad is None:
+        if args.pipeline and args.grad != "separate":
             # batch i+1's assembly (side stream) overlaps batch i's loss: one step object per
             # replica (its own workspace / batch buffers), the public two-halves API
             steps = [step] + [optim.PpoStep(reps[r][0], GaeParams(0.99, 0.95), spec,
@@ -454,13 +454,14 @@ def main():
         step = optim.GrpoStep(reps[0][0], opts, GrpoParams(0.2), comm=comm)
         run0 = lambda i: step(reps[i % R][0], reps[i % R][2], reps[i % R][1])  # noqa: E731
         launches_per_step = 3
-        if args.pipeline and args.grad is None:
+        if args.pipeline and args.grad != "separate":
             steps = [step] + [optim.GrpoStep(reps[r][0], opts, GrpoParams(0.2), comm=comm) for r in range(1, R)]
             pipe = optim.Pipelined(steps, loss_streams=args.loss_streams)
     run = run0
     if args.grad == "fused":  # dlogits written by the loss launch itself (LossOutputs.dlogits)
-        step.outputs.dlogits = torch.empty_like(reps[0][1].logits)
-        step._oc = step.outputs.c()
+        for st in (pipe.steps if pipe is not None else [step]):  # one dlogits buffer per in-flight batch
+            st.outputs.dlogits = torch.empty_like(reps[0][1].logits)
+            st._oc = st.outputs.c()
     if args.grad == "separate":  # + dlogits for the model backward (policy_net.cpp:431-456)
         from paper_2510_06710_b200 import policy as ckpolicy
         dlogits = torch.empty_like(reps[0][1].logits)
