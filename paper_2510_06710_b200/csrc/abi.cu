@@ -578,22 +578,56 @@ static int chain_enabled() {
   return n;
 }
 
-// Whether a pipelined loss launches as a programmatic dependent (CKRL_CHAIN: 0 never, 1 always,
-// 2 = by size, the default). By size: launches of < 8 or > 64 56-KB tiles per SM chain; in
-// between they launch normally. Measured with two alternating loss streams (optim.Pipelined):
-// cfg1 (4 tiles/SM) 14.7 -> 13.7 us and cfg4 (221) 296 -> 284 us with chaining, cfg3 (17)
-// 34.6 -> 33.1 us and cfg2 (17, GRPO) 37.4 -> 32.9 us without — the early-launched CTAs hold
-// SMs the next batch's assembly (GRPO: a 160 KB-smem group kernel) then waits for.
-static bool chain_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
-  const int mode = chain_enabled();
-  if (mode == 0 || po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS) return false;
-  if (mode == 1) return true;
-  const double bytes = (double)ro->num_envs * ro->num_chunks * ro->chunk_len * ro->tokens_per_action *
-                       ro->vocab * (po->logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
+// Launch policy of the pipelined halves' losses (ckrl_*_step_loss; the callers alternate them
+// over two streams, optim.Pipelined). Measured per step on B200:
+//  * grid cap: consecutive losses run side by side on disjoint SMs when each leaves SMs free.
+//    PPO launches of <= 32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 30.1 us, cfg1
+//    14.7 -> 12.7 us, cfg3 bf16 27.2 -> 24.4 us); GRPO losses leave 6 SMs free, where the next
+//    batch's single-CTA group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
+//    long PPO launches keep one CTA per SM.
+//  * chaining (programmatic dependent launch of the previous loss on the stream): on, except
+//    uncapped launches of 8..64 tiles per SM (there the early-launched CTAs hold the SMs the
+//    next assembly needs).
+// CKRL_LOSS_CTAS overrides the cap (0 = one CTA per SM, N = N CTAs), CKRL_CHAIN the chaining
+// (0 never, 1 always, 2 = policy, the default).
+static int loss_cta_knob() {
+  static int n = -2;
+  if (n == -2) {
+    const char* env = getenv("CKRL_LOSS_CTAS");
+    n = env ? atoi(env) : -1;  // -1: policy
+  }
+  return n;
+}
+static int device_sm_count() {
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const double per_sm = bytes / (56.0 * 1024) / (sms > 0 ? sms : 148);
+  return sms > 0 ? sms : 148;
+}
+static double tiles_per_sm(const ckrl_rollout* ro, const ckrl_policy_outputs* po) {
+  const double bytes = (double)ro->num_envs * ro->num_chunks * ro->chunk_len * ro->tokens_per_action *
+                       ro->vocab * (po->logits_dtype == CKRL_DTYPE_BF16 ? 2 : 4);
+  return bytes / (56.0 * 1024) / device_sm_count();
+}
+// cap: the communicator's cap (several ranks on one device) or 0
+static int pipelined_cap(const ckrl_rollout* ro, const ckrl_policy_outputs* po, bool grpo, int cap) {
+  const int k = loss_cta_knob();
+  int want = 0;
+  if (k >= 0) {
+    want = k;
+  } else if (po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS) {
+    const int sms = device_sm_count();
+    if (grpo) want = sms - 6;
+    else if (tiles_per_sm(ro, po) <= 32.0) want = (sms * 3) / 5;
+  }
+  if (want <= 0) return cap;
+  return (cap == 0 || want < cap) ? want : cap;
+}
+static bool chain_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po, bool capped) {
+  const int mode = chain_enabled();
+  if (mode == 0 || po->logits_dtype == CKRL_DTYPE_TOKEN_ROWS) return false;
+  if (mode == 1 || capped) return true;
+  const double per_sm = tiles_per_sm(ro, po);
   return per_sm < 8.0 || per_sm > 64.0;
 }
 
@@ -855,8 +889,9 @@ int32_t ckrl_ppo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* po
   LossArgs a = ppo_args(ro, b, po, spec, p, out, diag, ws, 1,
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1);
   a.ex = exchange_view(comm);
-  a.max_ctas = loss_cta_cap(comm);
-  if (chain_loss(ro, po)) {
+  const int comm_cap = loss_cta_cap(comm);
+  a.max_ctas = pipelined_cap(ro, po, false, comm_cap);
+  if (chain_loss(ro, po, a.max_ctas != comm_cap)) {
     a.pdl = 1;
     a.ro = *ro;
   }
@@ -897,8 +932,9 @@ int32_t ckrl_grpo_step_loss(const ckrl_rollout* ro, const ckrl_policy_outputs* p
   WsLayout L = ws_layout(ro->num_envs, world);
   return grpo_loss_impl(ro, gb, po, spec, p, out, diag, ws, 1,
                         reinterpret_cast<const StatsRecord*>((char*)ws + L.stats_local), 1,
-                        (cudaStream_t)stream, chain_loss(ro, po),
-                        exchange_view(comm), loss_cta_cap(comm));
+                        (cudaStream_t)stream,
+                        chain_loss(ro, po, pipelined_cap(ro, po, true, loss_cta_cap(comm)) != loss_cta_cap(comm)),
+                        exchange_view(comm), pipelined_cap(ro, po, true, loss_cta_cap(comm)));
 }
 
 int32_t ckrl_read_diagnostics(const double* diag_device, double* diag_host, ckrl_stream_t stream) {

@@ -51,6 +51,15 @@ def rounded(d):
     return r
 
 
+def assert_diag_close(got, want, what, rel=1e-11):
+    assert got.keys() == want.keys(), what
+    for k in want:
+        if k == "units":
+            assert got[k] == want[k], (what, k)
+        else:
+            assert abs(got[k] - want[k]) <= rel * max(abs(want[k]), 1e-300) + 1e-18, (what, k, got[k], want[k])
+
+
 def case(cfg_name, envs, seed=11):
     cfg = synth.SynthConfig(**{**synth.CONFIGS[cfg_name].__dict__, "num_envs": envs, "seed": seed})
     d = synth.episodes_numpy(cfg)
@@ -302,7 +311,9 @@ def test_pipelined_batches_match_plain_steps(world):
         for rep in range(R):
             last = max(i for i in range(n_batches) if i % R == rep)
             got = pipes[r].steps[rep].diagnostics()
-            assert got == want[last][r], (r, rep)
+            # the pipelined losses may run on fewer CTAs (launch policy, csrc/abi.cu): the same
+            # sums in another CTA grouping, so the fp64 diagnostics agree to rounding
+            assert_diag_close(got, want[last][r], (r, rep))
             assert torch.equal(pipes[r].steps[rep].batch.counted, plain[r][rep].batch.counted)
     for c in comms:
         if c is not None:
@@ -359,7 +370,7 @@ def test_pipelined_graph_matches_plain_steps(algo):
         torch.cuda.synchronize()
         for rep in range(R):
             last = max(i for i in range(n_batches) if i % R == rep)
-            assert pipe.steps[rep].diagnostics() == want[last], rep
+            assert_diag_close(pipe.steps[rep].diagnostics(), want[last], rep)
             if algo == "ppo":
                 assert torch.equal(pipe.steps[rep].batch.counted, plain[rep].batch.counted)
             else:
