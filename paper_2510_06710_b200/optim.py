@@ -228,12 +228,13 @@ class Pipelined:
     args_of(i) -> (assemble args, loss args)."""
 
     def __init__(self, steps, loss_streams: int = 2):
-        """loss_streams = 2 alternates the losses between the current stream and a second one,
-        so batch i+1's loss depends only on its own assembly (not on batch i's loss): its CTAs
-        start and run their unit phases while batch i's last CTAs finish."""
+        """loss_streams = n > 1 rotates the losses over the current stream and n - 1 more, so
+        batch i+1's loss depends only on its own assembly (not on batch i's loss): its CTAs
+        start and run their unit phases while batch i's last CTAs finish (with the library's
+        capped loss grids, side by side on disjoint SMs)."""
         import torch
         self.steps = steps
-        self.alt = torch.cuda.Stream() if loss_streams > 1 else None
+        self.alts = [torch.cuda.Stream() for _ in range(max(1, loss_streams) - 1)]
         # across ranks the exchange holds two batches in flight: an assembly may only start
         # once the loss two batches back has completed (ckrl.h, ckrl_ppo_step_assemble)
         self.multi_rank = any(getattr(st, "comm", None) is not None and st.comm.world > 1 for st in steps)
@@ -258,8 +259,8 @@ class Pipelined:
             self.steps[j % n].assemble(*a_args, stream=side)
             self.ev_asm[j % n].record(side)
 
-        if self.alt is not None:
-            self.alt.wait_stream(main)
+        for st in self.alts:
+            st.wait_stream(main)
         with torch.cuda.stream(side):
             asm(0)
         for i in range(K):
@@ -267,7 +268,8 @@ class Pipelined:
                 with torch.cuda.stream(side):
                     asm(i + 1)
             _, l_args = args_of(i)
-            ls = self.alt if (self.alt is not None and i % 2 == 1) else main
+            q = i % (len(self.alts) + 1)
+            ls = main if q == 0 else self.alts[q - 1]
             ls.wait_event(self.ev_asm[i % n])
             if loss_events is not None:  # (start, end) timing events around each loss launch
                 loss_events[i][0].record(ls)
@@ -277,8 +279,8 @@ class Pipelined:
                 loss_events[i][1].record(ls)
             self.ev_loss[i % n].record(ls)
         main.wait_stream(side)
-        if self.alt is not None:
-            main.wait_stream(self.alt)
+        for st in self.alts:
+            main.wait_stream(st)
 
 
 class AdamParamsC(C.Structure):
