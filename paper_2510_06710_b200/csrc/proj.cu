@@ -38,8 +38,14 @@ namespace {
 constexpr int kPM = 128;  // positions per tile (UMMA M; TMEM lanes)
 constexpr int kPN = 256;  // bins (UMMA N; TMEM columns per accumulator)
 constexpr int kPK = 64;   // K per stage: one 128-byte swizzle atom of bf16
-constexpr int kStA = 7;  // feature stages (16 KB): the HBM stream, deeper in flight
-constexpr int kStB = 3;  // W_pol stages (32 KB): served from L2
+#ifndef CKRL_PROJ_STA
+#define CKRL_PROJ_STA 7
+#endif
+#ifndef CKRL_PROJ_STB
+#define CKRL_PROJ_STB 3
+#endif
+constexpr int kStA = CKRL_PROJ_STA;  // feature stages (16 KB): the HBM stream, deeper in flight
+constexpr int kStB = CKRL_PROJ_STB;  // W_pol stages (32 KB): served from L2
 constexpr uint32_t kABytes = kPM * kPK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kPN * kPK * 2;  // 32 KB
 constexpr int kProjThreads = 352;            // A producer, MMA, 8 epilogue warps, B producer
