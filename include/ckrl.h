@@ -494,10 +494,10 @@ typedef struct {
 enum { CKRL_SAMPLER_REFERENCE = 0, CKRL_SAMPLER_PARALLEL = 1 };
 
 /* RolloutSpec (placement/rollout.hpp:16-22) + pipeline depth k (PlacementPlan::pipeline_stage_num)
- * + placement. gen_device < 0: colocated (PlacementMode::Colocated, plan.cpp:60-68): env and
- * generation kernels share the calling device. gen_device >= 0: the generation role runs on
- * that device (hybrid / disaggregated placement; it may equal the env device, which keeps the
- * hand-offs): every chunk the stage's observation batch is copied env -> gen and its action
+ * + placement. placed = 0 (a zero-initialised spec): colocated (PlacementMode::Colocated,
+ * plan.cpp:60-68): env and generation kernels share the calling device. placed = 1: the
+ * generation role runs on gen_device (hybrid / disaggregated placement; it may equal the env
+ * device, which keeps the hand-offs): every chunk the stage's observation batch is copied env -> gen and its action
  * batch (tokens, log-probs, values, optional logits) gen -> env over NVLink peer copies, the
  * reference's obs / act channels (real_backend.cpp:15-37, 59-138), with per-stage events on
  * both devices. The slab is bit-identical across k and placement. */
@@ -509,8 +509,9 @@ typedef struct {
   uint64_t sample_seed;
   const int32_t* reset_state_ids; /* [num_envs] device, or NULL */
   int32_t sampler;                /* CKRL_SAMPLER_* */
-  int32_t gen_device;             /* -1 colocated; else the generation device */
-  void* gen_workspace;            /* gen_device >= 0: ckrl_pipeline_gen_workspace_bytes on gen_device */
+  int32_t placed;                 /* 0 colocated, 1 generation on gen_device */
+  int32_t gen_device;             /* placed: the generation device */
+  void* gen_workspace;            /* placed: ckrl_pipeline_gen_workspace_bytes on gen_device */
   size_t gen_workspace_bytes;
 } ckrl_pipeline_spec;
 
@@ -553,7 +554,7 @@ typedef struct {
 
 int64_t ckrl_policy_num_params(const ckrl_policy_desc* desc);
 size_t ckrl_pipeline_workspace_bytes(const ckrl_pipeline_spec* spec);
-/* Generation-side scratch for gen_device >= 0 (policy copy, sampling streams, obs / action
+/* Generation-side scratch of a placed pipeline (policy copy, sampling streams, obs / action
  * staging), allocated by the caller on gen_device. */
 size_t ckrl_pipeline_gen_workspace_bytes(const ckrl_pipeline_spec* spec);
 /* One rollout epoch (StageSim / StageGen / merge_stages, placement/rollout.cpp:11-109;

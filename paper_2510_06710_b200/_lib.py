@@ -104,7 +104,7 @@ PLACEMENT_COLOCATED, PLACEMENT_DISAGGREGATED, PLACEMENT_HYBRID = 0, 1, 2
 class PipelineSpec(C.Structure):
     _fields_ = [("env", EnvConfig), ("policy", PolicyDesc), ("num_chunks", C.c_int32),
                 ("stages", C.c_int32), ("sample_seed", C.c_uint64), ("reset_state_ids", vp),
-                ("sampler", C.c_int32), ("gen_device", C.c_int32), ("gen_workspace", vp),
+                ("sampler", C.c_int32), ("placed", C.c_int32), ("gen_device", C.c_int32), ("gen_workspace", vp),
                 ("gen_workspace_bytes", C.c_size_t)]
 
 

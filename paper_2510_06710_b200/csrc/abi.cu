@@ -1126,10 +1126,10 @@ int32_t ckrl_pipeline_run(const ckrl_pipeline_spec* sp, const double* params,
   if ((st = check_device())) return st;
   CKRL_REQUIRE(params && out && ws, CKRL_ERR_INVALID_ARGUMENT, "params / outputs / workspace required");
   CKRL_REQUIRE(ws_bytes >= pipeline_ws_bytes(*sp), CKRL_ERR_INVALID_ARGUMENT, "pipeline workspace too small");
-  if (sp->gen_device >= 0) {
+  if (sp->placed) {
     int n = 0;
     cudaGetDeviceCount(&n);
-    CKRL_REQUIRE(sp->gen_device < n, CKRL_ERR_INVALID_ARGUMENT, "gen_device out of range");
+    CKRL_REQUIRE(sp->gen_device >= 0 && sp->gen_device < n, CKRL_ERR_INVALID_ARGUMENT, "gen_device out of range");
     CKRL_REQUIRE(sp->gen_workspace && sp->gen_workspace_bytes >= pipeline_gen_ws_bytes(*sp),
                  CKRL_ERR_INVALID_ARGUMENT, "generation workspace missing or too small");
   }

@@ -863,7 +863,7 @@ size_t pipeline_ws_layout(const ckrl_pipeline_spec& sp, EnvState* st, double** p
 size_t staging_bytes(const ckrl_pipeline_spec& sp);
 size_t pipeline_ws_bytes(const ckrl_pipeline_spec& sp) {
   size_t n = pipeline_ws_layout(sp, nullptr, nullptr, nullptr);
-  if (sp.gen_device >= 0) n += staging_bytes(sp);  // the env side's receive buffers
+  if (sp.placed) n += staging_bytes(sp);  // the env side's receive buffers
   return n;
 }
 int64_t policy_num_params(const ckrl_policy_desc& d) { return make_layout(d).total; }
@@ -984,7 +984,7 @@ static cudaError_t set_kernel_smem(size_t gen_smem, size_t boot_smem) {
 // [s*E/k, (s+1)*E/k) (rollout.cpp:11-17) and runs Reset -> (Gen(t) -> Sim(t)) x T.
 //   colocated: stage s on its own stream of the calling device; the k stage streams run
 //     concurrently, so stage s's env step overlaps stage s'’s policy inference.
-//   placed (gen_device >= 0): the generation role on gen_device with its own policy copy and
+//   placed (spec.placed): the generation role on gen_device with its own policy copy and
 //     sampling streams; per chunk the env stream sends the stage's obs rows (peer copy) and
 //     records obs_ev[s], the gen stream waits it, samples, sends the action rows back and
 //     records done(gen)[s], which the env stream waits before scattering them into the slab
@@ -1040,7 +1040,7 @@ cudaError_t pipeline_run(const ckrl_pipeline_spec& sp, const double* params, ckr
   int env_dev = 0;
   cudaError_t err = cudaGetDevice(&env_dev);
   if (err) return err;
-  const bool placed = sp.gen_device >= 0;
+  const bool placed = sp.placed;
   const int gen_dev = placed ? sp.gen_device : env_dev;
   if ((err = set_kernel_smem(gen_smem, boot_smem))) return err;
   cudaMemsetAsync(out.status, 0, sizeof(int32_t), stream);

@@ -134,8 +134,8 @@ class RolloutPipeline:
         self.reset_ids = (None if reset_state_ids is None else
                           torch.as_tensor(reset_state_ids, dtype=torch.int32).to(self.device))
         self.spec = _lib.PipelineSpec(env.c(), policy.c(), num_chunks, stages, sample_seed,
-                                      _ptr(self.reset_ids), int(sampler),
-                                      -1 if gen_device is None else int(gen_device), None, 0)
+                                      _ptr(self.reset_ids), int(sampler), int(gen_device is not None),
+                                      0 if gen_device is None else int(gen_device), None, 0)
         self._lib = _lib.lib()
         nbytes = int(self._lib.ckrl_pipeline_workspace_bytes(C.byref(self.spec)))
         if nbytes == 0:  # invalid spec: re-run validation to raise the reference's exception

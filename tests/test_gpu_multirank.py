@@ -375,3 +375,55 @@ def test_pipelined_graph_matches_plain_steps(algo):
                 assert torch.equal(pipe.steps[rep].batch.counted, plain[rep].batch.counted)
             else:
                 assert torch.equal(pipe.steps[rep].batch.env_group, plain[rep].batch.env_group)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_grpo_step_key_sharded_ranks_match_full_batch(world, oracle):
+    """GroupKeys merged across non-adjacent envs (reset ids drawn with replacement,
+    train.cpp:92-101), sharded by key (dist.key_shard: every key on one rank, non-contiguous env
+    sets): the K ranks' CUDA steps, exchanging only the retained-group count and the raw loss
+    sums, report the full batch's diagnostics; each rank's weights equal the oracle's rows."""
+    from test_multirank import gather_envs
+    from paper_2510_06710_b200.dist import key_shard
+    cfg, d, logits = case("cfg2", 48, seed=17)
+    rng = np.random.default_rng(17)
+    ids = rng.integers(0, 9, cfg.num_envs).astype(d["ep_reset_id"].dtype)
+    d["ep_reset_id"] = ids[d["ep_env_id"]]
+    a, l, v = synth.SPECS["cfg2"]
+    spec = GranularitySpec(Level(a), Level(l), Level(v))
+    first = {}
+    for e, t, rid in zip(d["ep_env_id"], d["ep_task"], d["ep_reset_id"]):
+        first.setdefault(int(e), (int(t), int(rid)))
+    parts = key_shard([first[e] for e in range(cfg.num_envs)], world)
+    assert any(np.any(np.diff(p) > 1) for p in parts)
+    comms = Comm.local_group(world)
+    steps, calls = [], []
+    lg = logits.cpu()
+    for r in range(world):
+        s = gather_envs(d, parts[r])
+        ro = RolloutBuffer.from_arrays(s, s["boot_scalar"], cfg.vocab)
+        ept = EpisodeTable.from_arrays(s)
+        pol = PolicyOutputs(lg[torch.as_tensor(parts[r])].contiguous().cuda())
+        st = optim.GrpoStep(ro, GrpoAssemblyOptions(spec), GrpoParams(0.2), comm=comms[r])
+        steps.append(st)
+        calls.append(lambda stream, st=st, ro=ro, ept=ept, pol=pol: st(ro, ept, pol, stream=stream))
+    runs = run_ranks(steps, calls, 2)
+    r = rounded({**d, "logits": logits.cpu().numpy()})
+    st0, asm = oracle.assemble_grpo(r, (a, l, v))
+    assert st0 == 0 and asm["groups_retained"] > 1
+    _, want, coeff = oracle.grpo_loss(r, l, asm, r["logits"], 0.2)
+    for it, diags in enumerate(runs):
+        vecs = [np.array([dd[k] for k in DIAG]) for dd in diags]
+        for q in range(1, world):
+            np.testing.assert_array_equal(vecs[q], vecs[0], err_msg=f"rank {q} iter {it}")
+        assert vecs[0][6] == want[6]
+        # a signed sum of cancelling group terms, summed per rank then across ranks: 1e-5 of
+        # the terms' L1 mass (sum |coeff_lp| at this lp level)
+        mass = float(np.abs(coeff).sum())
+        assert_close(vecs[0][:2], want[:2], TOL, f"grpo keys world={world} loss", floor=mass)
+        assert_close(vecs[0][2:6], want[2:6], TOL, f"grpo keys world={world} diag")
+    for st, envs in zip(steps, parts):
+        np.testing.assert_array_equal(st.batch.slot_weight.cpu().numpy(), asm["slot_weight"][envs])
+        np.testing.assert_array_equal(st.batch.env_advantage.cpu().numpy(), asm["env_adv"][envs])
+    for c in comms:
+        c.close()
