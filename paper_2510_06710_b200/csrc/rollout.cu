@@ -331,6 +331,22 @@ __device__ __forceinline__ double madd(double s, double a, double b) { return __
 // consecutive rows, so every weight load is coalesced.
 __device__ void matvec_t(const double* WT, const double* bias, int rows, int cols, const double* in,
                          double* out, bool tanh_act, int tid, int nth) {
+  if (cols == 32) {  // the common width: every load issued before the (unchanged) sum chain
+    for (int r = tid; r < rows; r += nth) {
+      double wv[32], iv[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        wv[c] = __ldg(WT + (int64_t)c * rows + r);
+        iv[c] = in[c];
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) s = madd(s, wv[c], iv[c]);
+      const double v = bias ? __dadd_rn(s, __ldg(bias + r)) : s;
+      out[r] = tanh_act ? tanh(v) : v;
+    }
+    return;
+  }
   for (int r = tid; r < rows; r += nth) {
     double s = 0.0;
 #pragma unroll 8
@@ -353,8 +369,19 @@ __device__ void matvec_split(const double* WT, const double* bias, int rows, int
     const int r = rb + tid / G;
     double s = 0.0;
     if (r < rows) {
+      if (c1 - c0 == 8) {  // H = 32: the quarter's loads issued before its sum chain
+        double wv[8], iv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          wv[c] = __ldg(WT + (int64_t)(c0 + c) * rows + r);
+          iv[c] = in[c0 + c];
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s = madd(s, wv[c], iv[c]);
+      } else {
 #pragma unroll 4
-      for (int c = c0; c < c1; ++c) s = madd(s, __ldg(WT + (int64_t)c * rows + r), in[c]);
+        for (int c = c0; c < c1; ++c) s = madd(s, __ldg(WT + (int64_t)c * rows + r), in[c]);
+      }
     }
     s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
     s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
@@ -517,8 +544,14 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
   double* s_sum = w.ex;
   double* s_scan = w.ex + 4;
   int* s_min = reinterpret_cast<int*>(w.ex + 8);
+  constexpr int kQ = 8;
+  double ex[kQ];  // exp(l_v - max) of this thread's bins (up to 8 kept in registers)
   double part = 0.0;
-  for (int v = v0; v < v1; ++v) part = __dadd_rn(part, exp(__dsub_rn(w.lg[v], mx)));
+  for (int v = v0; v < v1; ++v) {
+    const double e = exp(__dsub_rn(w.lg[v], mx));
+    if (v - v0 < kQ) ex[v - v0] = e;
+    part = __dadd_rn(part, e);
+  }
   double tot = part;
 #pragma unroll
   for (int o = 16; o; o >>= 1) tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, o));
@@ -526,12 +559,13 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
   __syncthreads();
   const double sum = __dadd_rn(__dadd_rn(s_sum[0], s_sum[1]), __dadd_rn(s_sum[2], s_sum[3]));
   const double lse = __dadd_rn(mx, log(sum));
-  // probabilities (kept in registers for up to 8 bins per thread) and this thread's inclusive sum
-  constexpr int kQ = 8;
+  // probabilities exp(l - max) / sum (one division, no second exp) and this thread's inclusive
+  // sum; bins beyond the register block (V > 1024) recompute exp(l - lse)
+  const double inv = 1.0 / sum;
   double pv[kQ];
   double acc = 0.0;
   for (int v = v0; v < v1; ++v) {
-    const double p = exp(__dsub_rn(w.lg[v], lse));
+    const double p = v - v0 < kQ ? ex[v - v0] * inv : exp(__dsub_rn(w.lg[v], lse));
     if (v - v0 < kQ) pv[v - v0] = p;
     acc = __dadd_rn(acc, p);
   }
@@ -580,6 +614,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
   const int64_t rec = gen_rec(go, e, t);
   const bool par = a.sampler == CKRL_SAMPLER_PARALLEL;
   uint64_t rng = (tid == 0 || par) ? a.gsamp[e] : 0;  // parallel: every thread draws the same u
+  // H <= threads (one hidden unit per thread): the embedding row of the token just drawn is
+  // loaded into a register and consumed only in the next position's trunk input, after the
+  // token-independent part (W_in obs + b_in + pos_bias), so its latency overlaps that work;
+  // the additions keep the reference's order
+  const bool reg_emb = L.H <= kGenThreads;
+  double e_new = 0.0, e_run = 0.0;  // (reg_emb, thread hh = tid) latest row / parallel running sum
   for (int pos = 0; pos < L.P; ++pos) {
     // trunk input (policy_net.cpp:197-212): W_in obs + (b_in + pos_bias) + sum_k emb[k][tok_k]
     for (int hh = tid; hh < L.H; hh += kGenThreads) {
@@ -587,7 +627,21 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
       for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
       s = __dadd_rn(s, __dadd_rn(__ldg(p + L.b_in + hh), __ldg(p + L.pos_bias + (int64_t)pos * L.H + hh)));
       if (par) {  // the prefix's embeddings as one running sum
-        if (pos > 0) s = __dadd_rn(s, w.embc[hh]);
+        if (reg_emb) {
+          if (pos > 0) {
+            e_run = pos == 1 ? e_new : __dadd_rn(e_run, e_new);
+            s = __dadd_rn(s, e_run);
+          }
+        } else if (pos > 0) {
+          s = __dadd_rn(s, w.embc[hh]);
+        }
+      } else if (reg_emb) {
+#pragma unroll 8
+        for (int k = 0; k + 1 < pos; ++k) s = __dadd_rn(s, w.embc[k * L.H + hh]);
+        if (pos > 0) {
+          s = __dadd_rn(s, e_new);
+          w.embc[(pos - 1) * L.H + hh] = e_new;  // for the later positions' sums
+        }
       } else {
 #pragma unroll 8
         for (int k = 0; k < pos; ++k) s = __dadd_rn(s, w.embc[k * L.H + hh]);
@@ -626,10 +680,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
         go.lp[k] = (float)lp;
         go.lp64[k] = lp;
       }
-      // every thread holds the token: the running embedding sum of the prefix (row 0 of the
-      // cache) is updated by the thread that reads it in the next trunk input
-      for (int hh = tid; hh < L.H; hh += kGenThreads)
-        w.embc[hh] = __dadd_rn(pos == 0 ? 0.0 : w.embc[hh], __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh));
+      // every thread holds the token: the running embedding sum of the prefix (a register, or
+      // row 0 of the cache) is updated by the thread that reads it in the next trunk input
+      if (reg_emb) {
+        if (tid < L.H) e_new = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + tid);
+      } else {
+        for (int hh = tid; hh < L.H; hh += kGenThreads)
+          w.embc[hh] = __dadd_rn(pos == 0 ? 0.0 : w.embc[hh], __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh));
+      }
       continue;
     }
     // log_softmax (policy_net.cpp:90-102): exps in parallel, the sum in v order on thread 0
@@ -688,9 +746,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
     }
     __syncthreads();
     const int tok = w.prefix[pos];
-    for (int hh = tid; hh < L.H; hh += kGenThreads)
-      w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
-    // the next position's trunk input reads embc[pos][hh] from the same thread
+    if (reg_emb) {
+      if (tid < L.H) e_new = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + tid);
+    } else {
+      for (int hh = tid; hh < L.H; hh += kGenThreads)
+        w.embc[pos * L.H + hh] = __ldg(p + L.emb + ((int64_t)pos * L.V + tok) * L.H + hh);
+    }
+    // the next position's trunk input reads embc[pos][hh] / e_new from the same thread
   }
   if (tid == 0) a.gsamp[e] = rng;
   __syncthreads();
