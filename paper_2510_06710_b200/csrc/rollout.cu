@@ -620,12 +620,26 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
   // the additions keep the reference's order
   const bool reg_emb = L.H <= kGenThreads;
   double e_new = 0.0, e_run = 0.0;  // (reg_emb, thread hh = tid) latest row / parallel running sum
+  // (reg_emb) the chunk's W_in obs (the observation is fixed for the whole chunk), b_in and the
+  // next position's pos_bias in registers: the same sums, off the per-position critical path
+  double win_obs = 0.0, b_in = 0.0, pb_next = 0.0;
+  if (reg_emb && tid < L.H) {
+    for (int c = 0; c < L.D; ++c) win_obs = madd(win_obs, __ldg(pk + a.pk.win + (int64_t)c * L.H + tid), obs[c]);
+    b_in = __ldg(p + L.b_in + tid);
+    pb_next = __ldg(p + L.pos_bias + tid);
+  }
   for (int pos = 0; pos < L.P; ++pos) {
     // trunk input (policy_net.cpp:197-212): W_in obs + (b_in + pos_bias) + sum_k emb[k][tok_k]
     for (int hh = tid; hh < L.H; hh += kGenThreads) {
-      double s = 0.0;
-      for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
-      s = __dadd_rn(s, __dadd_rn(__ldg(p + L.b_in + hh), __ldg(p + L.pos_bias + (int64_t)pos * L.H + hh)));
+      double s;
+      if (reg_emb) {
+        s = __dadd_rn(win_obs, __dadd_rn(b_in, pb_next));
+        if (pos + 1 < L.P) pb_next = __ldg(p + L.pos_bias + (int64_t)(pos + 1) * L.H + hh);
+      } else {
+        s = 0.0;
+        for (int c = 0; c < L.D; ++c) s = madd(s, __ldg(pk + a.pk.win + (int64_t)c * L.H + hh), obs[c]);
+        s = __dadd_rn(s, __dadd_rn(__ldg(p + L.b_in + hh), __ldg(p + L.pos_bias + (int64_t)pos * L.H + hh)));
+      }
       if (par) {  // the prefix's embeddings as one running sum
         if (reg_emb) {
           if (pos > 0) {
