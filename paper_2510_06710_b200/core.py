@@ -203,7 +203,11 @@ class PolicyOutputs:
 
     def c(self) -> _lib.PolicyOutputs:
         if self.token_rows is not None:
-            return _lib.PolicyOutputs(_lib.DTYPE_TOKEN_ROWS, _ptr(self.token_rows), _ptr(self.values))
+            t = self.token_rows
+            if t.dtype != torch.float64 or t.shape[-1] != 2 or not t.is_contiguous():
+                raise ValueError("token_rows must be a contiguous float64 [E][Tc][C][M][2] tensor "
+                                 "(one 16-byte ckrl_token_row per position)")
+            return _lib.PolicyOutputs(_lib.DTYPE_TOKEN_ROWS, _ptr(t), _ptr(self.values))
         dt = _lib.DTYPE_BF16 if self.logits.dtype == torch.bfloat16 else _lib.DTYPE_F32
         return _lib.PolicyOutputs(dt, _ptr(self.logits), _ptr(self.values))
 

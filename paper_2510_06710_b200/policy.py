@@ -59,10 +59,19 @@ def project_token_stats(feature: torch.Tensor, w_pol: torch.Tensor, b_pol, token
     w_pol = w_pol.contiguous()
     if feature.dtype != torch.bfloat16 or w_pol.dtype != torch.bfloat16:
         raise TypeError("feature and w_pol must be bfloat16")
+    if w_pol.dim() != 2 or w_pol.shape[1] != H:
+        raise ValueError(f"w_pol must be [vocab, {H}], got {tuple(w_pol.shape)}")
     V = w_pol.shape[0]
+    if tokens.shape != tuple(lead):
+        raise ValueError(f"tokens must have shape {tuple(lead)}, got {tuple(tokens.shape)}")
     b = None if b_pol is None else b_pol.to(device=dev, dtype=torch.float32).contiguous()
+    if b is not None and b.numel() != V:
+        raise ValueError(f"b_pol must have {V} entries")
     if rows_out is None:
         rows_out = torch.empty((*lead, 2), dtype=torch.float64, device=dev)
+    elif (rows_out.dtype != torch.float64 or tuple(rows_out.shape) != (*lead, 2)
+          or not rows_out.is_contiguous() or rows_out.device != dev):
+        raise ValueError("rows_out must be a contiguous float64 [..., 2] tensor on the features' device")
     lp = None if rows_only else torch.empty(tuple(lead), dtype=torch.float64, device=dev)
     ent = None if rows_only else torch.empty(tuple(lead), dtype=torch.float32, device=dev)
     logits = None
