@@ -581,8 +581,8 @@ static int chain_enabled() {
 // Launch policy of the pipelined halves' losses (ckrl_*_step_loss; the callers alternate them
 // over two streams, optim.Pipelined). Measured per step on B200:
 //  * grid cap: consecutive losses run side by side on disjoint SMs when each leaves SMs free.
-//    PPO launches of <= 32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 30.1 us, cfg1
-//    14.7 -> 12.7 us, cfg3 bf16 27.2 -> 24.4 us); GRPO losses leave 6 SMs free, where the next
+//    PPO launches of 8..32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 30.1 us, cfg3
+//    bf16 27.2 -> 24.4 us), below 8 a quarter (cfg1 14.7 -> 12.3 us); GRPO losses leave 6 SMs free, where the next
 //    batch's single-CTA group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
 //    long PPO launches keep one CTA per SM.
 //  * chaining (programmatic dependent launch of the previous loss on the stream): on, except
@@ -617,8 +617,10 @@ static int pipelined_cap(const ckrl_rollout* ro, const ckrl_policy_outputs* po, 
     want = k;
   } else if (po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS) {
     const int sms = device_sm_count();
+    const double t = tiles_per_sm(ro, po);
     if (grpo) want = sms - 6;
-    else if (tiles_per_sm(ro, po) <= 32.0) want = (sms * 3) / 5;
+    else if (t < 8.0) want = sms / 4;  // tiny launches: a quarter (cfg1 12.7 -> 12.3 us)
+    else if (t <= 32.0) want = (sms * 3) / 5;
   }
   if (want <= 0) return cap;
   return (cap == 0 || want < cap) ? want : cap;
