@@ -52,3 +52,16 @@ TEST_CASE("fails") { CHECK(2 + 2 == 5); CHECK_FALSE(true); CHECK(0.1 == doctest:
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 1
     assert "test cases: 3 | 1 failed | assertions: 8 | 3 failed" in r.stdout, r.stdout
+
+
+def test_reference_acceptance_criteria_pass(tmp_path):
+    """proj/tests/acceptance.cpp — the reference's nine acceptance criteria (GAE vs the
+    double-sum oracle, FD gradients, granularity identity, GRPO standardization / exhaustive
+    filter, partial reset, scheduling invariance across placements / k / backends, virtual-clock
+    throughput band, ToyReach learning, chunk_step equivalence) built in place with its harness
+    (oracle/Makefile `acceptance`)."""
+    subprocess.run(["make", "-s", "-j8", "-C", ORACLE, "acceptance"], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(ORACLE, "_ref", "suites", "acceptance")], cwd=tmp_path,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "all 9 acceptance criteria passed" in r.stdout, r.stdout[-3000:]
