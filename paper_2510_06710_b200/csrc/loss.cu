@@ -2027,7 +2027,10 @@ static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int ns
     // 35.2 -> 32.8, cfg1 bf16 21.2 -> 19.4); long launches (cfg4: 221 tiles per SM) and GRPO
     // keep 14 row warps, which the steady-state row throughput needs (cfg4 f32 308 vs 372 us)
     const int64_t per_sm = (a.n_rec + a.rec_per_tile - 1) / a.rec_per_tile / device_sms_cached();
-    variant = (MODE == MODE_PPO && !FUSED && per_sm <= 32) ? 5 : 4;
+    // a capped grid (the pipelined halves' launch policy) leaves SMs free for the assembly, so
+    // the 14-row-warp CTA wins there (cfg3 29.7 -> 26.5 us, cfg1 12.3 -> 10.6 us per step)
+    const bool capped = a.max_ctas > 0 && a.max_ctas < device_sms_cached();
+    variant = (MODE == MODE_PPO && !FUSED && per_sm <= 32 && !capped) ? 5 : 4;
   }
   switch (variant) {
     // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
