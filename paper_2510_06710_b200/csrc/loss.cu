@@ -2030,7 +2030,9 @@ static cudaError_t launch_tma(LossArgs& a, cudaStream_t s, int* grid_out, int ns
     // a capped grid (the pipelined halves' launch policy) leaves SMs free for the assembly, so
     // the 14-row-warp CTA wins there (cfg3 29.7 -> 26.5 us, cfg1 12.3 -> 10.6 us per step)
     const bool capped = a.max_ctas > 0 && a.max_ctas < device_sms_cached();
-    variant = (MODE == MODE_PPO && !FUSED && per_sm <= 32 && !capped) ? 5 : 4;
+    // the 16-warp CTA only where an assembly CTA must share its SM: a programmatic dependent
+    // of its own assembly (ckrl_ppo_step) on a full grid
+    variant = (MODE == MODE_PPO && !FUSED && per_sm <= 32 && !capped && a.pdl) ? 5 : 4;
   }
   switch (variant) {
     // measured on B200 (cfg4 f32): 16x1 reaches the HBM roofline; 8x2 is latency-bound
