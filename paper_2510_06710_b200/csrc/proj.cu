@@ -38,6 +38,12 @@ namespace {
 constexpr int kPM = 128;  // positions per tile (UMMA M; TMEM lanes)
 constexpr int kPN = 256;  // bins (UMMA N; TMEM columns per accumulator)
 constexpr int kPK = 64;   // K per stage: one 128-byte swizzle atom of bf16
+#ifndef CKRL_PROJ_L2PROMO
+#define CKRL_PROJ_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+#ifndef CKRL_PROJ_A_EVICT
+#define CKRL_PROJ_A_EVICT "evict_first"
+#endif
 #ifndef CKRL_PROJ_STA
 #define CKRL_PROJ_STA 7
 #endif
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       const bool is_a = warp == 0;
       uint64_t pol;
       if (is_a)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("createpolicy.fractional.L2::" CKRL_PROJ_A_EVICT ".b64 %0, 1.0;" : "=l"(pol));
       else
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       const int nst = is_a ? kStA : kStB;
@@ -403,7 +409,7 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t outer, int H, int box_row
   cuuint32_t box[2] = {(cuuint32_t)kPK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CKRL_PROJ_L2PROMO,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
