@@ -526,7 +526,11 @@ __device__ void value_heads(const PipeArgs& a, const double* pk, const double* f
   if (BLOCK) __syncthreads(); else __syncwarp();
 }
 
-constexpr int kGenThreads = 128;
+#ifndef CKRL_GEN_THREADS
+#define CKRL_GEN_THREADS 256
+#endif
+constexpr int kGenThreads = CKRL_GEN_THREADS;  // threads per env (a multiple of 32, <= 256)
+constexpr int kGenWarps = kGenThreads / 32;
 
 // CKRL_SAMPLER_PARALLEL: log_softmax's sum of exp(l_v - max) and the inverse-CDF walk of
 // sample_chunk (policy_net.cpp:90-102, 306-316) as block-wide fixed-order reductions: thread i
@@ -542,8 +546,8 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
   // block scratch in w.ex (unused by this sampler): warp sums, warp scan totals, warp minima —
   // distinct slots, so only the three hand-off barriers below are needed
   double* s_sum = w.ex;
-  double* s_scan = w.ex + 4;
-  int* s_min = reinterpret_cast<int*>(w.ex + 8);
+  double* s_scan = w.ex + kGenWarps;
+  int* s_min = reinterpret_cast<int*>(w.ex + 2 * kGenWarps);
   constexpr int kQ = 8;
   double ex[kQ];  // exp(l_v - max) of this thread's bins (up to 8 kept in registers)
   double part = 0.0;
@@ -557,7 +561,9 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
   for (int o = 16; o; o >>= 1) tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, o));
   if (lane == 0) s_sum[warp] = tot;
   __syncthreads();
-  const double sum = __dadd_rn(__dadd_rn(s_sum[0], s_sum[1]), __dadd_rn(s_sum[2], s_sum[3]));
+  double sum = s_sum[0];
+#pragma unroll
+  for (int q2 = 1; q2 < kGenWarps; ++q2) sum = __dadd_rn(sum, s_sum[q2]);
   const double lse = __dadd_rn(mx, log(sum));
   // probabilities exp(l - max) / sum (one division, no second exp) and this thread's inclusive
   // sum; bins beyond the register block (V > 1024) recompute exp(l - lse)
@@ -593,7 +599,9 @@ __device__ int sample_parallel(const PolScratch& w, int V, double mx, double u, 
   for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) s_min[warp] = m;
   __syncthreads();
-  m = min(min(s_min[0], s_min[1]), min(s_min[2], s_min[3]));
+  m = s_min[0];
+#pragma unroll
+  for (int q2 = 1; q2 < kGenWarps; ++q2) m = min(m, s_min[q2]);
   lse_out = lse;
   return m < V ? m : V - 1;
 }
@@ -679,7 +687,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(PipeArgs a, int first,
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) w.red[warp] = mx;
     __syncthreads();
-    mx = fmax(fmax(w.red[0], w.red[1]), fmax(w.red[2], w.red[3]));
+    {
+      double m2 = w.red[0];
+#pragma unroll
+      for (int q2 = 1; q2 < kGenWarps; ++q2) m2 = fmax(m2, w.red[q2]);
+      mx = m2;
+    }
     if (go.logits) {
       float* dst = go.logits + (rec * L.P + pos) * (int64_t)L.V;
       for (int v = tid; v < L.V; v += kGenThreads) dst[v] = (float)w.lg[v];
