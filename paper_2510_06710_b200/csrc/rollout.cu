@@ -534,8 +534,8 @@ constexpr int kGenWarps = kGenThreads / 32;
 
 // CKRL_SAMPLER_PARALLEL: log_softmax's sum of exp(l_v - max) and the inverse-CDF walk of
 // sample_chunk (policy_net.cpp:90-102, 306-316) as block-wide fixed-order reductions: thread i
-// owns the contiguous bins [i*q, (i+1)*q) (q = ceil(V / 128)), sums them in bin order, then a
-// shuffle tree per warp and the 4 warp totals in warp order (the LSE); the CDF is the same
+// owns the contiguous bins [i*q, (i+1)*q) (q = ceil(V / threads)), sums them in bin order, then a
+// shuffle tree per warp and the warp totals in warp order (the LSE); the CDF is the same
 // partition's inclusive scan (own bins serially, warp Kogge-Stone, warp offsets), and the
 // token is the smallest v with u < cdf[v] (V - 1 if none, as the reference). Every thread
 // returns the token; w.red[4] = lse. Deterministic and independent of scheduling.
