@@ -35,3 +35,21 @@ def test_bench_two_ranks_share_gpu():
     assert two["config"]["global_envs"] == 2 * one["config"]["global_envs"]
     # rank-distinct envs: the job-wide diagnostics cover twice the units
     assert two["diagnostics"]["units"] > one["diagnostics"]["units"]
+
+
+def test_bench_head_line():
+    """--head: the step fed from trunk features through the tcgen05 projection (row N2)."""
+    j = run_bench("--config", "cfg3", "--head", "256", "--steps", "5", "--warmup", "3", "--no-cpu-baseline")
+    r = j["roofline"]
+    assert j["config"]["head_hidden"] == 256 and r["kernel"].startswith("proj_stats_kernel")
+    assert 0 < r["tensor_frac"] < 1.2 and 0 < r["hbm_frac"] < 1.2 and r["loss_from_rows_ms_alone"] > 0
+    assert j["diagnostics"]["units"] > 0
+
+
+def test_bench_cfg5_variants():
+    """cfg5: every {placement} x {sampler} x k variant timed, identical slabs are asserted by
+    tests/test_gpu_pipeline.py; here the line's schema."""
+    j = run_bench("--config", "cfg5", "--steps", "2", "--warmup", "3", "--stages", "1,2")
+    keys = set(j["pipeline"])
+    assert {"colocated/reference/k1", "colocated/parallel/k2", "placed/parallel/k1"} <= keys
+    assert j["e2e"]["h2d_bytes_per_step"] > 0 and j["value"] > 0
