@@ -584,7 +584,7 @@ static int chain_enabled() {
 //    PPO launches of 8..32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 26.8 us, cfg3
 //    bf16 27.2 -> 22.6 us, with the 14-row-warp CTA, csrc/loss.cu), below 8 a quarter (cfg1
 //    14.7 -> 10.8 us); GRPO losses leave 6 SMs free, where the next
-//    batch's single-CTA group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
+//    batch's single-CTA (1024-thread) group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
 //    long PPO launches keep one CTA per SM.
 //  * chaining (programmatic dependent launch of the previous loss on the stream): on, except
 //    uncapped launches of 8..64 tiles per SM (there the early-launched CTAs hold the SMs the

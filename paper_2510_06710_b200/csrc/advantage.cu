@@ -5,6 +5,7 @@
 //
 // Reference semantics: advantage/gae.cpp:7-37, advantage/assembler.cpp:33-267,
 // advantage/grpo.cpp:9-79, optim/update.cpp:14-45.
+#include <algorithm>
 #include "common.cuh"
 #include "gae.cuh"
 #include "kernels.h"
@@ -255,7 +256,10 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
   const int n = s_n;
   // up to kGrpoMaxEligible eligible episodes sort in shared memory; beyond, in the workspace's
   // sort region (one eligible episode per env at most: the one starting at step 0)
-  const bool big = n > kGrpoMaxEligible;
+  // the shared-memory arrays are sized for min(kGrpoMaxEligible, pow2 >= E) (launch_grpo_assemble):
+  // small enough at a few hundred envs for the CTA to share an SM with a loss CTA
+  const int scap = min(kGrpoMaxEligible, pow2_at_least(num_envs));
+  const bool big = n > scap;
   if (big && n > num_envs) {
     if (tid == 0) {
       *st = StatsRecord{0.0, 0.0, 0, 0, 0, 0, 0, CKRL_ERR_INVALID_ARGUMENT};
@@ -266,7 +270,7 @@ grpo_group_kernel(ckrl_episodes ep, int num_envs, ckrl_grpo_options opt, ckrl_gr
     return;
   }
   while (cap < n) cap <<= 1;
-  const int capacity = big ? pow2_at_least(num_envs) : kGrpoMaxEligible;
+  const int capacity = big ? pow2_at_least(num_envs) : scap;
   unsigned char* sort_base = big ? reinterpret_cast<unsigned char*>(ws + L.grpo_sort) : smem;
   uint64_t* keys = reinterpret_cast<uint64_t*>(sort_base);
   int32_t* idx = reinterpret_cast<int32_t*>(keys + capacity);
@@ -508,11 +512,13 @@ cudaError_t launch_normalize(const ckrl_rollout& ro, int action_level, const uin
 cudaError_t launch_grpo_assemble(const ckrl_rollout& ro, const ckrl_episodes& ep,
                                  const ckrl_grpo_options& opt, ckrl_grpo_batch& gb, char* ws,
                                  const WsLayout& L, cudaStream_t s, const ExchangeView& ex) {
-  size_t smem = (size_t)kGrpoMaxEligible * 16 + sizeof(int32_t) * (kGrpoMaxEligible + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(grpo_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  const int scap = std::min(kGrpoMaxEligible, pow2_at_least(ro.num_envs < 1 ? 1 : ro.num_envs));
+  const size_t smem = (size_t)scap * 16 + sizeof(int32_t) * (scap + 1);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(grpo_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)kGrpoMaxEligible * 16 + sizeof(int32_t) * (kGrpoMaxEligible + 1)));
+    attr = (size_t)kGrpoMaxEligible * 16 + sizeof(int32_t) * (kGrpoMaxEligible + 1);
   }
   grpo_group_kernel<<<1, kGrpoThreads, smem, s>>>(ep, ro.num_envs, opt, gb, ws, L, ex);
   cudaError_t err = cudaGetLastError();
