@@ -1052,7 +1052,9 @@ def e2e_timing(args, cfg, rep, step, run, R, dev, world):
     """Same metric through the public API with host buffers: every step copies that step's
     inputs host->device from pinned memory — the logits as one copy, every other input packed
     into one pinned staging buffer and copied at once (the step then reads device views of the
-    packed block) — runs the step and reads the loss back."""
+    packed block) — runs the step and reads the loss back. The device inputs are double
+    buffered: step i+1's copies run on a copy stream while step i computes (each slot is
+    overwritten only after the step that read it has finished), so the host link stays busy."""
     import dataclasses
     import torch
     from paper_2510_06710_b200.core import EpisodeTable, PolicyOutputs, RolloutBuffer
@@ -1061,10 +1063,7 @@ def e2e_timing(args, cfg, rep, step, run, R, dev, world):
     small.append(("pol", "values", pol.values))
     if ept is not None:
         small += [("ept", f.name, getattr(ept, f.name)) for f in dataclasses.fields(EpisodeTable)]
-    views = {"ro": {}, "pol": {}, "ept": {}}
-    for owner, name, t in small:
-        if t is None:
-            views[owner][name] = None
+    nones = [(owner, name) for owner, name, t in small if t is None]
     small = [x for x in small if x[2] is not None]
     off, layout = 0, []
     for owner, name, t in small:
@@ -1072,36 +1071,64 @@ def e2e_timing(args, cfg, rep, step, run, R, dev, world):
         layout.append((owner, name, t, off, nb))
         off = (off + nb + 255) // 256 * 256
     host_pack = torch.zeros(max(off, 1), dtype=torch.uint8).pin_memory()
-    dev_pack = torch.empty(max(off, 1), dtype=torch.uint8, device=dev)
     for owner, name, t, o, nb in layout:
         host_pack[o:o + nb].copy_(t.detach().contiguous().view(-1).view(torch.uint8).cpu())
-        views[owner][name] = dev_pack[o:o + nb].view(t.dtype).view(t.shape)
-    ro_e = RolloutBuffer(**views["ro"], vocab=ro.vocab)
-    pol_e = PolicyOutputs(torch.empty_like(pol.logits), views["pol"]["values"])
-    ept_e = EpisodeTable(**views["ept"]) if ept is not None else None
     host_logits = pol.logits.detach().cpu().pin_memory()
+    slots = []
+    for _ in range(2):
+        dev_pack = torch.empty(max(off, 1), dtype=torch.uint8, device=dev)
+        views = {"ro": {}, "pol": {}, "ept": {}}
+        for owner, name in nones:
+            views[owner][name] = None
+        for owner, name, t, o, nb in layout:
+            views[owner][name] = dev_pack[o:o + nb].view(t.dtype).view(t.shape)
+        slots.append({
+            "pack": dev_pack,
+            "ro": RolloutBuffer(**views["ro"], vocab=ro.vocab),
+            "pol": PolicyOutputs(torch.empty_like(pol.logits), views["pol"]["values"]),
+            "ept": EpisodeTable(**views["ept"]) if ept is not None else None,
+            "out": torch.empty(8, dtype=torch.float64).pin_memory(),
+            "ready": torch.cuda.Event(), "free": torch.cuda.Event(),
+        })
     h2d = host_pack.numel() + host_logits.numel() * host_logits.element_size()
-    out = torch.empty(8, dtype=torch.float64).pin_memory()
-    d2h = out.numel() * out.element_size()
+    d2h = slots[0]["out"].numel() * slots[0]["out"].element_size()
     stream = torch.cuda.current_stream()
+    cs = torch.cuda.Stream(device=dev)
     n = max(5, min(args.steps, 30))
 
-    def one():
-        pol_e.logits.copy_(host_logits, non_blocking=True)
-        dev_pack.copy_(host_pack, non_blocking=True)
-        if ept_e is None:
-            step(ro_e, pol_e)
-        else:
-            step(ro_e, ept_e, pol_e)
-        out.copy_(step.diag, non_blocking=True)
+    def copy_in(i):
+        sl = slots[i % 2]
+        with torch.cuda.stream(cs):
+            if i >= 2:
+                cs.wait_event(sl["free"])  # step i-2 has finished reading this slot
+            sl["pol"].logits.copy_(host_logits, non_blocking=True)
+            sl["pack"].copy_(host_pack, non_blocking=True)
+            sl["ready"].record(cs)
 
-    for _ in range(2):
-        one()
+    def compute(i):
+        sl = slots[i % 2]
+        stream.wait_event(sl["ready"])
+        if sl["ept"] is None:
+            step(sl["ro"], sl["pol"])
+        else:
+            step(sl["ro"], sl["ept"], sl["pol"])
+        sl["free"].record(stream)
+        sl["out"].copy_(step.diag, non_blocking=True)
+
+    def run_steps(count, start_ev=None):
+        if start_ev is not None:
+            cs.wait_event(start_ev)
+        copy_in(0)
+        for i in range(count):
+            if i + 1 < count:
+                copy_in(i + 1)  # overlaps step i on the copy stream
+            compute(i)
+
+    run_steps(2)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(n):
-        one()
+    run_steps(n, e0)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
@@ -1112,7 +1139,8 @@ def e2e_timing(args, cfg, rep, step, run, R, dev, world):
     return {"value": world * env_steps(cfg) / (ms * 1e-3), "unit": "env-steps/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
             "h2d_gbs": h2d_gbs, "host_link_gbs": link, "host_link_frac": h2d_gbs / link,
-            "h2d_copies_per_step": 2, "device_frac": None}
+            "h2d_copies_per_step": 2, "input_buffers": "double (copy stream overlaps the previous step)",
+            "device_frac": None}
 
 if __name__ == "__main__":
     launch()
