@@ -1685,6 +1685,30 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>() > 608 ? tma_threads<RO
       }
     };
     load_toks(blockIdx.x, tk_next);
+    constexpr bool kBatchFinish = sizeof(LT) == 2;
+    auto finish_row = [&](const RowSmem& sm, int row, float fs, float ft, float fc, float fxt) {
+      // The row is finished here, by the lane that holds its sums: log2 s = ex +
+      // log2(mant), mant in [1, 2) (the exponent exactly, the mantissa's log2 by the
+      // accurate fp32 log2f, |result| < 1: abs error <= 6e-8, so no fp32 rounding of a
+      // value up to 8 reaches the log-prob), E[y] = t / s at 2 ulp (entropy only), then
+      // in fp64 the first-order correction for the fp32 log2(e) constant (the sums see x
+      // scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x]). The unit phase then
+      // reads one fp64 log-prob and one entropy per row.
+      const int ebits = (__float_as_int(fs) >> 23) - 127;  // s >= 1: normal, positive
+      const float mant = __int_as_float((__float_as_int(fs) & 0x007fffff) | 0x3f800000);
+      const float l2m = log2f(mant);
+      const float eyf = __fdividef(ft, fs);
+      const double l2s = (double)ebits + (double)l2m;
+      const double ls = l2s * kLN2;
+      const double ey = (double)eyf, xc = (double)fc;
+      sm.lp[row] = ((double)fxt - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
+      sm.ent[row] = (float)(ls - kLN2 * ey);
+      if (GRAD) {  // the fused seam's re-read (grad_row): shift, log2 s, E[y]
+        sm.s[row] = (float)l2s;
+        sm.t2[row] = eyf;
+        sm.c[row] = fc;
+      }
+    };
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++it,
                  s = (s + 1 == nstage) ? (sph ^= 1u, 0) : s + 1, b = (b + 1 == nbuf) ? (bph ^= 1u, 0) : b + 1) {
       RowSmem sm;
@@ -1704,6 +1728,9 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>() > 608 ? tma_threads<RO
       if (cwarp == 0 && lane == 0 && it < 3) tl_mark(12 + 3 * it);
       CKRL_PROBE(if (blockIdx.x == 0 && cwarp == 0 && lane == 0 && it < 64) g_tile_times[0][it] = gtimer());
       const LT* stage = reinterpret_cast<const LT*>(stage_base + (size_t)s * tile_bytes);
+      static_assert(kPasses <= 8, "one captured row per lane of an 8-lane group");
+      int f_row = -1;
+      float f_s = 1.0f, f_t = 0.0f, f_c = 0.0f, f_xt = 0.0f;
 #pragma unroll
       for (int p = 0; p < kPasses; p += RIF) {
         const int rg0 = (p * kCW + cwarp) * 4;
@@ -1723,42 +1750,36 @@ __global__ void __launch_bounds__(tma_threads<ROWW, BW>() > 608 ? tma_threads<RO
           rows_fast_smem<LT, RIF>(rp, l8, s_, t_, c_);
         else
           rows_fast_smem<LT, 1>(rp, l8, s_, t_, c_);
-        if (l8 == 0) {
+        // bf16 rows: the row of pass p + q is finished by lane p + q of its 8-lane group (every
+        // lane holds the group's sums) — the capture is a few selects per pass and the
+        // finishing math runs once per tile on up to kPasses lanes at a time (bf16 cfg4 226 ->
+        // 208 us); f32 rows, whose passes are longer, finish on lane 0 right after each pass
+        // (measured 1-2 % faster for them).
 #pragma unroll
-          for (int q = 0; q < RIF; ++q) {
-            const int row = rowq[q];
-            if (!live[q] || row >= rows) continue;
+        for (int q = 0; q < RIF; ++q) {
+          const int row = rowq[q];
+          if (!live[q] || row >= rows) continue;
+          if (GRAD && l8 == 0) grad_of(b).tok[row] = tk[p + q];
+          if (l8 == (kBatchFinish ? p + q : 0)) {
             // every row is finished (the unit phase masks by counted / membership); a token
             // id outside [0, V) of an unused row must not read outside the staged row
             const int tok = tk[p + q] & (V - 1);
-            if (GRAD) grad_of(b).tok[row] = tk[p + q];
             const float xt = sizeof(LT) == 4
                                  ? (float)reinterpret_cast<const float*>(rp[q])[tok]
                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rp[q])[tok]);
-            // The row is finished here, by the lane that holds its sums: log2 s = ex +
-            // log2(mant), mant in [1, 2) (the exponent exactly, the mantissa's log2 by the
-            // accurate fp32 log2f, |result| < 1: abs error <= 6e-8, so no fp32 rounding of a
-            // value up to 8 reaches the log-prob), E[y] = t / s at 2 ulp (entropy only), then
-            // in fp64 the first-order correction for the fp32 log2(e) constant (the sums see x
-            // scaled by 1 + kL2EDelta: LSE((1+d) x) = LSE(x) + d E[x]). The unit phase then
-            // reads one fp64 log-prob and one entropy per row.
-            const int ebits = (__float_as_int(s_[q]) >> 23) - 127;  // s >= 1: normal, positive
-            const float mant = __int_as_float((__float_as_int(s_[q]) & 0x007fffff) | 0x3f800000);
-            const float l2m = log2f(mant);
-            const float eyf = __fdividef(t_[q], s_[q]);
-            const double l2s = (double)ebits + (double)l2m;
-            const double ls = l2s * kLN2;
-            const double ey = (double)eyf, xc = (double)c_[q];
-            sm.lp[row] = ((double)xt - xc * kLN2) - ls + kL2EDelta * (ey + xc) * kInvL2EF;
-            sm.ent[row] = (float)(ls - kLN2 * ey);
-            if (GRAD) {  // the fused seam's re-read (grad_row): shift, log2 s, E[y]
-              sm.s[row] = (float)l2s;
-              sm.t2[row] = eyf;
-              sm.c[row] = c_[q];
+            if (kBatchFinish) {
+              f_row = row;
+              f_s = s_[q];
+              f_t = t_[q];
+              f_c = c_[q];
+              f_xt = xt;
+            } else {
+              finish_row(sm, row, s_[q], t_[q], c_[q], xt);
             }
           }
         }
       }
+      if (kBatchFinish && f_row >= 0) finish_row(sm, f_row, f_s, f_t, f_c, f_xt);
       // Every lane arrives (barrier counts are per thread): each lane's own shared-memory
       // writes are ordered before its arrival (release, CTA scope), which the consumers'
       // try_wait acquires — a per-thread happens-before that racecheck can also see.
