@@ -912,7 +912,10 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
 template <typename LT, int R>
 __device__ __forceinline__ void rows_fast_smem(const LT* const* rowp, int l8, float* s_out,
                                                float* t_out, float* c_out) {
-  uint64_t x[R][16];
+  // f32: the row as 16 packed (even, odd) pairs; bf16: the 16 raw words (two bf16 each),
+  // widened only where the exponent loop consumes them (16 live registers per row, not 32)
+  uint64_t x[R][sizeof(LT) == 4 ? 16 : 1];
+  uint32_t wr[R][sizeof(LT) == 2 ? 16 : 1];
   float m[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -956,7 +959,7 @@ __device__ __forceinline__ void rows_fast_smem(const LT* const* rowp, int l8, fl
         for (int i = 0; i < k; ++i) mw[i] = bmax2(mw[i], mw[i + k]);
       m[r] = fmaxf(bf16_lo(mw[0]), bf16_hi(mw[0]));
 #pragma unroll
-      for (int i = 0; i < 16; ++i) x[r][i] = f2pack(bf16_lo(w[i]), bf16_hi(w[i]));
+      for (int i = 0; i < 16; ++i) wr[r][i] = w[i];
     }
   }
 #pragma unroll
@@ -976,7 +979,12 @@ __device__ __forceinline__ void rows_fast_smem(const LT* const* rowp, int l8, fl
   for (int i = 0; i < 16; ++i)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint64_t y = ffma2(x[r][i], l2e, nc[r]);
+      uint64_t xi;
+      if constexpr (sizeof(LT) == 4)
+        xi = x[r][i];
+      else
+        xi = f2pack(bf16_lo(wr[r][i]), bf16_hi(wr[r][i]));
+      const uint64_t y = ffma2(xi, l2e, nc[r]);
       float y0, y1;
       f2unpack(y, y0, y1);
       const uint64_t e = f2pack(ex2(y0), ex2(y1));
