@@ -12,8 +12,15 @@ truncation at max_episode_steps, and the three rollout modes of harness/config.c
   mask           auto_reset off: frozen until the rollout ends
   fixed length   ignore_terminations: only truncations end episodes
 
-Structural arrays are built with numpy (vectorised over envs, looping over time); the
-large per-token tensors (logits, old log-probs) are drawn directly on the device.
+Every draw comes from the reference's generator, chunkrl::Rng (core/rng.hpp:11-57: splitmix64,
+next_double = (u64 >> 11) * 2^-53, next_below = u64 % n, next_normal = Box-Muller on two
+doubles), with per-purpose seeds from its mix_seed (rng.hpp:60-65). splitmix64 is a counter
+generator — the k-th draw of a stream is mix(seed + k * gamma) — so a stream of n draws is
+vectorised (`Rng`, numpy, host) or generated on the device (`_device_draws`, torch int64
+arithmetic) with the same values, and a rank's shard of the per-token tensors skips to its
+offset in the full-batch stream (shard r's logits are rows of the full batch's). Structural
+arrays are built with numpy (vectorised over envs, looping over time); the large per-token
+tensors (logits, tokens, old log-probs) are drawn directly on the device.
 """
 from __future__ import annotations
 
@@ -23,6 +30,83 @@ import numpy as np
 import torch
 
 TERM, TRUNC, VALID = 1, 2, 4
+
+_U64 = (1 << 64) - 1
+_GAMMA = 0x9E3779B97F4A7C15
+_M1, _M2 = 0xBF58476D1CE4E5B9, 0x94D049BB133111EB
+
+
+def _mix_np(z):
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(_M1)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(_M2)
+    return z ^ (z >> np.uint64(31))
+
+
+def mix_seed(a: int, b: int) -> int:
+    """chunkrl::mix_seed (core/rng.hpp:60-65)."""
+    z = np.array([(a + _GAMMA * (b + 1)) & _U64], dtype=np.uint64)
+    return int(_mix_np(z)[0])
+
+
+class Rng:
+    """chunkrl::Rng (core/rng.hpp:11-57), n draws of the sequential stream at a time."""
+
+    def __init__(self, seed: int):
+        self.state = seed & _U64
+        self.u64(2)  # the constructor's two decorrelating draws
+
+    def u64(self, n: int) -> np.ndarray:
+        k = np.arange(1, n + 1, dtype=np.uint64)
+        z = np.uint64(self.state) + k * np.uint64(_GAMMA)  # wraps mod 2^64
+        self.state = (self.state + n * _GAMMA) & _U64
+        return _mix_np(z)
+
+    def double(self, n: int) -> np.ndarray:
+        return (self.u64(n) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+    def below(self, n: int, bound: int) -> np.ndarray:
+        return (self.u64(n) % np.uint64(bound)).astype(np.int64)
+
+    def normal(self, n: int) -> np.ndarray:
+        d = self.double(2 * n)
+        u1, u2 = d[0::2], d[1::2]
+        # next_normal redraws u1 == 0 (probability 2^-53 per draw); a vectorised stream cannot
+        # shift its later positions, so such a seed is rejected instead
+        if not np.all(u1 > 0.0):
+            raise ValueError("Rng.normal: u1 == 0 drawn; pick another seed")
+        return np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586476925287 * u2)
+
+
+def _as_i64(u: int) -> int:
+    return u - (1 << 64) if u >= (1 << 63) else u
+
+
+def _srl(z: torch.Tensor, k: int) -> torch.Tensor:
+    """Logical right shift of int64-held uint64 bits."""
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def _device_draws(seed: int, first: int, n: int, device) -> torch.Tensor:
+    """u64 draws first+1 .. first+n (1-based after the constructor's two) of Rng(seed), as
+    int64 bit patterns on `device` (int64 multiplies wrap mod 2^64 like the uint64 ones)."""
+    k = torch.arange(first + 3, first + n + 3, dtype=torch.int64, device=device)
+    z = k * _as_i64(_GAMMA) + _as_i64(seed & _U64)
+    z = (z ^ _srl(z, 30)) * _as_i64(_M1)
+    z = (z ^ _srl(z, 27)) * _as_i64(_M2)
+    return z ^ _srl(z, 31)
+
+
+def _device_doubles(seed, first, n, device):
+    return _srl(_device_draws(seed, first, n, device), 11).to(torch.float64) * 2.0 ** -53
+
+
+def _device_normals(seed: int, first: int, n: int, device) -> torch.Tensor:
+    """next_normal draws first .. first+n-1 of Rng(seed) (two doubles each), f64."""
+    d = _device_doubles(seed, 2 * first, 2 * n, device).view(n, 2)
+    u1, u2 = d[:, 0], d[:, 1]
+    if not bool((u1 > 0.0).all()):
+        raise ValueError("next_normal: u1 == 0 drawn; pick another seed")
+    return torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(6.283185307179586476925287 * u2)
 
 
 @dataclass
@@ -60,7 +144,7 @@ def episodes_numpy(cfg: SynthConfig, env_offset: int = 0) -> dict:
     """Structural SoA arrays + episode table (numpy, host)."""
     E, Tc, C = cfg.num_envs, cfg.num_chunks, cfg.chunk_len
     T = Tc * C
-    rng = np.random.default_rng(cfg.seed * 1_000_003 + env_offset)
+    rng = Rng(mix_seed(cfg.seed, 1_000_003 + env_offset))
     reward = np.zeros((E, T), np.float64)
     flags = np.zeros((E, T), np.uint8)
     epi = np.full((E, T), -1, np.int32)
@@ -73,7 +157,8 @@ def episodes_numpy(cfg: SynthConfig, env_offset: int = 0) -> dict:
     frozen = np.zeros(E, bool)
     latched = np.zeros(E, np.uint8)
     # GRPO: success step per (env, episode) drawn lazily at episode start
-    succ_at = np.where(rng.random(E) < cfg.p_success, rng.integers(0, T, E), -1)
+    p_draw = rng.double(E)
+    succ_at = np.where(p_draw < cfg.p_success, rng.below(E, T), -1)
     table = []
 
     def close(e, complete):
@@ -99,8 +184,8 @@ def episodes_numpy(cfg: SynthConfig, env_offset: int = 0) -> dict:
         ae = np.nonzero(act)[0]
         epi[ae, t] = ep_idx[ae]
         if cfg.algo == "ppo":
-            r = rng.standard_normal(len(ae))
-            term = rng.random(len(ae)) < cfg.p_terminate
+            r = rng.normal(len(ae))
+            term = rng.double(len(ae)) < cfg.p_terminate
         else:
             hit = (succ_at[ae] == t)
             r = hit.astype(np.float64)
@@ -143,25 +228,36 @@ def episodes_numpy(cfg: SynthConfig, env_offset: int = 0) -> dict:
     out["ep_task"] = np.zeros(n, np.int32)
     # unique reset id per group of G envs: groups never merge by key
     out["ep_reset_id"] = (out["ep_env_id"] // cfg.group_size).astype(np.int32)
-    out["value_scalar"] = rng.standard_normal((E, Tc))
-    out["value_vector"] = rng.standard_normal((E, Tc, C))
-    out["boot_scalar"] = rng.standard_normal((E, Tc, C))
-    out["boot_vector0"] = rng.standard_normal((E, Tc, C))
-    out["new_value_scalar"] = rng.standard_normal((E, Tc))
-    out["new_value_vector"] = rng.standard_normal((E, Tc, C))
+    out["value_scalar"] = rng.normal(int(np.prod((E, Tc)))).reshape((E, Tc))
+    out["value_vector"] = rng.normal(int(np.prod((E, Tc, C)))).reshape((E, Tc, C))
+    out["boot_scalar"] = rng.normal(int(np.prod((E, Tc, C)))).reshape((E, Tc, C))
+    out["boot_vector0"] = rng.normal(int(np.prod((E, Tc, C)))).reshape((E, Tc, C))
+    out["new_value_scalar"] = rng.normal(int(np.prod((E, Tc)))).reshape((E, Tc))
+    out["new_value_vector"] = rng.normal(int(np.prod((E, Tc, C)))).reshape((E, Tc, C))
     return out
 
 
 def token_tensors(cfg: SynthConfig, device="cuda", dtype=torch.float32, env_offset: int = 0):
     """Logits ~ N(0, logit_std^2), tokens ~ U[0, V), old log-probs = current log-prob of the
-    token + N(0, old_lp_noise^2) so ratios straddle the clip band. Drawn on `device`."""
+    token + N(0, old_lp_noise^2) so ratios straddle the clip band. Drawn on `device` from three
+    reference Rng streams (mix_seed(seed, 5 / 6 / 7)); env_offset skips each stream to the
+    shard's first env, so a shard's tensors are the full batch's rows."""
     E, Tc, C, M, V = cfg.num_envs, cfg.num_chunks, cfg.chunk_len, cfg.tokens_per_action, cfg.vocab
-    g = torch.Generator(device=device)
-    g.manual_seed(cfg.seed * 7919 + 5 + env_offset)
+    per_env = Tc * C * M
+    s_logit, s_tok, s_noise = (mix_seed(cfg.seed, k) for k in (5, 6, 7))
     logits = torch.empty((E, Tc, C, M, V), dtype=torch.float32, device=device)
-    logits.normal_(0.0, cfg.logit_std, generator=g)
+    flat = logits.view(-1)
+    first = env_offset * per_env * V
+    step = 1 << 24
+    for i in range(0, flat.numel(), step):
+        n = min(step, flat.numel() - i)
+        flat[i:i + n] = (_device_normals(s_logit, first + i, n, device) * cfg.logit_std).float()
     logits = logits.to(dtype)
-    tokens = torch.randint(0, V, (E, Tc, C, M), generator=g, device=device, dtype=torch.int64)
+    n_tok = E * per_env
+    u = _device_draws(s_tok, env_offset * per_env, n_tok, device)
+    # next_below(V) = u64 % V as unsigned arithmetic: ((u >> 1) % V * 2 + (u & 1)) % V
+    tokens = ((_srl(u, 1) % V) * 2 + (u & 1)) % V
+    tokens = tokens.view(E, Tc, C, M)
     # old log-prob from the (possibly bf16-rounded) logits, chunked to bound memory
     lp = torch.empty((E, Tc, C, M), dtype=torch.float32, device=device)
     flat_l = logits.view(-1, V)
@@ -171,7 +267,7 @@ def token_tensors(cfg: SynthConfig, device="cuda", dtype=torch.float32, env_offs
     for i in range(0, flat_t.numel(), step):
         ls = torch.log_softmax(flat_l[i:i + step].double(), dim=-1)
         flat_o[i:i + step] = ls.gather(1, flat_t[i:i + step, None]).squeeze(1).float()
-    noise = torch.empty_like(lp).normal_(0.0, cfg.old_lp_noise, generator=g)
+    noise = (_device_normals(s_noise, env_offset * per_env, n_tok, device) * cfg.old_lp_noise).float().view_as(lp)
     old_lp = lp + noise
     tok_dtype = torch.uint8 if V <= 256 else torch.int32
     return logits, tokens.to(tok_dtype), old_lp
