@@ -9,7 +9,7 @@ import bench  # noqa: E402
 from paper_2510_06710_b200.pipeline import RolloutPipeline, random_params  # noqa: E402
 
 sampler = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-for E in (64, 148, 256, 296, 444, 592):
+for E in (32, 64, 128, 148, 256, 296, 444, 592):
     env, pol = bench.cfg5_specs(E, seed=3)
     params = random_params(pol, seed=7, device="cuda")
     pipe = RolloutPipeline(env, pol, bench.CFG5["num_chunks"], stages=1, sampler=sampler, keep_logits=False)
