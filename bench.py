@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--head", type=int, default=0,
                    help="row N2: feed the step from trunk features of this width H through the "
                         "tcgen05 policy-head projection (ckrl_project_token_stats) instead of logits")
-    p.add_argument("--loss-streams", type=int, default=2,
+    p.add_argument("--loss-streams", type=int, default=3,
                    help="pipelined steps: alternate the losses over this many streams")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)

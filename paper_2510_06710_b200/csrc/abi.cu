@@ -581,8 +581,9 @@ static int chain_enabled() {
 // Launch policy of the pipelined halves' losses (ckrl_*_step_loss; the callers alternate them
 // over two streams, optim.Pipelined). Measured per step on B200:
 //  * grid cap: consecutive losses run side by side on disjoint SMs when each leaves SMs free.
-//    PPO launches of 8..32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 26.8 us, cfg3
-//    bf16 27.2 -> 22.6 us, with the 14-row-warp CTA, csrc/loss.cu), below 8 a quarter (cfg1
+//    PPO launches of 12..32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 26.8 us, with
+//    the 14-row-warp CTA, csrc/loss.cu), 8..12 a third (cfg3 bf16 21.0 -> 19.2 us with the
+//    losses over 3 streams; roughly 27-30 tiles per CTA in both bands), below 8 a quarter (cfg1
 //    14.7 -> 10.8 us); GRPO losses leave 6 SMs free, where the next
 //    batch's single-CTA (1024-thread) group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
 //    long PPO launches keep one CTA per SM.
@@ -621,6 +622,7 @@ static int pipelined_cap(const ckrl_rollout* ro, const ckrl_policy_outputs* po, 
     const double t = tiles_per_sm(ro, po);
     if (grpo) want = sms - 6;
     else if (t < 8.0) want = sms / 4;  // tiny launches: a quarter (cfg1 12.7 -> 12.3 us)
+    else if (t < 12.0) want = sms / 3;  // cfg3 bf16 (9 tiles / SM), 3 loss streams: 21.0 -> 19.2 us
     else if (t <= 32.0) want = (sms * 3) / 5;
   }
   if (want <= 0) return cap;

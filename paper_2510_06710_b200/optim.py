@@ -227,11 +227,12 @@ class Pipelined:
     current stream (graph-capturable); batch i uses steps[i % len(steps)] and
     args_of(i) -> (assemble args, loss args)."""
 
-    def __init__(self, steps, loss_streams: int = 2):
+    def __init__(self, steps, loss_streams: int = 3):
         """loss_streams = n > 1 rotates the losses over the current stream and n - 1 more, so
         batch i+1's loss depends only on its own assembly (not on batch i's loss): its CTAs
         start and run their unit phases while batch i's last CTAs finish (with the library's
-        capped loss grids, side by side on disjoint SMs)."""
+        capped loss grids, side by side on disjoint SMs). Default 3: measured 1-3 % faster than 2
+        for cfg3 / cfg2 and 10 % for cfg3 bf16 (with the 8..12-tiles-per-SM grid cap)."""
         import torch
         self.steps = steps
         self.alts = [torch.cuda.Stream() for _ in range(max(1, loss_streams) - 1)]
