@@ -19,7 +19,7 @@ for h in 4096 1024; do
 done
 timeout 300 python bench.py --config adam --steps 20 >> $O 2>/dev/null
 timeout 600 python bench.py --config cfg5 --steps 10 --warmup 3 >> $O 2>/dev/null
-for c in cfg3 cfg2 cfg4; do
+for c in cfg3 cfg2 cfg4 cfg5; do
   timeout 300 python bench.py --impl reference --config $c --steps 3 --warmup 1 >> $O 2>/dev/null
 done
 wc -l $O
