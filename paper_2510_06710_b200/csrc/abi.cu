@@ -584,7 +584,8 @@ static int chain_enabled() {
 //    PPO launches of 12..32 56-KB tiles per SM use 60 % of the SMs (cfg3 33.1 -> 26.8 us, with
 //    the 14-row-warp CTA, csrc/loss.cu), 8..12 a third (cfg3 bf16 21.0 -> 19.2 us with the
 //    losses over 3 streams; roughly 27-30 tiles per CTA in both bands), below 8 a quarter (cfg1
-//    14.7 -> 10.8 us); GRPO losses leave 6 SMs free, where the next
+//    14.7 -> 10.8 us); GRPO losses of 8..12 tiles per SM use 3/7 of the SMs (cfg2 bf16 22.3 ->
+//    20.8 us), other GRPO losses leave 6 SMs free, where the next
 //    batch's single-CTA (1024-thread) group kernel runs (cfg2 32.9 -> 26.7 us, cfg4 bf16 241 -> 228 us);
 //    long PPO launches keep one CTA per SM.
 //  * chaining (programmatic dependent launch of the previous loss on the stream): on, except
@@ -620,7 +621,7 @@ static int pipelined_cap(const ckrl_rollout* ro, const ckrl_policy_outputs* po, 
   } else if (po->logits_dtype != CKRL_DTYPE_TOKEN_ROWS) {
     const int sms = device_sm_count();
     const double t = tiles_per_sm(ro, po);
-    if (grpo) want = sms - 6;
+    if (grpo) want = (t >= 8.0 && t < 12.0) ? (sms * 3) / 7 : sms - 6;  // cfg2 bf16: 22.3 -> 20.8 us
     else if (t < 8.0) want = sms / 4;  // tiny launches: a quarter (cfg1 12.7 -> 12.3 us)
     else if (t < 12.0) want = sms / 3;  // cfg3 bf16 (9 tiles / SM), 3 loss streams: 21.0 -> 19.2 us
     else if (t <= 32.0) want = (sms * 3) / 5;
