@@ -729,7 +729,9 @@ def bench_head(args, rank, world, local):
         inner = optim.PpoStep(ro, GaeParams(0.99, 0.95), spec, PpoParams(0.2, 0.5, 0.01, True))
         reps.append((ro, pol))
         steps.append(HeadStep(inner, feat, tokens, rows))
-    pipe = optim.Pipelined(steps)
+    # two loss streams: the projection fills the SMs, so a third stream only adds contention
+    # (H = 4096: 263 vs 280 us per step, end of round 2)
+    pipe = optim.Pipelined(steps, loss_streams=2)
     args_of = lambda i: ((reps[i % R][0],), reps[i % R])  # noqa: E731
     stream = torch.cuda.current_stream()
     pipe.issue(max(3, args.warmup), args_of)
